@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""Benchmark: gate applications/s on the BASELINE.json hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N=1 workload = BASELINE.json configs[1]: random layer circuit, n=26
+complex128, 200 layers x (26 one-qubit gates + 13 CNOTs) = 7,800 gate
+applications per step, from |0...0>, on one B200.  A step resets the 1 GiB
+state (> 126 MB L2, so no L2 flush is needed) and applies the whole circuit.
+
+N>1 (torchrun, one process per GPU): weak scaling over the partitioned
+engine -- n = 26 + log2(N) qubits, k = log2(N) global qubits, so every GPU
+holds a 2^26-amplitude slab and CNOTs touching a global qubit exchange with
+the partner rank (paper_1801_01037_b200.dist).
+
+Extra keys on the one JSON line:
+  roofline      dominant kernel's algorithmic bytes / its CUDA-event time
+                (libsvb's in-library event profiler, on the launch stream,
+                over the timed region) vs MEASURED_PEAKS.json hbm_gbs;
+  cpu_baseline  the reference's own compiled kernel (oracle/_ref, built
+                from /root/reference by build()) on all host cores, over a
+                bounded prefix of the same circuit;
+  e2e           same metric through the public host-memory call
+                device.simulate (pinned H2D + run + D2H per step);
+  local_gate_sweep  BASELINE configs[2]: n=30, one Haar U per target
+                t=0..29 x 10 reps, per-target HBM GB/s (one launch per
+                application, no fusion);
+  clocks        nvidia-smi samples during the timed region.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+N_QUBITS = 26
+LAYERS = 200
+SWEEP_N = 30
+SWEEP_REPS = 10
+METRIC = "gate applications/s"
+UNIT = "gate_apps/s"
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def peaks() -> tuple[float, str]:
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ("sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle/ is the checker and the CPU baseline; never the product)
+
+
+def cpu_reference_rate(circuit, budget_s: float, cores: int) -> dict:
+    """The reference's compiled kernel (oracle/_ref, else the C port) on the
+    host over a bounded prefix of `circuit`, mode parallel_collapsed."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle
+
+    ref = oracle.ref_module()
+    kind = "reference" if ref is not None else "port"
+    amps = np.zeros(1 << circuit.n, np.complex128)
+    amps[0] = 1.0
+
+    def one(op):
+        g = op.gate
+        if ref is not None:
+            if op.control is None:
+                ref.apply_single(amps, g.q11, g.q12, g.q21, g.q22, op.target, 3, cores)
+            else:
+                ref.apply_controlled(amps, g.q11, g.q12, g.q21, g.q22, op.control, op.target, 3, cores)
+        else:
+            if op.control is None:
+                oracle.apply_single(amps, g, op.target, cores)
+            else:
+                oracle.apply_controlled(amps, g, op.control, op.target, cores)
+
+    done = 0
+    t0 = time.perf_counter()
+    for op in circuit.ops:
+        one(op)
+        done += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"first {done} of {len(circuit.ops)} ops of the n={circuit.n} random layer "
+                      f"circuit (configs[1]), {'svsim _stride_cy' if ref else 'oracle C port'} "
+                      f"mode parallel_collapsed x{cores}, {dt:.1f} s"}
+
+
+def run_reference_arm(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_1801_01037_b200 import workloads
+
+    n = N_QUBITS
+    circuit = workloads.random_layer_circuit(n, LAYERS)
+    cores = host_cores()
+    steps, warm = max(args.steps, 1), max(args.warmup, 0)
+    per_step = max(2.0, min(20.0, 150.0 / (steps + warm)))
+    for _ in range(warm):
+        cpu_reference_rate(circuit, per_step / 4, cores)
+    rates, samples = [], []
+    for _ in range(steps):
+        r = cpu_reference_rate(circuit, per_step, cores)
+        rates.append(r["value"])
+        samples.append(r)
+    value = float(np.mean(rates))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": steps, "warmup": warm,
+        "ms_per_step": 1e3 * len(circuit.ops) / value,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c128", "data": "synthetic (seeded, BASELINE configs[1])",
+        "config": {"workload": f"random layer circuit n={n}, {LAYERS} layers, 7800 ops (configs[1])",
+                   "n_qubits": n, "layers": LAYERS},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": samples[-1]["kind"],
+                         "sample": samples[-1]["sample"]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+
+def local_gate_sweep(n: int, reps: int, peak: float) -> dict:
+    """configs[2]: per-target HBM GB/s of single general-U applications."""
+    import torch
+
+    from paper_1801_01037_b200 import _lib, device, workloads
+
+    lib = _lib.load()
+    st = device.DeviceState.random(n, seed=workloads.SEED_STATE)
+    circ = workloads.sweep_ops(n, reps)
+    stream = torch.cuda.current_stream()
+    sp = device._stream_ptr()
+    bytes_per_app = 32 * (1 << n)
+    per_t = []
+    for t in range(n):
+        q = _lib.gate_array(circ.ops[t * reps].gate)
+        lib.svb_apply_1q(st.ptr, 1 << n, q, t, sp)  # warm
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            _lib.check(lib.svb_apply_1q(st.ptr, 1 << n, q, t, sp))
+        e1.record(stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        per_t.append(bytes_per_app / ms / 1e6)
+    nrm = device.norm2(st)
+    del st
+    torch.cuda.empty_cache()
+    arr = np.array(per_t)
+    return {"config": f"n={n}, Haar U on t=0..{n - 1} x {reps} reps (configs[2])",
+            "gbs_min": round(float(arr.min()), 1), "gbs_median": round(float(np.median(arr)), 1),
+            "gbs_max": round(float(arr.max()), 1),
+            "frac_min": round(float(arr.min()) / peak, 4), "frac_median": round(float(np.median(arr)) / peak, 4),
+            "apps_per_s_median": round(float(np.median(arr)) * 1e9 / bytes_per_app, 1),
+            "per_target_gbs": [round(float(x), 1) for x in arr],
+            "norm_after": nrm, "bytes_per_app": bytes_per_app}
+
+
+def run_gpu_arm(args) -> None:
+    import torch
+
+    from paper_1801_01037_b200 import _lib, device, workloads
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        from paper_1801_01037_b200 import dist
+
+        dist.bench_main(args)
+        return
+
+    lib = _lib.load()
+    torch.cuda.set_device(0)
+    n = N_QUBITS
+    circuit = workloads.random_layer_circuit(n, LAYERS)
+    nops = len(circuit.ops)
+    ops_arr, _ = _lib.ops_array(circuit.ops)
+    flags = 0 if args.no_fuse else _lib.RUN_FUSE
+    passes = device.plan_passes(n, circuit, fuse=not args.no_fuse)
+    st = device.DeviceState.zeros(n)
+    stream = torch.cuda.current_stream()
+    sp = device._stream_ptr()
+
+    def step():
+        st.amps.zero_()
+        st.amps[0] = 1.0
+        _lib.check(lib.svb_run_ops(st.ptr, 1 << n, ops_arr, nops, flags, sp), "run_ops")
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    _lib.profile_enable(True)
+    launches0 = _lib.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    launches = _lib.launch_count() - launches0
+    prof = _lib.profile_read()
+    _lib.profile_enable(False)
+    norm_after = device.norm2(st)
+    value = nops * args.steps / (ms / 1e3)
+
+    peak, peak_src = peaks()
+    dom = max(prof.items(), key=lambda kv: kv[1][1]) if prof else None
+    roofline = None
+    if dom:
+        name, (cnt, tms, nbytes) = dom
+        achieved = nbytes / (tms / 1e3) / 1e9
+        traffic = None
+        tpath = os.path.join(REPO, "profiles", "traffic.json")
+        if os.path.exists(tpath):
+            with open(tpath) as f:
+                traffic = json.load(f).get(name)
+        roofline = {"bound": "hbm", "kernel": name, "achieved": round(achieved, 1), "peak": peak,
+                    "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                    "alg_bytes_per_launch": nbytes // cnt, "avg_launch_ms": round(tms / cnt, 4),
+                    "launches": cnt, "share_of_step": round(tms / ms, 4), "peak_source": peak_src}
+    kernels = {k: {"launches": v[0], "ms": round(v[1], 3), "gbs": round(v[2] / (v[1] / 1e3) / 1e9, 1)}
+               for k, v in prof.items()}
+
+    # e2e through the public host-memory call, pinned buffers
+    pin_in = torch.zeros(1 << n, dtype=torch.complex128).pin_memory()
+    pin_in[0] = 1.0
+    pin_out = torch.empty(1 << n, dtype=torch.complex128).pin_memory()
+    a_in, a_out = pin_in.numpy(), pin_out.numpy()
+    e2e_steps = max(1, min(args.steps, 3))
+    device.simulate(circuit, a_in, fuse=not args.no_fuse, out=a_out)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        device.simulate(circuit, a_in, fuse=not args.no_fuse, out=a_out)
+    e2e_dt = time.perf_counter() - t0
+    e2e_norm = float(np.vdot(a_out, a_out).real)
+
+    sweep = None if args.no_sweep else local_gate_sweep(SWEEP_N, SWEEP_REPS, peak)
+
+    cores = host_cores()
+    cpu = None
+    if not args.no_cpu:
+        cpu = cpu_reference_rate(circuit, args.cpu_budget, cores)
+
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic (seeded numpy PCG64 circuit, |0...0> start)",
+        "config": {"workload": f"random layer circuit n={n}, {LAYERS} layers x ({n} 1q + {n // 2} CNOT) "
+                               f"= {nops} ops (BASELINE configs[1])",
+                   "n_qubits": n, "layers": LAYERS, "ops_per_step": nops, "fused": not args.no_fuse,
+                   "hbm_passes_per_step": passes, "state_bytes": 16 << n,
+                   "l2": "state 1 GiB > 126 MB L2; no flush needed", "parallelism": "single GPU"},
+        "roofline": roofline,
+        "kernels": kernels,
+        "gpu_launches": launches,
+        "e2e": {"value": round(nops * e2e_steps / e2e_dt, 1), "unit": UNIT,
+                "h2d_bytes_per_step": 16 << n, "d2h_bytes_per_step": 16 << n,
+                "api": "paper_1801_01037_b200.device.simulate (svb_host_run_ops), pinned host buffers",
+                "steps": e2e_steps},
+        "cpu_baseline": cpu,
+        "local_gate_sweep": sweep,
+        "clocks": clk.summary(),
+        "check": {"norm_after_step": norm_after, "e2e_norm": e2e_norm},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-fuse", action="store_true", help="one launch per gate")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the configs[2] n=30 sweep")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU reference work")
+    args = ap.parse_args(argv)
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,148 @@
+/*
+ * svb.h -- C ABI of the B200 state-vector gate engine (libsvb.so).
+ *
+ * Drop-in boundary for the reference package `svsim` (read-only at
+ * /root/reference/pkg).  Each entry point names the reference interface it
+ * replaces.  Plain pointers and sizes only: amplitude buffers are interleaved
+ * complex128 (re, im) -- numpy complex128 on the host, CUDA double2 on the
+ * device.  Gates cross as `const double q[8]` = re/im of q11, q12, q21, q22
+ * (svsim.core.Gate2x2, core.py:67-94).  Streams are `cudaStream_t` passed as
+ * `void*` (NULL = legacy default stream).
+ *
+ * Conventions: qubit i <-> index bit 2^i (core.py:3-9).  Return 0 on success,
+ * a negative SVB_E* code on failure; svb_last_error() gives the message of
+ * the calling thread's last failure.  The host layer maps SVB_EINVAL ->
+ * ValidationError, SVB_ENOMEM -> CapacityError, SVB_ESTATE ->
+ * ContractViolation, SVB_ECUDA/SVB_ENCCL -> SvsimError (errors.py:9-32).
+ *
+ * Arithmetic: every pair update is (q11*lo + q12*hi, q21*lo + q22*hi) with
+ * complex products (ac-bd, ad+bc) in round-to-nearest, no FMA -- the
+ * reference's compiled kernel built with -ffp-contract=off
+ * (_stride_cy.pyx:16-21, setup.py:46-48) -- so single-gate results are
+ * bit-identical to it (zeros may differ in sign only).
+ */
+#ifndef SVB_H
+#define SVB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SVB_OK 0
+#define SVB_EINVAL (-1)  /* bad argument                  -> ValidationError   */
+#define SVB_ENOMEM (-2)  /* allocation failed / too large -> CapacityError     */
+#define SVB_ECUDA (-3)   /* CUDA runtime error            -> SvsimError        */
+#define SVB_ENCCL (-4)   /* communication error           -> SvsimError        */
+#define SVB_ESTATE (-5)  /* call not allowed in state     -> ContractViolation */
+
+/* One circuit operation: svsim.core.GateOp (core.py:97-115).
+ * kind 0 = single (control ignored), 1 = controlled. */
+typedef struct svb_op {
+    int32_t kind;
+    int32_t target;
+    int32_t control;
+    int32_t reserved;
+    double q[8];
+} svb_op;
+
+/* svb_run_ops flags */
+#define SVB_RUN_FUSE 1u         /* plan multi-gate shared-memory passes        */
+#define SVB_RUN_STRICT_ORDER 2u /* fuse only contiguous runs (bit-exact order) */
+
+int svb_abi_version(void);
+const char *svb_last_error(void);
+/* Kernels launched by this library since load (all entry points). */
+int64_t svb_launch_count(void);
+
+/* Launch profiler: while enabled, every gate/exchange launch is bracketed by
+ * CUDA events on its own stream and aggregated per kernel class (0
+ * k_pair_high, 1 k_pair_low, 2 k_diag, 3 k_tiny, 4 k_fused, 5 k_exchange)
+ * with its algorithmic HBM bytes.  enable() resets the totals; read()
+ * synchronises on the recorded events. */
+int svb_profile_enable(int on);
+int svb_profile_read(int cls, int64_t *launches, double *total_ms, int64_t *alg_bytes);
+const char *svb_profile_class_name(int cls);
+
+/* ---- device buffers, stream-ordered (asynchronous) ---------------------- */
+
+/* Replaces svsim.kernel.apply_single (kernel/__init__.py:107-117) and the
+ * backend entry _stride_cy.apply_single (_stride_cy.pyx:24-54). */
+int svb_apply_1q(void *amps, int64_t n_amps, const double q[8], int target, void *stream);
+
+/* Replaces svsim.kernel.apply_controlled (kernel/__init__.py:120-134) and
+ * _stride_cy.apply_controlled (_stride_cy.pyx:57-90). */
+int svb_apply_c1q(void *amps, int64_t n_amps, const double q[8], int control, int target,
+                  void *stream);
+
+/* Applies ops[0..nops) in order -- the per-op loop of run_circuit for one
+ * rank (engine.py:483-494) -- optionally fusing gates into shared-memory
+ * passes (flags).  Results agree with op-by-op application within 1e-12;
+ * with SVB_RUN_STRICT_ORDER they are bit-identical. */
+int svb_run_ops(void *amps, int64_t n_amps, const svb_op *ops, int nops, unsigned flags,
+                void *stream);
+
+/* Number of HBM passes svb_run_ops would make for these ops (planner only,
+ * no device work). */
+int svb_plan_passes(int n_qubits, const svb_op *ops, int nops, unsigned flags, int *passes);
+
+/* sum |a_j|^2 -> *out (host).  Synchronises `stream`.  Replaces norm2
+ * (core.py:171-174) / _dist_norm2 for one slab (engine.py:453-454). */
+int svb_norm2(const void *amps, int64_t n_amps, double *out, void *stream);
+
+/* probs[j] = |a_j|^2 into a device buffer of n_amps doubles. */
+int svb_probs(const void *amps, int64_t n_amps, double *probs, void *stream);
+
+/* Own-row exchange update of the paper's single-amplitude protocol for one
+ * received chunk (engine.py:241-254 scheme b, 257-272 chunked): for
+ * j in [0, count): own[j] = own_is_low ? q11*own[j] + q12*other[j]
+ *                                      : q21*other[j] + q22*own[j],
+ * restricted to local indices (index_offset + j) with bit cbit set when
+ * cbit >= 0 (engine.py:199-203). */
+int svb_exchange_own_row(void *own, const void *other, int64_t count, const double q[8],
+                         int own_is_low, int cbit, int64_t index_offset, void *stream);
+
+/* Both rows for amplitude pairs held in two slabs (lo_slab[j], hi_slab[j]),
+ * j in [begin, end), masked by local bit cbit when cbit >= 0.  The fused
+ * peer-memory form of a global-target exchange (one side may be a peer
+ * device's memory).  Arithmetic identical to the own-row rule. */
+int svb_pair_update(void *lo_slab, void *hi_slab, int64_t begin, int64_t end, const double q[8],
+                    int cbit, void *stream);
+
+/* ---- host buffers, synchronous (the svsim kernel-backend contract) ------ */
+
+/* Backend-module contract apply_single(amps, q11, q12, q21, q22, target,
+ * mode, workers) (_stride_py.py:93-98; _stride_cy.pyx:24-25): in place on a
+ * host complex128 array; mode/workers are accepted and ignored. */
+int svb_host_apply_1q(double *host_amps, int64_t n_amps, const double q[8], int target);
+int svb_host_apply_c1q(double *host_amps, int64_t n_amps, const double q[8], int control,
+                       int target);
+/* Whole op list on host memory: H2D of host_in, svb_run_ops, D2H into
+ * host_out (may equal host_in).  Synchronous.  The end-to-end public call. */
+int svb_host_run_ops(const double *host_in, double *host_out, int64_t n_amps, const svb_op *ops,
+                     int nops, unsigned flags);
+
+/* ---- partitioned state over 2^k ranks (engine.py DistState) ------------- */
+
+typedef struct svb_dist svb_dist;
+
+/* n qubits over 2^k ranks; rank r's slab of 2^(n-k) amplitudes lives at
+ * slabs[r] on device devices[r] (ranks may share a device).  Peer access is
+ * enabled between distinct devices.  Does not take ownership of slabs. */
+int svb_dist_create(int n, int k, const int *devices, void *const *slabs, svb_dist **out);
+/* needs_comm(t) ? pairwise exchange : local sweep (engine.py:488-492). */
+int svb_dist_apply_1q(svb_dist *d, const double q[8], int target);
+/* The three controlled regimes (engine.py:415-450). */
+int svb_dist_apply_c1q(svb_dist *d, const double q[8], int control, int target);
+int svb_dist_norm2(svb_dist *d, double *out);
+/* Cumulative per-rank exchange accounting: amplitudes each rank read from
+ * and wrote to its partner's slab (peer traffic), and exchanges performed. */
+int svb_dist_stats(svb_dist *d, int64_t *exchanges, int64_t *peer_bytes_per_rank);
+int svb_dist_sync(svb_dist *d);
+int svb_dist_destroy(svb_dist *d);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SVB_H */

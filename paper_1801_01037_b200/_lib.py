@@ -1,0 +1,162 @@
+"""ctypes binding of libsvb.so (include/svb.h).
+
+This is exactly the stub a maintainer would add on the reference side
+(INTEGRATION.md): plain pointers, sizes and 8-double gate records.  There is
+no fallback -- if the library is missing or no CUDA device is visible, every
+compute entry point raises NativeLibraryMissing / SvsimError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .errors import (
+    CapacityError,
+    ContractViolation,
+    NativeLibraryMissing,
+    SvsimError,
+    ValidationError,
+)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsvb.so")
+
+SVB_OK, SVB_EINVAL, SVB_ENOMEM, SVB_ECUDA, SVB_ENCCL, SVB_ESTATE = 0, -1, -2, -3, -4, -5
+RUN_FUSE = 1
+RUN_STRICT_ORDER = 2
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_i64 = ctypes.c_int64
+_int = ctypes.c_int
+_vp = ctypes.c_void_p
+
+
+class SvbOp(ctypes.Structure):
+    """svb_op (include/svb.h) -- one GateOp (core.py:97-115)."""
+
+    _fields_ = [("kind", ctypes.c_int32), ("target", ctypes.c_int32),
+                ("control", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("q", ctypes.c_double * 8)]
+
+
+_SIGS = {
+    "svb_abi_version": ([], _int),
+    "svb_last_error": ([], ctypes.c_char_p),
+    "svb_launch_count": ([], _i64),
+    "svb_apply_1q": ([_vp, _i64, _dp, _int, _vp], _int),
+    "svb_apply_c1q": ([_vp, _i64, _dp, _int, _int, _vp], _int),
+    "svb_run_ops": ([_vp, _i64, ctypes.POINTER(SvbOp), _int, ctypes.c_uint, _vp], _int),
+    "svb_plan_passes": ([_int, ctypes.POINTER(SvbOp), _int, ctypes.c_uint, ctypes.POINTER(_int)], _int),
+    "svb_norm2": ([_vp, _i64, _dp, _vp], _int),
+    "svb_probs": ([_vp, _i64, _vp, _vp], _int),
+    "svb_exchange_own_row": ([_vp, _vp, _i64, _dp, _int, _int, _i64, _vp], _int),
+    "svb_pair_update": ([_vp, _vp, _i64, _i64, _dp, _int, _vp], _int),
+    "svb_host_apply_1q": ([_vp, _i64, _dp, _int], _int),
+    "svb_host_apply_c1q": ([_vp, _i64, _dp, _int, _int], _int),
+    "svb_host_run_ops": ([_vp, _vp, _i64, ctypes.POINTER(SvbOp), _int, ctypes.c_uint], _int),
+    "svb_profile_enable": ([_int], _int),
+    "svb_profile_read": ([_int, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64)], _int),
+    "svb_profile_class_name": ([_int], ctypes.c_char_p),
+    "svb_dist_create": ([_int, _int, ctypes.POINTER(_int), ctypes.POINTER(_vp), ctypes.POINTER(_vp)], _int),
+    "svb_dist_apply_1q": ([_vp, _dp, _int], _int),
+    "svb_dist_apply_c1q": ([_vp, _dp, _int, _int], _int),
+    "svb_dist_norm2": ([_vp, _dp], _int),
+    "svb_dist_stats": ([_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)], _int),
+    "svb_dist_sync": ([_vp], _int),
+    "svb_dist_destroy": ([_vp], _int),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+
+
+def load(require_cuda: bool = True):
+    """Load libsvb.so.  Raises NativeLibraryMissing if it is not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise NativeLibraryMissing(
+                f"{LIB_PATH} is not built; run __graft_entry__.build() (no CPU fallback)")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (args, res) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = lib
+    if require_cuda:
+        import torch
+
+        if not torch.cuda.is_available():
+            raise NativeLibraryMissing("no CUDA device visible; the gate engine is GPU-only")
+    return _lib
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == SVB_OK:
+        return
+    msg = (_lib.svb_last_error() or b"").decode(errors="replace")
+    msg = f"{what}: {msg}" if what else msg
+    if rc == SVB_EINVAL:
+        raise ValidationError(msg)
+    if rc == SVB_ENOMEM:
+        raise CapacityError(msg)
+    if rc == SVB_ESTATE:
+        raise ContractViolation(msg)
+    raise SvsimError(f"{msg} (svb status {rc})")
+
+
+def gate_array(g) -> ctypes.Array:
+    """Gate2x2 / 4 complex / 8 doubles -> ctypes double[8]."""
+    if hasattr(g, "as_doubles"):
+        vals = g.as_doubles()
+    elif hasattr(g, "q11"):
+        vals = [v for z in (g.q11, g.q12, g.q21, g.q22) for v in (complex(z).real, complex(z).imag)]
+    else:
+        arr = np.asarray(g)
+        if arr.dtype.kind == "c":
+            arr = arr.reshape(-1)
+            vals = [v for z in arr for v in (z.real, z.imag)]
+        else:
+            vals = [float(v) for v in arr.reshape(-1)]
+    if len(vals) != 8:
+        raise ValidationError("gate must have four complex entries")
+    return (ctypes.c_double * 8)(*vals)
+
+
+def ops_array(ops) -> tuple[ctypes.Array, int]:
+    """Iterable of GateOp -> svb_op[]"""
+    ops = list(ops)
+    arr = (SvbOp * max(len(ops), 1))()
+    for i, op in enumerate(ops):
+        arr[i].kind = 0 if op.kind == "single" else 1
+        arr[i].target = int(op.target)
+        arr[i].control = -1 if op.control is None else int(op.control)
+        arr[i].q[:] = list(op.gate.as_doubles())
+    return arr, len(ops)
+
+
+PROFILE_CLASSES = ("k_pair_high", "k_pair_low", "k_diag", "k_tiny", "k_fused", "k_exchange")
+
+
+def profile_enable(on: bool = True) -> None:
+    check(load().svb_profile_enable(1 if on else 0), "profile_enable")
+
+
+def profile_read() -> dict:
+    """{class name: (launches, total_ms, algorithmic bytes)} since enable."""
+    lib = load()
+    out = {}
+    for cls, name in enumerate(PROFILE_CLASSES):
+        n, ms, b = _i64(), ctypes.c_double(), _i64()
+        check(lib.svb_profile_read(cls, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(b)), "profile_read")
+        if n.value:
+            out[name] = (n.value, ms.value, b.value)
+    return out
+
+
+def launch_count() -> int:
+    return int(load(require_cuda=False).svb_launch_count())

@@ -1,0 +1,655 @@
+// abi.cu -- the extern "C" boundary (include/svb.h) and the partitioned-state
+// runtime (svb_dist).
+//
+// Validation mirrors the reference wrapper (kernel/__init__.py:83-97,
+// 124-128): power-of-two length >= 2, 2^(t+1) <= size, control in range and
+// != target.  Failures return SVB_EINVAL with a message; nothing is launched.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/svb.h"
+#include "svb_common.cuh"
+
+namespace svb {
+
+LaunchInfo launch_gate(double2 *a, int64_t n_amps, const Gate &g, int t, int c, cudaStream_t s);
+int launch_norm2(const double2 *a, int64_t n, double *scratch, cudaStream_t s);
+int norm_scratch_doubles();
+int launch_probs(const double2 *a, int64_t n, double *p, cudaStream_t s);
+LaunchInfo launch_exchange_own_row(double2 *own, const double2 *other, int64_t count, const Gate &g,
+                                   int own_is_low, int cbit, int64_t offset, cudaStream_t s);
+LaunchInfo launch_pair_update(double2 *lo_slab, double2 *hi_slab, int64_t begin, int64_t end,
+                              const Gate &g, int cbit, cudaStream_t s);
+int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsigned flags,
+                   cudaStream_t s, int64_t *launches);
+int plan_passes(int n, const svb_op *ops, int nops, unsigned flags);
+
+static thread_local char g_err[512];
+std::atomic<int64_t> g_launches{0};
+
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+}
+
+int cuda_status(cudaError_t e, const char *where) {
+    set_error("%s: CUDA error %d (%s)", where, (int)e, cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? SVB_ENOMEM : SVB_ECUDA;
+}
+
+// ---- launch profiler -------------------------------------------------------
+struct ProfRec {
+    cudaEvent_t a, b;
+    int cls;
+    int64_t bytes;
+};
+static std::mutex g_prof_mu;
+static bool g_prof_enabled = false;
+static std::vector<ProfRec> g_prof_recs;
+static std::vector<cudaEvent_t> g_prof_pool;
+static cudaEvent_t g_prof_pending = nullptr;
+static double g_prof_ms[PROF_NCLASSES];
+static int64_t g_prof_n[PROF_NCLASSES], g_prof_bytes[PROF_NCLASSES];
+
+static cudaEvent_t prof_event() {
+    if (!g_prof_pool.empty()) {
+        cudaEvent_t e = g_prof_pool.back();
+        g_prof_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+bool prof_on() { return g_prof_enabled; }
+
+void prof_begin(cudaStream_t s) {
+    if (!g_prof_enabled) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_pending = prof_event();
+    cudaEventRecord(g_prof_pending, s);
+}
+
+void prof_end(cudaStream_t s, const LaunchInfo &li) {
+    if (!g_prof_enabled || !g_prof_pending) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    cudaEvent_t b = prof_event();
+    cudaEventRecord(b, s);
+    g_prof_recs.push_back(ProfRec{g_prof_pending, b, li.cls, li.alg_bytes});
+    g_prof_pending = nullptr;
+}
+
+// fold finished records into the per-class totals (synchronises on events)
+static void prof_drain() {
+    for (auto &r : g_prof_recs) {
+        float ms = 0.f;
+        cudaEventSynchronize(r.b);
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        g_prof_ms[r.cls] += ms;
+        g_prof_n[r.cls] += 1;
+        g_prof_bytes[r.cls] += r.bytes;
+        g_prof_pool.push_back(r.a);
+        g_prof_pool.push_back(r.b);
+    }
+    g_prof_recs.clear();
+}
+
+static int log2_exact(int64_t n) {
+    if (n < 2 || (n & (n - 1))) return -1;
+    int b = 0;
+    while ((int64_t(1) << b) < n) ++b;
+    return b;
+}
+
+static int check_amps(const void *amps, int64_t n_amps) {
+    if (!amps) {
+        set_error("amplitude pointer is NULL");
+        return SVB_EINVAL;
+    }
+    if (log2_exact(n_amps) < 0) {
+        set_error("amplitude count must be a power of two >= 2, got %lld", (long long)n_amps);
+        return SVB_EINVAL;
+    }
+    if (reinterpret_cast<uintptr_t>(amps) % 16) {
+        set_error("amplitude buffer must be 16-byte aligned");
+        return SVB_EINVAL;
+    }
+    return SVB_OK;
+}
+
+static int check_target(int t, int64_t n_amps) {  // kernel/__init__.py:95-97
+    if (t < 0 || t > 62 || (int64_t(2) << t) > n_amps) {
+        set_error("qubit %d out of range for %lld amplitudes", t, (long long)n_amps);
+        return SVB_EINVAL;
+    }
+    return SVB_OK;
+}
+
+static int check_control(int c, int t, int64_t n_amps) {  // kernel/__init__.py:124-128
+    if (c < 0 || c > 62 || (int64_t(1) << c) >= n_amps) {
+        set_error("control %d out of range for %lld amplitudes", c, (long long)n_amps);
+        return SVB_EINVAL;
+    }
+    if (c == t) {
+        set_error("control and target must differ");
+        return SVB_EINVAL;
+    }
+    return SVB_OK;
+}
+
+int check_ops(int n, const svb_op *ops, int nops) {
+    if (nops < 0 || (nops > 0 && !ops)) {
+        set_error("bad op list");
+        return SVB_EINVAL;
+    }
+    int64_t n_amps = int64_t(1) << n;
+    for (int i = 0; i < nops; ++i) {
+        const svb_op &o = ops[i];
+        if (o.kind != 0 && o.kind != 1) {
+            set_error("op %d: unknown kind %d", i, o.kind);
+            return SVB_EINVAL;
+        }
+        int r = check_target(o.target, n_amps);
+        if (r == SVB_OK && o.kind == 1) r = check_control(o.control, o.target, n_amps);
+        if (r != SVB_OK) return r;
+    }
+    return SVB_OK;
+}
+
+// Grow-only device staging buffer for the host-buffer entry points.
+struct Staging {
+    std::mutex mu;
+    void *ptr = nullptr;
+    size_t bytes = 0;
+    int device = -1;
+};
+static Staging g_stage;
+
+}  // namespace svb
+
+using namespace svb;
+
+extern "C" {
+
+int svb_abi_version(void) { return 1; }
+
+const char *svb_last_error(void) { return g_err; }
+
+int64_t svb_launch_count(void) { return g_launches.load(); }
+
+int svb_apply_1q(void *amps, int64_t n_amps, const double q[8], int target, void *stream) {
+    int r = check_amps(amps, n_amps);
+    if (r == SVB_OK) r = check_target(target, n_amps);
+    if (r != SVB_OK) return r;
+    prof_begin((cudaStream_t)stream);
+    LaunchInfo li = launch_gate((double2 *)amps, n_amps, make_gate(q), target, -1, (cudaStream_t)stream);
+    prof_end((cudaStream_t)stream, li);
+    g_launches += li.kernels;
+    SVB_CHECK_LAUNCH("svb_apply_1q");
+    return SVB_OK;
+}
+
+int svb_apply_c1q(void *amps, int64_t n_amps, const double q[8], int control, int target,
+                  void *stream) {
+    int r = check_amps(amps, n_amps);
+    if (r == SVB_OK) r = check_target(target, n_amps);
+    if (r == SVB_OK) r = check_control(control, target, n_amps);
+    if (r != SVB_OK) return r;
+    prof_begin((cudaStream_t)stream);
+    LaunchInfo li = launch_gate((double2 *)amps, n_amps, make_gate(q), target, control,
+                                (cudaStream_t)stream);
+    prof_end((cudaStream_t)stream, li);
+    g_launches += li.kernels;
+    SVB_CHECK_LAUNCH("svb_apply_c1q");
+    return SVB_OK;
+}
+
+int svb_run_ops(void *amps, int64_t n_amps, const svb_op *ops, int nops, unsigned flags,
+                void *stream) {
+    int r = check_amps(amps, n_amps);
+    if (r != SVB_OK) return r;
+    int n = log2_exact(n_amps);
+    if ((r = check_ops(n, ops, nops)) != SVB_OK) return r;
+    int64_t launches = 0;
+    r = run_ops_device((double2 *)amps, n_amps, ops, nops, flags, (cudaStream_t)stream, &launches);
+    g_launches += launches;
+    if (r != SVB_OK) return r;
+    SVB_CHECK_LAUNCH("svb_run_ops");
+    return SVB_OK;
+}
+
+int svb_plan_passes(int n_qubits, const svb_op *ops, int nops, unsigned flags, int *passes) {
+    if (n_qubits < 1 || n_qubits > 62 || !passes) {
+        set_error("bad arguments to svb_plan_passes");
+        return SVB_EINVAL;
+    }
+    int r = check_ops(n_qubits, ops, nops);
+    if (r != SVB_OK) return r;
+    *passes = plan_passes(n_qubits, ops, nops, flags);
+    return SVB_OK;
+}
+
+int svb_norm2(const void *amps, int64_t n_amps, double *out, void *stream) {
+    int r = check_amps(amps, n_amps);
+    if (r != SVB_OK) return r;
+    if (!out) {
+        set_error("out is NULL");
+        return SVB_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    double *scratch = nullptr;
+    cudaError_t e = cudaMallocAsync((void **)&scratch, sizeof(double) * norm_scratch_doubles(), s);
+    if (e != cudaSuccess) return cuda_status(e, "svb_norm2 alloc");
+    g_launches += launch_norm2((const double2 *)amps, n_amps, scratch, s);  // not profiled
+    e = cudaMemcpyAsync(out, scratch + norm_scratch_doubles() - 1, sizeof(double),
+                        cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(scratch, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_status(e, "svb_norm2");
+    return SVB_OK;
+}
+
+int svb_probs(const void *amps, int64_t n_amps, double *probs, void *stream) {
+    int r = check_amps(amps, n_amps);
+    if (r != SVB_OK) return r;
+    if (!probs) {
+        set_error("probs is NULL");
+        return SVB_EINVAL;
+    }
+    g_launches += launch_probs((const double2 *)amps, n_amps, probs, (cudaStream_t)stream);
+    SVB_CHECK_LAUNCH("svb_probs");
+    return SVB_OK;
+}
+
+int svb_exchange_own_row(void *own, const void *other, int64_t count, const double q[8],
+                         int own_is_low, int cbit, int64_t index_offset, void *stream) {
+    if (!own || !other || count < 0 || cbit > 62 || index_offset < 0) {
+        set_error("bad arguments to svb_exchange_own_row");
+        return SVB_EINVAL;
+    }
+    prof_begin((cudaStream_t)stream);
+    LaunchInfo li = launch_exchange_own_row((double2 *)own, (const double2 *)other, count,
+                                            make_gate(q), own_is_low, cbit, index_offset,
+                                            (cudaStream_t)stream);
+    prof_end((cudaStream_t)stream, li);
+    g_launches += li.kernels;
+    SVB_CHECK_LAUNCH("svb_exchange_own_row");
+    return SVB_OK;
+}
+
+int svb_pair_update(void *lo_slab, void *hi_slab, int64_t begin, int64_t end, const double q[8],
+                    int cbit, void *stream) {
+    if (!lo_slab || !hi_slab || begin < 0 || end < begin || cbit > 62) {
+        set_error("bad arguments to svb_pair_update");
+        return SVB_EINVAL;
+    }
+    prof_begin((cudaStream_t)stream);
+    LaunchInfo li = launch_pair_update((double2 *)lo_slab, (double2 *)hi_slab, begin, end,
+                                       make_gate(q), cbit, (cudaStream_t)stream);
+    prof_end((cudaStream_t)stream, li);
+    g_launches += li.kernels;
+    SVB_CHECK_LAUNCH("svb_pair_update");
+    return SVB_OK;
+}
+
+// ---- host-buffer entry points ---------------------------------------------
+
+static int host_stage(double *host, int64_t n_amps, void **dev) {
+    int d;
+    cudaError_t e = cudaGetDevice(&d);
+    if (e != cudaSuccess) return cuda_status(e, "cudaGetDevice");
+    size_t bytes = size_t(n_amps) * 16;
+    if (g_stage.ptr && (g_stage.device != d || g_stage.bytes < bytes)) {
+        int cur = d;
+        cudaSetDevice(g_stage.device);
+        cudaFree(g_stage.ptr);
+        cudaSetDevice(cur);
+        g_stage.ptr = nullptr;
+        g_stage.bytes = 0;
+    }
+    if (!g_stage.ptr) {
+        e = cudaMalloc(&g_stage.ptr, bytes);
+        if (e != cudaSuccess) {
+            g_stage.ptr = nullptr;
+            return cuda_status(e, "staging cudaMalloc");
+        }
+        g_stage.bytes = bytes;
+        g_stage.device = d;
+    }
+    e = cudaMemcpy(g_stage.ptr, host, bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_status(e, "H2D");
+    *dev = g_stage.ptr;
+    return SVB_OK;
+}
+
+static int host_unstage(double *host, int64_t n_amps, const void *dev) {
+    cudaError_t e = cudaMemcpy(host, dev, size_t(n_amps) * 16, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_status(e, "D2H");
+    return SVB_OK;
+}
+
+int svb_host_apply_1q(double *host_amps, int64_t n_amps, const double q[8], int target) {
+    int r = check_amps(host_amps, n_amps);
+    if (r == SVB_OK) r = check_target(target, n_amps);
+    if (r != SVB_OK) return r;
+    std::lock_guard<std::mutex> lk(g_stage.mu);
+    void *dev;
+    if ((r = host_stage(host_amps, n_amps, &dev)) != SVB_OK) return r;
+    if ((r = svb_apply_1q(dev, n_amps, q, target, nullptr)) != SVB_OK) return r;
+    return host_unstage(host_amps, n_amps, dev);
+}
+
+int svb_host_apply_c1q(double *host_amps, int64_t n_amps, const double q[8], int control,
+                       int target) {
+    int r = check_amps(host_amps, n_amps);
+    if (r == SVB_OK) r = check_target(target, n_amps);
+    if (r == SVB_OK) r = check_control(control, target, n_amps);
+    if (r != SVB_OK) return r;
+    std::lock_guard<std::mutex> lk(g_stage.mu);
+    void *dev;
+    if ((r = host_stage(host_amps, n_amps, &dev)) != SVB_OK) return r;
+    if ((r = svb_apply_c1q(dev, n_amps, q, control, target, nullptr)) != SVB_OK) return r;
+    return host_unstage(host_amps, n_amps, dev);
+}
+
+int svb_host_run_ops(const double *host_in, double *host_out, int64_t n_amps, const svb_op *ops,
+                     int nops, unsigned flags) {
+    int r = check_amps(host_in, n_amps);
+    if (r == SVB_OK) r = check_amps(host_out, n_amps);
+    if (r != SVB_OK) return r;
+    if ((r = check_ops(log2_exact(n_amps), ops, nops)) != SVB_OK) return r;
+    std::lock_guard<std::mutex> lk(g_stage.mu);
+    void *dev;
+    if ((r = host_stage(const_cast<double *>(host_in), n_amps, &dev)) != SVB_OK) return r;
+    if ((r = svb_run_ops(dev, n_amps, ops, nops, flags, nullptr)) != SVB_OK) return r;
+    return host_unstage(host_out, n_amps, dev);
+}
+
+int svb_profile_enable(int on) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    cudaDeviceSynchronize();
+    prof_drain();
+    for (int c = 0; c < PROF_NCLASSES; ++c) g_prof_ms[c] = 0.0, g_prof_n[c] = 0, g_prof_bytes[c] = 0;
+    g_prof_enabled = on != 0;
+    return SVB_OK;
+}
+
+int svb_profile_read(int cls, int64_t *launches, double *total_ms, int64_t *alg_bytes) {
+    if (cls < 0 || cls >= PROF_NCLASSES) {
+        set_error("profile class %d out of range", cls);
+        return SVB_EINVAL;
+    }
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    prof_drain();
+    if (launches) *launches = g_prof_n[cls];
+    if (total_ms) *total_ms = g_prof_ms[cls];
+    if (alg_bytes) *alg_bytes = g_prof_bytes[cls];
+    return SVB_OK;
+}
+
+const char *svb_profile_class_name(int cls) {
+    static const char *names[PROF_NCLASSES] = {"k_pair_high", "k_pair_low", "k_diag", "k_tiny",
+                                               "k_fused", "k_exchange", "k_norm"};
+    return (cls >= 0 && cls < PROF_NCLASSES) ? names[cls] : "";
+}
+
+}  // extern "C"
+
+// ---- partitioned state -----------------------------------------------------
+
+struct svb_dist {
+    int n, k, p;
+    int64_t L;
+    std::vector<int> dev;
+    std::vector<double2 *> slab;
+    std::vector<cudaStream_t> stream;
+    std::vector<cudaEvent_t> ev;
+    std::vector<double *> scratch;
+    int64_t exchanges = 0;
+    std::vector<int64_t> peer_bytes;
+};
+
+namespace {
+
+int set_dev(int d) {
+    cudaError_t e = cudaSetDevice(d);
+    return e == cudaSuccess ? SVB_OK : cuda_status(e, "cudaSetDevice");
+}
+
+// stream b waits for everything already queued on stream a
+int order_after(svb_dist *d, int b, int a) {
+    if (a == b) return SVB_OK;
+    int r = set_dev(d->dev[a]);
+    if (r) return r;
+    cudaError_t e = cudaEventRecord(d->ev[a], d->stream[a]);
+    if (e == cudaSuccess) {
+        set_dev(d->dev[b]);
+        e = cudaStreamWaitEvent(d->stream[b], d->ev[a], 0);
+    }
+    return e == cudaSuccess ? SVB_OK : cuda_status(e, "cross-rank ordering");
+}
+
+// Pairwise exchange on global bit gb among `mask`-selected ranks.
+int dist_exchange(svb_dist *d, const Gate &g, int gb, int cbit, int rank_bit_req) {
+    int64_t half = d->L >> 1;
+    for (int r = 0; r < d->p; ++r) {
+        int q = r ^ (1 << gb);
+        if (r > q) continue;
+        if (rank_bit_req >= 0 && !((r >> rank_bit_req) & 1)) continue;
+        // both sides see each other's earlier work before touching the slabs
+        int rc = order_after(d, r, q);
+        if (!rc) rc = order_after(d, q, r);
+        if (rc) return rc;
+        // lower rank owns pairs j < L/2, upper rank j >= L/2
+        if ((rc = set_dev(d->dev[r]))) return rc;
+        prof_begin(d->stream[r]);
+        LaunchInfo li = launch_pair_update(d->slab[r], d->slab[q], 0, half, g, cbit, d->stream[r]);
+        prof_end(d->stream[r], li);
+        g_launches += li.kernels;
+        SVB_CHECK_LAUNCH("dist exchange (low)");
+        if ((rc = set_dev(d->dev[q]))) return rc;
+        prof_begin(d->stream[q]);
+        li = launch_pair_update(d->slab[r], d->slab[q], half, d->L, g, cbit, d->stream[q]);
+        prof_end(d->stream[q], li);
+        g_launches += li.kernels;
+        SVB_CHECK_LAUNCH("dist exchange (high)");
+        // later work on either rank waits for both halves
+        rc = order_after(d, r, q);
+        if (!rc) rc = order_after(d, q, r);
+        if (rc) return rc;
+        int64_t moved = (cbit >= 0 ? half / 2 : half) * 16 * 2;  // read + write of partner amps
+        d->peer_bytes[r] += moved;
+        d->peer_bytes[q] += moved;
+    }
+    d->exchanges += 1;
+    return SVB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int svb_dist_create(int n, int k, const int *devices, void *const *slabs, svb_dist **out) {
+    if (!out || !devices || !slabs || n < 1 || n > 62 || k < 0 || k > n - 1 || k > 16) {
+        set_error("bad arguments to svb_dist_create (n=%d, k=%d)", n, k);
+        return SVB_EINVAL;
+    }
+    svb_dist *d = new svb_dist();
+    d->n = n;
+    d->k = k;
+    d->p = 1 << k;
+    d->L = int64_t(1) << (n - k);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (int r = 0; r < d->p; ++r) {
+        if (!slabs[r] || reinterpret_cast<uintptr_t>(slabs[r]) % 16) {
+            set_error("slab %d is NULL or misaligned", r);
+            delete d;
+            return SVB_EINVAL;
+        }
+        d->dev.push_back(devices[r]);
+        d->slab.push_back((double2 *)slabs[r]);
+    }
+    d->peer_bytes.assign(d->p, 0);
+    int rc = SVB_OK;
+    for (int r = 0; r < d->p && !rc; ++r) {
+        rc = set_dev(d->dev[r]);
+        cudaStream_t s;
+        cudaEvent_t e;
+        double *sc;
+        if (!rc && cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) rc = SVB_ECUDA;
+        if (!rc) d->stream.push_back(s);
+        if (!rc && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) rc = SVB_ECUDA;
+        if (!rc) d->ev.push_back(e);
+        if (!rc && cudaMalloc((void **)&sc, sizeof(double) * norm_scratch_doubles()) != cudaSuccess)
+            rc = SVB_ENOMEM;
+        if (!rc) d->scratch.push_back(sc);
+        // peer access for every partner on a different device
+        for (int b = 0; b < d->k && !rc; ++b) {
+            int peer = d->dev[r ^ (1 << b)];
+            if (peer == d->dev[r]) continue;
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, d->dev[r], peer);
+            if (!can) {
+                set_error("device %d cannot access peer %d", d->dev[r], peer);
+                rc = SVB_ESTATE;
+                break;
+            }
+            cudaError_t pe = cudaDeviceEnablePeerAccess(peer, 0);
+            if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) rc = cuda_status(pe, "peer access");
+            cudaGetLastError();
+        }
+    }
+    cudaSetDevice(cur);
+    if (rc) {
+        if (g_err[0] == 0) set_error("svb_dist_create failed");
+        svb_dist_destroy(d);
+        return rc;
+    }
+    *out = d;
+    return SVB_OK;
+}
+
+int svb_dist_apply_1q(svb_dist *d, const double q[8], int target) {
+    if (!d) return SVB_EINVAL;
+    if (target < 0 || target >= d->n) {
+        set_error("qubit %d out of range for n=%d", target, d->n);
+        return SVB_EINVAL;
+    }
+    Gate g = make_gate(q);
+    int boundary = d->n - d->k;
+    if (target >= boundary) return dist_exchange(d, g, target - boundary, -1, -1);
+    for (int r = 0; r < d->p; ++r) {  // engine.py:348-356, ranks concurrent
+        int rc = set_dev(d->dev[r]);
+        if (rc) return rc;
+        prof_begin(d->stream[r]);
+        LaunchInfo li = launch_gate(d->slab[r], d->L, g, target, -1, d->stream[r]);
+        prof_end(d->stream[r], li);
+        g_launches += li.kernels;
+        SVB_CHECK_LAUNCH("dist local gate");
+    }
+    return SVB_OK;
+}
+
+int svb_dist_apply_c1q(svb_dist *d, const double q[8], int control, int target) {
+    if (!d) return SVB_EINVAL;
+    if (control < 0 || control >= d->n || target < 0 || target >= d->n || control == target) {
+        set_error("bad control/target (%d, %d) for n=%d", control, target, d->n);
+        return SVB_EINVAL;
+    }
+    Gate g = make_gate(q);
+    int boundary = d->n - d->k;
+    if (control >= boundary) {  // regime (iii): the control selects ranks
+        int cb = control - boundary;
+        if (target >= boundary) return dist_exchange(d, g, target - boundary, -1, cb);
+        for (int r = 0; r < d->p; ++r) {
+            if (!((r >> cb) & 1)) continue;
+            int rc = set_dev(d->dev[r]);
+            if (rc) return rc;
+            prof_begin(d->stream[r]);
+            LaunchInfo li = launch_gate(d->slab[r], d->L, g, target, -1, d->stream[r]);
+            prof_end(d->stream[r], li);
+            g_launches += li.kernels;
+            SVB_CHECK_LAUNCH("dist rank-controlled gate");
+        }
+        return SVB_OK;
+    }
+    if (target >= boundary)  // regime (ii): exchange restricted to bit-c set
+        return dist_exchange(d, g, target - boundary, control, -1);
+    for (int r = 0; r < d->p; ++r) {  // regime (i)
+        int rc = set_dev(d->dev[r]);
+        if (rc) return rc;
+        prof_begin(d->stream[r]);
+        LaunchInfo li = launch_gate(d->slab[r], d->L, g, target, control, d->stream[r]);
+        prof_end(d->stream[r], li);
+        g_launches += li.kernels;
+        SVB_CHECK_LAUNCH("dist controlled gate");
+    }
+    return SVB_OK;
+}
+
+int svb_dist_norm2(svb_dist *d, double *out) {
+    if (!d || !out) return SVB_EINVAL;
+    double total = 0.0;
+    for (int r = 0; r < d->p; ++r) {
+        int rc = set_dev(d->dev[r]);
+        if (rc) return rc;
+        g_launches += launch_norm2(d->slab[r], d->L, d->scratch[r], d->stream[r]);
+        double v = 0.0;
+        cudaError_t e = cudaMemcpyAsync(&v, d->scratch[r] + norm_scratch_doubles() - 1,
+                                        sizeof(double), cudaMemcpyDeviceToHost, d->stream[r]);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(d->stream[r]);
+        if (e != cudaSuccess) return cuda_status(e, "svb_dist_norm2");
+        total += v;  // rank order, like engine.py:453-454
+    }
+    *out = total;
+    return SVB_OK;
+}
+
+int svb_dist_stats(svb_dist *d, int64_t *exchanges, int64_t *peer_bytes_per_rank) {
+    if (!d) return SVB_EINVAL;
+    if (exchanges) *exchanges = d->exchanges;
+    if (peer_bytes_per_rank)
+        for (int r = 0; r < d->p; ++r) peer_bytes_per_rank[r] = d->peer_bytes[r];
+    return SVB_OK;
+}
+
+int svb_dist_sync(svb_dist *d) {
+    if (!d) return SVB_EINVAL;
+    for (int r = 0; r < d->p; ++r) {
+        set_dev(d->dev[r]);
+        cudaError_t e = cudaStreamSynchronize(d->stream[r]);
+        if (e != cudaSuccess) return cuda_status(e, "svb_dist_sync");
+    }
+    return SVB_OK;
+}
+
+int svb_dist_destroy(svb_dist *d) {
+    if (!d) return SVB_OK;
+    for (size_t r = 0; r < d->stream.size(); ++r) {
+        cudaSetDevice(d->dev[r]);
+        cudaStreamSynchronize(d->stream[r]);
+        cudaStreamDestroy(d->stream[r]);
+    }
+    for (size_t r = 0; r < d->ev.size(); ++r) {
+        cudaSetDevice(d->dev[r]);
+        cudaEventDestroy(d->ev[r]);
+    }
+    for (size_t r = 0; r < d->scratch.size(); ++r) {
+        cudaSetDevice(d->dev[r]);
+        cudaFree(d->scratch[r]);
+    }
+    delete d;
+    return SVB_OK;
+}
+
+}  // extern "C"

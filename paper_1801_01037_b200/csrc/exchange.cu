@@ -1,0 +1,111 @@
+// exchange.cu -- global-qubit (rank-bit) gate kernels.
+//
+// A gate whose target bit is a rank bit pairs local index j of rank r with
+// local index j of partner r ^ 2^(t-(n-k)) (partition.py:126-137).
+//
+// k_exchange_own_row: the paper's single-amplitude protocol, batched: this
+//   rank received the partner's amplitudes `other` and updates only its own
+//   row (engine.py:249-254 scheme b; engine.py:257-272 chunked).  Used by the
+//   multi-process engine after an NCCL send/recv of a chunk.
+// k_pair_update: both rows of pairs (lo_slab[j], hi_slab[j]).  With peer
+//   access one GPU reads the partner slab over NVLink and writes both
+//   amplitudes back: the lower rank of a pair covers j < L/2, the upper rank
+//   j >= L/2, so each direction of the link carries 8*L bytes instead of a
+//   full 16*L slab exchange (the work split of scheme a, engine.py:206-238,
+//   without the staging buffer or the send-back).
+#include "svb_common.cuh"
+
+namespace svb {
+
+constexpr int kXThreads = 256;
+constexpr int kXUpt = 4;
+
+template <int KIND>
+__global__ void __launch_bounds__(kXThreads) k_exchange_own_row(double2 *__restrict__ own,
+                                                                const double2 *__restrict__ other,
+                                                                int64_t count, Gate g, int own_is_low,
+                                                                int cbit, int64_t offset) {
+    const int64_t base = int64_t(blockIdx.x) * kXThreads * kXUpt + threadIdx.x;
+    double2 mine[kXUpt], oth[kXUpt];
+    bool on[kXUpt];
+#pragma unroll
+    for (int k = 0; k < kXUpt; ++k) {
+        int64_t j = base + int64_t(k) * kXThreads;
+        on[k] = j < count && (cbit < 0 || (((offset + j) >> cbit) & 1));
+        if (on[k]) {
+            mine[k] = own[j];
+            oth[k] = other[j];
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kXUpt; ++k) {
+        if (!on[k]) continue;
+        int64_t j = base + int64_t(k) * kXThreads;
+        own[j] = own_is_low ? row<KIND>(g, false, mine[k], oth[k]) : row<KIND>(g, true, oth[k], mine[k]);
+    }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kXThreads) k_pair_update(double2 *lo_slab, double2 *hi_slab,
+                                                           int64_t begin, int64_t end, Gate g,
+                                                           int cbit) {
+    const int64_t base = begin + int64_t(blockIdx.x) * kXThreads * kXUpt + threadIdx.x;
+    double2 lo[kXUpt], hi[kXUpt];
+    bool on[kXUpt];
+#pragma unroll
+    for (int k = 0; k < kXUpt; ++k) {
+        int64_t j = base + int64_t(k) * kXThreads;
+        on[k] = j < end && (cbit < 0 || ((j >> cbit) & 1));
+        if (on[k]) {
+            lo[k] = lo_slab[j];
+            hi[k] = hi_slab[j];
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kXUpt; ++k) {
+        if (!on[k]) continue;
+        int64_t j = base + int64_t(k) * kXThreads;
+        pair_both<KIND>(g, lo[k], hi[k]);
+        lo_slab[j] = lo[k];
+        hi_slab[j] = hi[k];
+    }
+}
+
+static unsigned grid_for(int64_t count) {
+    return (unsigned)((count + int64_t(kXThreads) * kXUpt - 1) / (int64_t(kXThreads) * kXUpt));
+}
+
+LaunchInfo launch_exchange_own_row(double2 *own, const double2 *other, int64_t count, const Gate &g,
+                                   int own_is_low, int cbit, int64_t offset, cudaStream_t s) {
+    if (count <= 0) return LaunchInfo{0, PROF_EXCHANGE, 0};
+    unsigned blocks = grid_for(count);
+#define SVB_X(K) k_exchange_own_row<K><<<blocks, kXThreads, 0, s>>>(own, other, count, g, own_is_low, cbit, offset)
+    switch (g.kind) {
+        case K_REAL: SVB_X(K_REAL); break;
+        case K_DIAG: SVB_X(K_DIAG); break;
+        case K_ANTI: SVB_X(K_ANTI); break;
+        case K_RX: SVB_X(K_RX); break;
+        default: SVB_X(K_GENERAL); break;
+    }
+#undef SVB_X
+    // own read + write, partner chunk read (control-masked: half of each)
+    return LaunchInfo{1, PROF_EXCHANGE, (cbit >= 0 ? count / 2 : count) * 48};
+}
+
+LaunchInfo launch_pair_update(double2 *lo_slab, double2 *hi_slab, int64_t begin, int64_t end,
+                              const Gate &g, int cbit, cudaStream_t s) {
+    if (end <= begin) return LaunchInfo{0, PROF_EXCHANGE, 0};
+    unsigned blocks = grid_for(end - begin);
+#define SVB_P(K) k_pair_update<K><<<blocks, kXThreads, 0, s>>>(lo_slab, hi_slab, begin, end, g, cbit)
+    switch (g.kind) {
+        case K_REAL: SVB_P(K_REAL); break;
+        case K_DIAG: SVB_P(K_DIAG); break;
+        case K_ANTI: SVB_P(K_ANTI); break;
+        case K_RX: SVB_P(K_RX); break;
+        default: SVB_P(K_GENERAL); break;
+    }
+#undef SVB_P
+    return LaunchInfo{1, PROF_EXCHANGE, (cbit >= 0 ? (end - begin) / 2 : (end - begin)) * 64};
+}
+
+}  // namespace svb

@@ -1,0 +1,294 @@
+"""Partitioned execution over rank slabs in HBM (mirrors pkg/src/svsim/engine.py).
+
+Same public surface as the reference engine -- ``dist_init``, ``gather``,
+``dist_apply_local``, ``dist_apply_scheme_a/b``, ``dist_apply_chunked``,
+``dist_apply_controlled``, ``run_circuit``, ``GateStats``, ``time_ratio``
+(engine.py:157-521) -- but every rank's slab is a CUDA tensor and every
+update is a libsvb.so kernel driven through one ``svb_dist`` handle:
+
+* local gates: one kernel per rank, ranks' streams run concurrently
+  (the reference sweeps ranks one after another, engine.py:348-356);
+* global-target gates: the fused peer-memory pair kernel -- the lower rank
+  of each pair updates pairs j < L/2, the upper rank j >= L/2, each reading
+  and writing the partner slab directly (NVLink P2P when the ranks sit on
+  different GPUs);
+* the three controlled regimes of engine.py:415-450.
+
+All three reference protocols compute the same amplitudes (engine.py:160-184
+asserts agreement), so the scheme no longer changes the data path; it keeps
+its meaning for the accounting: ``GateStats`` reports the messages/bytes the
+reference protocol would send per rank (exact formulas, partition.py here),
+and ``peer_bytes`` what the fused kernel actually moved.
+
+Ranks may share a GPU (emulated ranks; every exchange is then a same-device
+pair kernel) or be spread over several GPUs of one process.  The
+multi-process, one-GPU-per-process engine is ``paper_1801_01037_b200.dist``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .core import Circuit, Gate2x2, StateVector
+from .errors import ContractViolation, ValidationError
+from .partition import (
+    SCHEME_A,
+    SCHEME_B,
+    CommScheme,
+    PartitionPlan,
+    needs_comm,
+    protocol_accounting,
+)
+
+
+@dataclass(frozen=True)
+class GateStats:
+    """Per-gate accounting (engine.py:143-154): messages/bytes are the max over
+    ranks of what the reference protocol sends; wall_time is device-synchronised
+    wall time of the gate."""
+
+    qubit: int
+    control: int | None
+    comm_required: bool
+    messages_sent_per_rank: int
+    bytes_sent_per_rank: int
+    wall_time: float
+
+
+class DistState:
+    """2^k slabs plus the native handle that drives them (engine.py:132-140)."""
+
+    def __init__(self, plan: PartitionPlan, scheme: CommScheme | None, slabs, devices):
+        self.plan = plan
+        self.scheme = scheme
+        self.slabs = slabs
+        self.devices = list(devices)
+        lib = _lib.load()
+        p = plan.p
+        dev_arr = (ctypes.c_int * p)(*self.devices)
+        slab_arr = (ctypes.c_void_p * p)(*[s.data_ptr() for s in slabs])
+        h = ctypes.c_void_p()
+        import torch
+
+        torch.cuda.synchronize()
+        _lib.check(lib.svb_dist_create(plan.n, plan.k, dev_arr, slab_arr, ctypes.byref(h)), "dist_init")
+        self._h = h
+        self.messages_sent = [0] * p
+        self.bytes_sent = [0] * p
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        if self._h is None:
+            raise ContractViolation("distributed state already closed")
+        return self._h
+
+    def sync(self) -> None:
+        _lib.check(_lib.load().svb_dist_sync(self.handle), "sync")
+
+    def peer_bytes(self) -> list[int]:
+        arr = (ctypes.c_int64 * self.plan.p)()
+        ex = ctypes.c_int64()
+        _lib.check(_lib.load().svb_dist_stats(self.handle, ctypes.byref(ex), arr), "stats")
+        return list(arr)
+
+    def close(self) -> None:
+        if self._h is not None:
+            _lib.load().svb_dist_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def dist_init(plan: PartitionPlan, scheme: CommScheme | None = None, devices=None,
+              initial=None) -> DistState:
+    """|0...0> (or `initial`, host array / StateVector) across the plan's ranks
+    (engine.py:157-185).  devices: list of CUDA ordinals per rank, default all
+    ranks on the current device."""
+    import torch
+
+    _lib.load()
+    if devices is None:
+        devices = [torch.cuda.current_device()] * plan.p
+    devices = list(devices)
+    if len(devices) != plan.p:
+        raise ValidationError(f"need {plan.p} device ordinals, got {len(devices)}")
+    if scheme is not None:
+        scheme.buffer_amps(plan)  # reference validation (chunk size <= slab)
+    L = plan.local_len
+    slabs = []
+    if initial is not None:
+        amps = initial.amps if isinstance(initial, StateVector) else np.ascontiguousarray(initial, np.complex128)
+        if amps.shape[0] != (1 << plan.n):
+            raise ValidationError(f"initial state must have 2**{plan.n} amplitudes")
+        for r in range(plan.p):
+            slabs.append(torch.from_numpy(amps[r * L:(r + 1) * L].copy()).to(f"cuda:{devices[r]}"))
+    else:
+        for r in range(plan.p):
+            s = torch.zeros(L, dtype=torch.complex128, device=f"cuda:{devices[r]}")
+            if r == 0:
+                s[0] = 1.0
+            slabs.append(s)
+    return DistState(plan, scheme, slabs, devices)
+
+
+def gather(ds: DistState) -> StateVector:
+    """Concatenate slabs in rank order (engine.py:188-192) on the host."""
+    ds.sync()
+    return StateVector(ds.plan.n, np.concatenate([s.cpu().numpy() for s in ds.slabs]), validate=False)
+
+
+def _account(ds: DistState, scheme: CommScheme, t: int, cbit: int | None, participants) -> None:
+    plan = ds.plan
+    gb = t - (plan.n - plan.k)
+    for r in range(plan.p):
+        if participants is not None and r not in participants:
+            continue
+        q = r ^ (1 << gb)
+        m, b = protocol_accounting(plan, scheme, r < q, cbit)
+        ds.messages_sent[r] += m
+        ds.bytes_sent[r] += b
+
+
+def protocol_stats(circuit: Circuit, plan: PartitionPlan, scheme: CommScheme | None) -> list[tuple[int, int]]:
+    """Host-only: per-op (messages, bytes) max over ranks that run_circuit's
+    GateStats report for this circuit (engine.py:495-505 semantics)."""
+    boundary = plan.n - plan.k
+    out = []
+    for op in circuit.ops:
+        t, c = op.target, op.control
+        if t < boundary:
+            out.append((0, 0))
+            continue
+        if scheme is None:
+            raise ValidationError("communicating target requires a scheme")
+        gb = t - boundary
+        parts = None
+        cbit = None
+        if c is not None:
+            if c >= boundary:
+                parts = {r for r in range(plan.p) if (r >> (c - boundary)) & 1}
+            else:
+                cbit = c
+        best = (0, 0)
+        msgs_max = bytes_max = 0
+        for r in range(plan.p):
+            if parts is not None and r not in parts:
+                continue
+            m, b = protocol_accounting(plan, scheme, r < (r ^ (1 << gb)), cbit)
+            msgs_max, bytes_max = max(msgs_max, m), max(bytes_max, b)
+        best = (msgs_max, bytes_max)
+        out.append(best)
+    return out
+
+
+def dist_apply_local(ds: DistState, g: Gate2x2, i: int, strat=None) -> None:
+    """engine.py:348-356."""
+    if needs_comm(ds.plan, i):
+        raise ContractViolation(f"qubit {i} spans ranks for n={ds.plan.n}, k={ds.plan.k}; use a scheme")
+    _lib.check(_lib.load().svb_dist_apply_1q(ds.handle, _lib.gate_array(g), int(i)), "dist_apply_local")
+
+
+def _exchange(ds: DistState, g: Gate2x2, i: int, scheme: CommScheme) -> None:
+    plan = ds.plan
+    if not needs_comm(plan, i):
+        raise ContractViolation(f"qubit {i} is rank-local for n={plan.n}, k={plan.k}; use dist_apply_local")
+    _lib.check(_lib.load().svb_dist_apply_1q(ds.handle, _lib.gate_array(g), int(i)), "exchange")
+    _account(ds, scheme, i, None, None)
+
+
+def dist_apply_scheme_a(ds: DistState, g: Gate2x2, i: int) -> None:
+    _exchange(ds, g, i, SCHEME_A)
+
+
+def dist_apply_scheme_b(ds: DistState, g: Gate2x2, i: int) -> None:
+    _exchange(ds, g, i, SCHEME_B)
+
+
+def dist_apply_chunked(ds: DistState, g: Gate2x2, i: int, m: int) -> None:
+    _exchange(ds, g, i, CommScheme("chunked", m))
+
+
+def dist_apply_controlled(ds: DistState, g: Gate2x2, c: int, t: int,
+                          scheme: CommScheme | None = None) -> None:
+    """engine.py:415-450: three regimes, dispatched natively."""
+    plan = ds.plan
+    for name, idx in (("control", c), ("target", t)):
+        if not (0 <= idx < plan.n):
+            raise ValidationError(f"{name} bit {idx} out of range for n={plan.n}")
+    if c == t:
+        raise ValidationError("control and target must differ")
+    scheme = scheme if scheme is not None else ds.scheme
+    boundary = plan.n - plan.k
+    if t >= boundary and scheme is None:
+        raise ValidationError("communicating target requires a scheme")
+    _lib.check(_lib.load().svb_dist_apply_c1q(ds.handle, _lib.gate_array(g), int(c), int(t)),
+               "dist_apply_controlled")
+    if t >= boundary:
+        if c >= boundary:
+            parts = {r for r in range(plan.p) if (r >> (c - boundary)) & 1}
+            _account(ds, scheme, t, None, parts)
+        else:
+            _account(ds, scheme, t, c, None)
+
+
+def dist_norm2(ds: DistState) -> float:
+    out = ctypes.c_double()
+    _lib.check(_lib.load().svb_dist_norm2(ds.handle, ctypes.byref(out)), "norm2")
+    return out.value
+
+
+def run_circuit(circuit: Circuit, plan: PartitionPlan, scheme: CommScheme | None = None,
+                strat=None, perm=None, norm_tol: float | None = None, devices=None,
+                initial=None) -> tuple[DistState, list[GateStats]]:
+    """engine.py:457-512 on the device.  Gate-by-gate with a device sync per
+    gate so GateStats.wall_time means what it does in the reference; use
+    device.run_ops / simulate for fused full-speed execution."""
+    if circuit.n != plan.n:
+        raise ValidationError(f"circuit has {circuit.n} qubits, plan has {plan.n}")
+    if perm is not None and perm.n != plan.n:
+        raise ValidationError(f"layout is over {perm.n} qubits, plan has {plan.n}")
+    ds = dist_init(plan, scheme, devices=devices, initial=initial)
+    l2p = perm.logical_to_phys if perm is not None else tuple(range(plan.n))
+    boundary = plan.n - plan.k
+    stats: list[GateStats] = []
+    for pos, op in enumerate(circuit.ops):
+        tbit = l2p[op.target]
+        before_m, before_b = list(ds.messages_sent), list(ds.bytes_sent)
+        t0 = time.perf_counter()
+        if op.kind == "single":
+            if tbit < boundary:
+                dist_apply_local(ds, op.gate, tbit)
+            else:
+                if ds.scheme is None:
+                    raise ValidationError(f"qubit {tbit} requires communication but no scheme was configured")
+                _exchange(ds, op.gate, tbit, ds.scheme)
+        else:
+            dist_apply_controlled(ds, op.gate, l2p[op.control], tbit)
+        ds.sync()
+        wall = time.perf_counter() - t0
+        msgs = max(a - b for a, b in zip(ds.messages_sent, before_m))
+        nbytes = max(a - b for a, b in zip(ds.bytes_sent, before_b))
+        stats.append(GateStats(op.target, op.control, tbit >= boundary, msgs, nbytes, wall))
+        if norm_tol is not None:
+            drift = abs(dist_norm2(ds) - 1.0)
+            if drift > norm_tol:
+                raise ValidationError(f"norm drifted by {drift:.3e} after gate {pos}")
+    return ds, stats
+
+
+def time_ratio(comm, nocomm) -> float:
+    """engine.py:515-521."""
+    tc = comm.wall_time if isinstance(comm, GateStats) else float(comm)
+    tn = nocomm.wall_time if isinstance(nocomm, GateStats) else float(nocomm)
+    if tc <= 0.0 or tn <= 0.0:
+        raise ValidationError("wall times must be positive to form a ratio")
+    return tc / tn

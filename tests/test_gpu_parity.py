@@ -1,0 +1,264 @@
+"""GPU parity: libsvb.so kernels vs the CPU oracle and the reference's golden
+outputs.  Bar: bit-identical (np.array_equal, zero signs aside) for single
+gate kernels and unfused op lists; max-abs <= 1e-12 (the north-star
+tolerance) wherever gates are fused or reordered."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import gate_from_q, golden, split_cases
+from paper_1801_01037_b200 import (
+    SCHEME_A,
+    SCHEME_B,
+    Circuit,
+    GateOp,
+    PartitionPlan,
+    StateVector,
+    apply_controlled,
+    apply_single,
+    chunked,
+    phase,
+    rx,
+    ry,
+    rz,
+    standard_gate,
+)
+from paper_1801_01037_b200 import _lib, device, engine, workloads as w
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+def canon_sha(a):
+    v = np.ascontiguousarray(a, dtype=np.complex128).view(np.float64) + 0.0
+    return hashlib.sha256(v.tobytes()).hexdigest()
+
+
+def all_gates(rng):
+    return [standard_gate(x) for x in "IXYZHST"] + [
+        rx(1.1), ry(-0.7), rz(2.5), phase(0.3), w.random_unitary2(rng)]
+
+
+def test_golden_kernel_single_bit_exact(cuda_ok):
+    z = golden("kernel_single.npz")
+    ins = split_cases(z["meta"][:, 0], z["inp"])
+    outs = split_cases(z["meta"][:, 0], z["out"])
+    for (n, c, t), q, a, want in zip(z["meta"], z["gates"], ins, outs):
+        s = StateVector(int(n), a.copy())
+        apply_single(s, gate_from_q(q), int(t))  # host array -> backend -> C ABI
+        assert np.array_equal(s.amps, want)
+
+
+def test_golden_kernel_controlled_bit_exact(cuda_ok):
+    z = golden("kernel_controlled.npz")
+    ins = split_cases(z["meta"][:, 0], z["inp"])
+    outs = split_cases(z["meta"][:, 0], z["out"])
+    for (n, c, t), q, a, want in zip(z["meta"], z["gates"], ins, outs):
+        s = StateVector(int(n), a.copy())
+        apply_controlled(s, gate_from_q(q), int(c), int(t))
+        assert np.array_equal(s.amps, want)
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 6, 7, 11, 16])
+def test_every_target_every_gate_kind_bit_exact(cuda_ok, n):
+    rng = np.random.default_rng(100 + n)
+    a = w.random_state_array(rng, n)
+    for g in all_gates(rng):
+        for t in range(n):
+            want = oracle.apply_single(a.copy(), g, t)
+            st = device.DeviceState.from_host(a)
+            device.apply_single(st, g, t)
+            assert np.array_equal(st.to_host().amps, want), (n, t, g)
+
+
+@pytest.mark.parametrize("n", [2, 6, 7, 12])
+def test_every_control_target_pair_bit_exact(cuda_ok, n):
+    rng = np.random.default_rng(200 + n)
+    a = w.random_state_array(rng, n)
+    gates = all_gates(rng)
+    for c in range(n):
+        for t in range(n):
+            if c == t:
+                continue
+            g = gates[(c * n + t) % len(gates)]
+            want = oracle.apply_controlled(a.copy(), g, c, t)
+            st = device.DeviceState.from_host(a)
+            device.apply_controlled(st, g, c, t)
+            assert np.array_equal(st.to_host().amps, want), (n, c, t)
+
+
+def test_qft20_matches_reference_sha(cuda_ok):
+    # config 1: QFT n=20, seeded Gaussian state; reference output hash
+    z = golden("qft.npz")
+    a = w.random_state_array(np.random.default_rng(w.SEED_STATE), 20)
+    out = device.simulate(w.qft_circuit(20), a.copy(), fuse=False)
+    assert canon_sha(out) == str(z["sha20"])
+    assert np.array_equal(out[z["idx20"]], z["amp20"])
+    fused = device.simulate(w.qft_circuit(20), a.copy(), fuse=True)
+    assert np.max(np.abs(fused - out)) <= TOL
+    st = device.DeviceState.from_host(fused)
+    p = device.probs(st).cpu().numpy()
+    assert np.max(np.abs(p[z["idx20"]] - z["prob20"])) <= TOL
+    assert abs(device.norm2(st) - float(z["norm20"])) <= 1e-12
+
+
+def test_layers_matches_reference(cuda_ok):
+    z = golden("layers.npz")
+    circ = w.random_layer_circuit(12, 20, seed=int(z["seed"]))
+    out = device.simulate(circ, None, fuse=False)
+    assert canon_sha(out) == str(z["sha"])
+    for strict in (True, False):
+        f = device.simulate(circ, None, fuse=True, strict_order=strict)
+        assert np.max(np.abs(f - z["out"])) <= TOL
+        if strict:
+            assert np.array_equal(f, z["out"])
+
+
+@pytest.mark.parametrize("n", [14, 18, 22])
+def test_fused_random_layers_vs_oracle(cuda_ok, n):
+    circ = w.random_layer_circuit(n, 6, seed=n)
+    a = w.random_state_array(np.random.default_rng(n), n)
+    want = oracle.run_ops(a.copy(), w.oracle_ops(circ), workers=8)
+    for fuse, strict in ((False, False), (True, True), (True, False)):
+        got = device.simulate(circ, a.copy(), fuse=fuse, strict_order=strict)
+        err = np.max(np.abs(got - want))
+        assert err <= TOL, (fuse, strict, err)
+        if not fuse or strict:
+            assert np.array_equal(got, want)
+
+
+def test_random_reference_circuits_vs_oracle(cuda_ok):
+    # conftest.random_circuit shape (p_controlled = 0.35, Haar gates), n up to 20
+    rng = np.random.default_rng(77)
+    for _ in range(20):
+        n = int(rng.integers(2, 21))
+        ops = []
+        for _ in range(30):
+            g = w.random_unitary2(rng)
+            if rng.random() < 0.35:
+                c, t = rng.choice(n, size=2, replace=False)
+                ops.append(GateOp("controlled", g, int(t), int(c)))
+            else:
+                ops.append(GateOp("single", g, int(rng.integers(n))))
+        circ = Circuit(n, tuple(ops))
+        a = w.random_state_array(rng, n)
+        want = oracle.run_ops(a.copy(), w.oracle_ops(circ))
+        assert np.array_equal(device.simulate(circ, a.copy(), fuse=False), want)
+        assert np.max(np.abs(device.simulate(circ, a.copy(), fuse=True) - want)) <= TOL
+
+
+def test_norm_and_probs(cuda_ok):
+    for n in (1, 5, 13, 21):
+        a = w.random_state_array(np.random.default_rng(n), n)
+        st = device.DeviceState.from_host(a)
+        assert abs(device.norm2(st) - float(np.vdot(a, a).real)) <= 1e-12
+        p = device.probs(st).cpu().numpy()
+        assert np.max(np.abs(p - np.abs(a) ** 2)) <= 1e-15
+        assert np.array_equal(p, oracle.probs(a))
+
+
+def test_edge_cases(cuda_ok):
+    # zero state never fires a control (test_kernel.py:96-99); identity; X twice
+    st = device.DeviceState.zeros(5)
+    device.apply_controlled(st, standard_gate("x"), 4, 2)
+    h = st.to_host().amps
+    assert h[0] == 1 and np.count_nonzero(h) == 1
+    a = w.random_state_array(np.random.default_rng(9), 10)
+    st = device.DeviceState.from_host(a)
+    for t in range(10):
+        device.apply_single(st, standard_gate("i"), t)
+    assert np.array_equal(st.to_host().amps, a)
+    for _ in range(2):
+        device.apply_single(st, standard_gate("x"), 7)
+    assert np.array_equal(st.to_host().amps, a)
+    # empty op list is a no-op
+    device.run_ops(st, [])
+    assert np.array_equal(st.to_host().amps, a)
+    # invalid arguments raise, never launch
+    from paper_1801_01037_b200 import ValidationError
+
+    with pytest.raises(ValidationError):
+        device.apply_single(st, standard_gate("x"), 10)
+    with pytest.raises(ValidationError):
+        device.apply_controlled(st, standard_gate("x"), 3, 3)
+
+
+def test_launch_counter_moves(cuda_ok):
+    before = _lib.launch_count()
+    st = device.DeviceState.zeros(12)
+    device.apply_single(st, standard_gate("h"), 3)
+    import torch
+
+    torch.cuda.synchronize()
+    assert _lib.launch_count() == before + 1
+
+
+# ---- partitioned engine ---------------------------------------------------
+
+
+def test_engine_vs_reference_golden(cuda_ok):
+    z = golden("engine.npz")
+    outs = split_cases(z["meta"][:, 0], z["out"])
+    ops = z["ops"]
+    pos = 0
+    for case, ((n, k, scheme_id, nops), want) in enumerate(zip(z["meta"], outs)):
+        rows = ops[ops[:, 0] == case]
+        circ = Circuit(int(n), tuple(
+            GateOp("single" if r[2] < 0 else "controlled", gate_from_q(r[3:]), int(r[1]),
+                   None if r[2] < 0 else int(r[2])) for r in rows))
+        scheme = (SCHEME_A, SCHEME_B, chunked(2))[int(scheme_id)]
+        ds, stats = engine.run_circuit(circ, PartitionPlan(int(n), int(k)), scheme)
+        got = engine.gather(ds).amps
+        ds.close()
+        assert np.max(np.abs(got - want)) <= TOL, case
+        if scheme_id == 1:  # scheme b: Python complex arithmetic == C kernel
+            assert np.array_equal(got, want), case
+        assert [s.messages_sent_per_rank for s in stats] == list(z["msgs"][pos:pos + nops])
+        assert [s.bytes_sent_per_rank for s in stats] == list(z["bytes"][pos:pos + nops])
+        pos += nops
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_engine_partitioned_equals_single_rank(cuda_ok, k):
+    n = 16
+    circ = w.random_layer_circuit(n, 3, seed=40 + k)
+    a = w.random_state_array(np.random.default_rng(k), n)
+    want = oracle.run_ops(a.copy(), w.oracle_ops(circ), workers=8)
+    ds, stats = engine.run_circuit(circ, PartitionPlan(n, k), SCHEME_B, initial=a)
+    got = engine.gather(ds).amps
+    assert np.array_equal(got, want)
+    assert any(s.comm_required for s in stats)
+    pb = ds.peer_bytes()
+    assert all(b > 0 for b in pb)
+    ds.close()
+
+
+def test_engine_known_answers(cuda_ok):
+    # test_engine.py:87-95: X on the top qubit at n=3, k=2 swaps the halves
+    ds = engine.dist_init(PartitionPlan(3, 2), SCHEME_B,
+                          initial=np.arange(8, dtype=np.complex128))
+    engine.dist_apply_scheme_b(ds, standard_gate("x"), 2)
+    assert np.array_equal(engine.gather(ds).amps, np.array([4, 5, 6, 7, 0, 1, 2, 3], np.complex128))
+    ds.close()
+    # test_engine.py:98-109 scheme a pairing
+    ds = engine.dist_init(PartitionPlan(4, 2), SCHEME_A, initial=np.arange(16, dtype=np.complex128))
+    engine.dist_apply_scheme_a(ds, standard_gate("x"), 3)
+    want = np.array([8, 9, 10, 11, 12, 13, 14, 15, 0, 1, 2, 3, 4, 5, 6, 7], np.complex128)
+    assert np.array_equal(engine.gather(ds).amps, want)
+    ds.close()
+
+
+def test_qft_known_answer_partitioned(cuda_ok):
+    n, k = 14, 3
+    x = 12345
+    e = np.zeros(1 << n, np.complex128)
+    e[x] = 1
+    ds, _ = engine.run_circuit(w.qft_circuit(n), PartitionPlan(n, k), SCHEME_B, initial=e)
+    out = engine.gather(ds).amps
+    ds.close()
+    for y in (0, 1, 77, 4096, 16383):
+        assert abs(out[y] - oracle.qft_basis_amplitude(x, y, n)) <= TOL
+    assert abs(np.vdot(out, out).real - 1) <= 1e-12
