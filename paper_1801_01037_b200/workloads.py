@@ -46,6 +46,17 @@ def random_state_array(rng: np.random.Generator, n: int) -> np.ndarray:
     return (v / np.linalg.norm(v)).astype(np.complex128)
 
 
+def seeded_state(n: int, seed: int) -> np.ndarray:
+    """Normalized complex Gaussian that is bit-identical on every host: the
+    same PCG64 draws as random_state_array, normalised with an exactly
+    rounded sum (math.fsum) instead of BLAS, whose rounding depends on the
+    CPU's SIMD width."""
+    rng = np.random.default_rng(seed)
+    v = rng.normal(size=2**n) + 1j * rng.normal(size=2**n)
+    s = math.fsum(np.concatenate([v.real * v.real, v.imag * v.imag]).tolist())
+    return (v / math.sqrt(s)).astype(np.complex128)
+
+
 def qft_circuit(n: int) -> Circuit:
     ops = []
     h = standard_gate("H")

@@ -42,6 +42,18 @@ def gate_from_q(q):
                    complex(q[6], q[7]))
 
 
+def circuit_from_rows(n, rows):
+    """Rebuild a circuit from golden op rows [target, control|-1, q0..q7]."""
+    from paper_1801_01037_b200.core import Circuit, GateOp
+
+    ops = []
+    for r in rows:
+        t, c = int(r[0]), int(r[1])
+        g = gate_from_q(r[2:])
+        ops.append(GateOp("single", g, t) if c < 0 else GateOp("controlled", g, t, c))
+    return Circuit(int(n), tuple(ops))
+
+
 @pytest.fixture(scope="session")
 def cuda_ok():
     import torch

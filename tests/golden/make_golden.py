@@ -117,6 +117,13 @@ def engine_cases(svsim, conftest):
                 bytes=np.array(cases["bytes"]))
 
 
+def op_rows(circ) -> np.ndarray:
+    """[target, control (-1), 8 gate doubles] per op: the exact gate bits, so
+    tests never depend on the host's libm/LAPACK rounding when rebuilding."""
+    return np.array([[op.target, -1 if op.control is None else op.control, *gq(op.gate)]
+                     for op in circ.ops])
+
+
 def run_ref(svsim, amps, circ, strat):
     s = svsim.StateVector(circ.n, amps, validate=False)
     for op in circ.ops:
@@ -144,8 +151,11 @@ def main():
     seq = svsim.ExecStrategy("sequential", 1)
     q = {}
     for n in (12, 20):
-        a = w.random_state_array(np.random.default_rng(w.SEED_STATE), n)
-        out = run_ref(svsim, a.copy(), w.qft_circuit(n), seq)
+        # seeded_state: host-independent normalisation (fsum, no BLAS)
+        a = w.seeded_state(n, w.SEED_STATE)
+        circ = w.qft_circuit(n)
+        q[f"ops{n}"] = op_rows(circ)
+        out = run_ref(svsim, a.copy(), circ, seq)
         q[f"sha{n}"] = np.array(canon_sha(out))
         q[f"in_sha{n}"] = np.array(canon_sha(a))
         q[f"norm{n}"] = np.array(float(np.vdot(out, out).real))
@@ -162,6 +172,7 @@ def main():
     a[0] = 1
     out = run_ref(svsim, a, circ, svsim.ExecStrategy("parallel_collapsed", 4))
     np.savez_compressed(os.path.join(HERE, "layers.npz"), out=out, sha=np.array(canon_sha(out)),
+                        ops=op_rows(circ),
                         n=np.array(12), layers=np.array(20), seed=np.array(w.SEED_CFG2))
     print("golden fixtures written to", HERE)
 

@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import oracle
-from conftest import gate_from_q, golden, split_cases
+from conftest import circuit_from_rows, gate_from_q, golden, split_cases
 from paper_1801_01037_b200 import (
     SCHEME_A,
     SCHEME_B,
@@ -93,11 +93,13 @@ def test_every_control_target_pair_bit_exact(cuda_ok, n):
 def test_qft20_matches_reference_sha(cuda_ok):
     # config 1: QFT n=20, seeded Gaussian state; reference output hash
     z = golden("qft.npz")
-    a = w.random_state_array(np.random.default_rng(w.SEED_STATE), 20)
-    out = device.simulate(w.qft_circuit(20), a.copy(), fuse=False)
+    a = w.seeded_state(20, w.SEED_STATE)
+    assert canon_sha(a) == str(z["in_sha20"])
+    circ = circuit_from_rows(20, z["ops20"])
+    out = device.simulate(circ, a.copy(), fuse=False)
     assert canon_sha(out) == str(z["sha20"])
     assert np.array_equal(out[z["idx20"]], z["amp20"])
-    fused = device.simulate(w.qft_circuit(20), a.copy(), fuse=True)
+    fused = device.simulate(circ, a.copy(), fuse=True)
     assert np.max(np.abs(fused - out)) <= TOL
     st = device.DeviceState.from_host(fused)
     p = device.probs(st).cpu().numpy()
@@ -107,7 +109,7 @@ def test_qft20_matches_reference_sha(cuda_ok):
 
 def test_layers_matches_reference(cuda_ok):
     z = golden("layers.npz")
-    circ = w.random_layer_circuit(12, 20, seed=int(z["seed"]))
+    circ = circuit_from_rows(12, z["ops"])
     out = device.simulate(circ, None, fuse=False)
     assert canon_sha(out) == str(z["sha"])
     for strict in (True, False):
