@@ -103,6 +103,15 @@ int svb_probs(const void *amps, int64_t n_amps, double *probs, void *stream);
 int svb_exchange_own_row(void *own, const void *other, int64_t count, const double q[8],
                          int own_is_low, int cbit, int64_t index_offset, void *stream);
 
+/* Control-masked exchange (regime ii, engine.py:444-447: only indices with
+ * the local control bit set travel).  Packed index p stands for local index
+ * insert_bit(offset + p, cbit, 1).  pack: dst[p] = src[that index], p in
+ * [0, count).  own_row_packed: own[that index] = own-row update with
+ * other_packed[p]. */
+int svb_pack_ctrl(const void *src, void *dst, int64_t count, int cbit, int64_t offset, void *stream);
+int svb_exchange_own_row_packed(void *own, const void *other_packed, int64_t count, const double q[8],
+                                int own_is_low, int cbit, int64_t offset, void *stream);
+
 /* Both rows for amplitude pairs held in two slabs (lo_slab[j], hi_slab[j]),
  * j in [begin, end), masked by local bit cbit when cbit >= 0.  The fused
  * peer-memory form of a global-target exchange (one side may be a peer

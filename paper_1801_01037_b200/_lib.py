@@ -54,6 +54,8 @@ _SIGS = {
     "svb_probs": ([_vp, _i64, _vp, _vp], _int),
     "svb_exchange_own_row": ([_vp, _vp, _i64, _dp, _int, _int, _i64, _vp], _int),
     "svb_pair_update": ([_vp, _vp, _i64, _i64, _dp, _int, _vp], _int),
+    "svb_pack_ctrl": ([_vp, _vp, _i64, _int, _i64, _vp], _int),
+    "svb_exchange_own_row_packed": ([_vp, _vp, _i64, _dp, _int, _int, _i64, _vp], _int),
     "svb_host_apply_1q": ([_vp, _i64, _dp, _int], _int),
     "svb_host_apply_c1q": ([_vp, _i64, _dp, _int, _int], _int),
     "svb_host_run_ops": ([_vp, _vp, _i64, ctypes.POINTER(SvbOp), _int, ctypes.c_uint], _int),

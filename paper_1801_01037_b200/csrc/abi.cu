@@ -26,6 +26,10 @@ LaunchInfo launch_exchange_own_row(double2 *own, const double2 *other, int64_t c
                                    int own_is_low, int cbit, int64_t offset, cudaStream_t s);
 LaunchInfo launch_pair_update(double2 *lo_slab, double2 *hi_slab, int64_t begin, int64_t end,
                               const Gate &g, int cbit, cudaStream_t s);
+LaunchInfo launch_pack_ctrl(const double2 *src, double2 *dst, int64_t count, int cbit, int64_t offset,
+                            cudaStream_t s);
+LaunchInfo launch_exchange_packed(double2 *own, const double2 *other, int64_t count, const Gate &g,
+                                  int own_is_low, int cbit, int64_t offset, cudaStream_t s);
 int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsigned flags,
                    cudaStream_t s, int64_t *launches);
 int plan_passes(int n, const svb_op *ops, int nops, unsigned flags);
@@ -283,6 +287,35 @@ int svb_exchange_own_row(void *own, const void *other, int64_t count, const doub
     prof_end((cudaStream_t)stream, li);
     g_launches += li.kernels;
     SVB_CHECK_LAUNCH("svb_exchange_own_row");
+    return SVB_OK;
+}
+
+int svb_pack_ctrl(const void *src, void *dst, int64_t count, int cbit, int64_t offset, void *stream) {
+    if (!src || !dst || count < 0 || cbit < 0 || cbit > 62 || offset < 0) {
+        set_error("bad arguments to svb_pack_ctrl");
+        return SVB_EINVAL;
+    }
+    prof_begin((cudaStream_t)stream);
+    LaunchInfo li = launch_pack_ctrl((const double2 *)src, (double2 *)dst, count, cbit, offset,
+                                     (cudaStream_t)stream);
+    prof_end((cudaStream_t)stream, li);
+    g_launches += li.kernels;
+    SVB_CHECK_LAUNCH("svb_pack_ctrl");
+    return SVB_OK;
+}
+
+int svb_exchange_own_row_packed(void *own, const void *other_packed, int64_t count, const double q[8],
+                                int own_is_low, int cbit, int64_t offset, void *stream) {
+    if (!own || !other_packed || count < 0 || cbit < 0 || cbit > 62 || offset < 0) {
+        set_error("bad arguments to svb_exchange_own_row_packed");
+        return SVB_EINVAL;
+    }
+    prof_begin((cudaStream_t)stream);
+    LaunchInfo li = launch_exchange_packed((double2 *)own, (const double2 *)other_packed, count,
+                                           make_gate(q), own_is_low, cbit, offset, (cudaStream_t)stream);
+    prof_end((cudaStream_t)stream, li);
+    g_launches += li.kernels;
+    SVB_CHECK_LAUNCH("svb_exchange_own_row_packed");
     return SVB_OK;
 }
 

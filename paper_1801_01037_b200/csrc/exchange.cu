@@ -71,6 +71,44 @@ __global__ void __launch_bounds__(kXThreads) k_pair_update(double2 *lo_slab, dou
     }
 }
 
+// Control-masked exchange (regime ii, engine.py:444-447): only local indices
+// with bit cbit set take part.  Packed index p (offset + p) maps to local
+// index insert_bit(offset + p, cbit, 1).
+__global__ void __launch_bounds__(kXThreads) k_pack_ctrl(const double2 *__restrict__ src,
+                                                         double2 *__restrict__ dst, int64_t count,
+                                                         int cbit, int64_t offset) {
+    const int64_t base = int64_t(blockIdx.x) * kXThreads * kXUpt + threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < kXUpt; ++k) {
+        int64_t p = base + int64_t(k) * kXThreads;
+        if (p < count) dst[p] = src[insert_bit(offset + p, cbit, 1)];
+    }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kXThreads) k_exchange_packed(double2 *__restrict__ own,
+                                                               const double2 *__restrict__ other,
+                                                               int64_t count, Gate g, int own_is_low,
+                                                               int cbit, int64_t offset) {
+    const int64_t base = int64_t(blockIdx.x) * kXThreads * kXUpt + threadIdx.x;
+    double2 mine[kXUpt], oth[kXUpt];
+    int64_t j[kXUpt];
+#pragma unroll
+    for (int k = 0; k < kXUpt; ++k) {
+        int64_t p = base + int64_t(k) * kXThreads;
+        j[k] = p < count ? insert_bit(offset + p, cbit, 1) : -1;
+        if (j[k] >= 0) {
+            mine[k] = own[j[k]];
+            oth[k] = other[p];
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kXUpt; ++k) {
+        if (j[k] < 0) continue;
+        own[j[k]] = own_is_low ? row<KIND>(g, false, mine[k], oth[k]) : row<KIND>(g, true, oth[k], mine[k]);
+    }
+}
+
 static unsigned grid_for(int64_t count) {
     return (unsigned)((count + int64_t(kXThreads) * kXUpt - 1) / (int64_t(kXThreads) * kXUpt));
 }
@@ -90,6 +128,29 @@ LaunchInfo launch_exchange_own_row(double2 *own, const double2 *other, int64_t c
 #undef SVB_X
     // own read + write, partner chunk read (control-masked: half of each)
     return LaunchInfo{1, PROF_EXCHANGE, (cbit >= 0 ? count / 2 : count) * 48};
+}
+
+LaunchInfo launch_pack_ctrl(const double2 *src, double2 *dst, int64_t count, int cbit, int64_t offset,
+                            cudaStream_t s) {
+    if (count <= 0) return LaunchInfo{0, PROF_EXCHANGE, 0};
+    k_pack_ctrl<<<grid_for(count), kXThreads, 0, s>>>(src, dst, count, cbit, offset);
+    return LaunchInfo{1, PROF_EXCHANGE, count * 32};
+}
+
+LaunchInfo launch_exchange_packed(double2 *own, const double2 *other, int64_t count, const Gate &g,
+                                  int own_is_low, int cbit, int64_t offset, cudaStream_t s) {
+    if (count <= 0) return LaunchInfo{0, PROF_EXCHANGE, 0};
+    unsigned blocks = grid_for(count);
+#define SVB_K(K) k_exchange_packed<K><<<blocks, kXThreads, 0, s>>>(own, other, count, g, own_is_low, cbit, offset)
+    switch (g.kind) {
+        case K_REAL: SVB_K(K_REAL); break;
+        case K_DIAG: SVB_K(K_DIAG); break;
+        case K_ANTI: SVB_K(K_ANTI); break;
+        case K_RX: SVB_K(K_RX); break;
+        default: SVB_K(K_GENERAL); break;
+    }
+#undef SVB_K
+    return LaunchInfo{1, PROF_EXCHANGE, count * 48};
 }
 
 LaunchInfo launch_pair_update(double2 *lo_slab, double2 *hi_slab, int64_t begin, int64_t end,

@@ -1,0 +1,333 @@
+"""Multi-process partitioned engine: one process per GPU (torchrun / NCCL).
+
+The reference runs 2^k ranks in one process over an in-memory FIFO
+transport (engine.py:57-120, 279-341).  Here every rank is a process that
+owns one GPU and one slab of L = 2^(n-k) amplitudes in HBM; torch.distributed
+is the transport (NCCL over NVLink/NVSwitch on GPUs, gloo on CPU for tests).
+
+Per op (engine.py:483-494):
+* rank-local target: appended to a batch that runs as ONE fused
+  svb_run_ops call (multi-gate HBM passes) when the next exchange is due;
+* rank-bit target, non-diagonal gate: the paper's partner exchange with
+  partner = rank ^ 2^(t-(n-k)) (partition.py:126-137), chunk-pipelined: the
+  send/recv of chunk i+1 (torch.distributed P2P, NCCL's stream) overlaps the
+  own-row update of chunk i (svb_exchange_own_row on the compute stream) --
+  the own-row rule of scheme b (engine.py:249-254) in chunks of m
+  amplitudes as in chunked(m) (engine.py:257-272), with no zero padding;
+* local control + rank-bit target (regime ii, engine.py:444-447): only the
+  control-set half is packed, exchanged and updated (8*L bytes each way);
+* rank-bit control (regime iii, engine.py:432-443): only ranks with that bit
+  set act; a local target then needs no communication at all;
+* diagonal gate on a rank-bit target (Z S T Rz CP): no exchange -- every
+  amplitude keeps its own row, scaled by q11 (bit clear) or q22 (bit set);
+  ``elide_diagonal=False`` restores the reference's exchange for NVLink
+  accounting (SURVEY 8(d) "diagonal-gate shortcut").
+
+The compute backend is libsvb.so (CudaCompute).  Tests on CPU inject a
+checker-backed compute object; the product never falls back to one.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from .core import Circuit, Gate2x2, GateOp
+from .errors import ValidationError
+from .partition import PartitionPlan
+
+DEFAULT_CHUNK = 1 << 24  # amplitudes per pipelined message (256 MiB)
+
+
+class CudaCompute:
+    """libsvb.so kernels on this rank's GPU (torch owns buffers/streams)."""
+
+    def __init__(self, device: int | None = None):
+        import torch
+
+        from . import _lib
+
+        self.torch = torch
+        self.lib = _lib.load()
+        self._lib = _lib
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+
+    def _sp(self):
+        return ctypes.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
+
+    def zeros(self, count: int):
+        return self.torch.zeros(count, dtype=self.torch.complex128, device=self.device)
+
+    def from_numpy(self, arr: np.ndarray):
+        return self.torch.from_numpy(np.ascontiguousarray(arr)).to(self.device)
+
+    def to_numpy(self, t) -> np.ndarray:
+        return t.cpu().numpy()
+
+    def run_ops(self, slab, ops, fuse: bool = True, strict: bool = False) -> None:
+        if not ops:
+            return
+        arr, nops = self._lib.ops_array(ops)
+        flags = (self._lib.RUN_FUSE if fuse else 0) | (self._lib.RUN_STRICT_ORDER if strict else 0)
+        self._lib.check(self.lib.svb_run_ops(ctypes.c_void_p(slab.data_ptr()), slab.shape[0], arr,
+                                             nops, flags, self._sp()), "run_ops")
+
+    def pack(self, src, dst, count: int, cbit: int, offset: int) -> None:
+        self._lib.check(self.lib.svb_pack_ctrl(ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(dst.data_ptr()),
+                                               count, cbit, offset, self._sp()), "pack")
+
+    def exchange_update(self, own, other, count: int, gate: Gate2x2, own_is_low: bool,
+                        cbit: int, offset: int, own_offset: int = 0) -> None:
+        """own-row update of `count` amplitudes; cbit >= 0: `other` is packed
+        (control-set elements only) and offset is in packed index space."""
+        q = self._lib.gate_array(gate)
+        if cbit < 0:
+            ptr = ctypes.c_void_p(own.data_ptr() + 16 * own_offset)
+            self._lib.check(self.lib.svb_exchange_own_row(ptr, ctypes.c_void_p(other.data_ptr()), count, q,
+                                                          int(own_is_low), -1, 0, self._sp()), "exchange")
+        else:
+            self._lib.check(self.lib.svb_exchange_own_row_packed(
+                ctypes.c_void_p(own.data_ptr()), ctypes.c_void_p(other.data_ptr()), count, q,
+                int(own_is_low), cbit, offset, self._sp()), "exchange")
+
+    def norm2(self, slab) -> float:
+        out = ctypes.c_double()
+        self._lib.check(self.lib.svb_norm2(ctypes.c_void_p(slab.data_ptr()), slab.shape[0],
+                                           ctypes.byref(out), self._sp()), "norm2")
+        return out.value
+
+    def synchronize(self) -> None:
+        self.torch.cuda.synchronize(self.device)
+
+
+@dataclass
+class ExchangeStats:
+    exchanges: int = 0
+    elided: int = 0
+    bytes_sent: int = 0
+    bytes_recv: int = 0
+    messages: int = 0
+
+
+def _is_diag(g: Gate2x2) -> bool:
+    return complex(g.q12) == 0 and complex(g.q21) == 0
+
+
+class DistEngine:
+    """This process's rank of a 2^k-way partitioned n-qubit state."""
+
+    def __init__(self, n: int, compute=None, group=None, initial=None, chunk: int = DEFAULT_CHUNK,
+                 fuse: bool = True, elide_diagonal: bool = True):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        k = self.world.bit_length() - 1
+        if (1 << k) != self.world:
+            raise ValidationError(f"world size {self.world} is not a power of two")
+        self.plan = PartitionPlan(n, k)
+        self.n, self.k = n, k
+        self.L = self.plan.local_len
+        self.boundary = n - k
+        self.compute = compute if compute is not None else CudaCompute()
+        self.chunk = max(1, min(int(chunk), self.L))
+        self.fuse = fuse
+        self.elide_diagonal = elide_diagonal
+        self.stats = ExchangeStats()
+        if initial is not None:
+            amps = np.asarray(initial, np.complex128)
+            if amps.shape[0] != (1 << n):
+                raise ValidationError(f"initial state must have 2**{n} amplitudes")
+            self.slab = self.compute.from_numpy(amps[self.rank * self.L:(self.rank + 1) * self.L])
+        else:
+            self.slab = self.compute.zeros(self.L)
+            if self.rank == 0:
+                self.slab[0] = 1.0
+        self._pending: list[GateOp] = []
+        self._bufs = None
+
+    # -- helpers ------------------------------------------------------------
+
+    def _buffers(self, count: int, packed: bool):
+        m = min(self.chunk, count)
+        if self._bufs is None or self._bufs[0].shape[0] < m:
+            self._bufs = [self.compute.zeros(m) for _ in range(4)]  # recv x2, send x2
+        return m
+
+    def _flush(self) -> None:
+        if self._pending:
+            self.compute.run_ops(self.slab, self._pending, fuse=self.fuse)
+            self._pending = []
+
+    def _diag_local(self, g: Gate2x2, bit_set: bool, cbit: int | None) -> None:
+        """Global-target diagonal gate: scale own amplitudes by q11 or q22."""
+        s = complex(g.q22) if bit_set else complex(g.q11)
+        if s == 1:
+            return
+        d = Gate2x2(s, 0, 0, s)
+        if cbit is None:
+            self._pending.append(GateOp("single", d, 0))
+        else:
+            self._pending.append(GateOp("controlled", d, 1 if cbit == 0 else 0, cbit))
+
+    def _exchange(self, g: Gate2x2, t: int, cbit: int | None) -> None:
+        self._flush()
+        dist = self.dist
+        partner = self.rank ^ (1 << (t - self.boundary))
+        low = self.rank < partner
+        count = self.L if cbit is None else self.L // 2
+        m = self._buffers(count, cbit is not None)
+        recv = self._bufs[0:2]
+        send = self._bufs[2:4]
+        nchunks = math.ceil(count / m)
+        peer = dist.get_global_rank(self.group, partner) if self.group is not None else partner
+
+        def post(ci):
+            off = ci * m
+            cnt = min(m, count - off)
+            if cbit is None:
+                src = self.slab[off:off + cnt]
+            else:
+                self.compute.pack(self.slab, send[ci % 2], cnt, cbit, off)
+                src = send[ci % 2][:cnt]
+            ops = [dist.P2POp(dist.isend, src, peer, self.group),
+                   dist.P2POp(dist.irecv, recv[ci % 2][:cnt], peer, self.group)]
+            return dist.batch_isend_irecv(ops)
+
+        works = post(0)
+        for ci in range(nchunks):
+            nxt = post(ci + 1) if ci + 1 < nchunks else None
+            for w in works:
+                w.wait()
+            off = ci * m
+            cnt = min(m, count - off)
+            if cbit is None:
+                self.compute.exchange_update(self.slab, recv[ci % 2], cnt, g, low, -1, 0, own_offset=off)
+            else:
+                self.compute.exchange_update(self.slab, recv[ci % 2], cnt, g, low, cbit, off)
+            works = nxt
+        self.stats.exchanges += 1
+        self.stats.messages += nchunks
+        self.stats.bytes_sent += 16 * count
+        self.stats.bytes_recv += 16 * count
+
+    # -- public ---------------------------------------------------------------
+
+    def apply(self, op: GateOp) -> None:
+        """One op with the reference's regime dispatch (engine.py:488-494, 415-450)."""
+        t, c, g = op.target, op.control, op.gate
+        b = self.boundary
+        if c is not None and c >= b:
+            if not (self.rank >> (c - b)) & 1:
+                return  # regime (iii): this rank's control bit is clear
+            c = None  # acts as an uncontrolled gate on participating ranks
+        if t < b:
+            self._pending.append(GateOp("single", g, t) if c is None else GateOp("controlled", g, t, c))
+            return
+        bit_set = bool((self.rank >> (t - b)) & 1)
+        if self.elide_diagonal and _is_diag(g):
+            self._diag_local(g, bit_set, c)
+            self.stats.elided += 1
+            return
+        self._exchange(g, t, c)
+
+    def run(self, circuit: Circuit) -> "DistEngine":
+        if circuit.n != self.n:
+            raise ValidationError(f"circuit has {circuit.n} qubits, engine has {self.n}")
+        for op in circuit.ops:
+            self.apply(op)
+        self._flush()
+        return self
+
+    def norm2(self) -> float:
+        import torch
+
+        self._flush()
+        local = self.compute.norm2(self.slab)
+        dev = self.slab.device if self.slab.is_cuda else torch.device("cpu")
+        t = torch.tensor([local], dtype=torch.float64, device=dev)
+        self.dist.all_reduce(t, group=self.group)
+        return float(t.item())
+
+    def gather(self) -> np.ndarray | None:
+        """Full state on rank 0 (engine.py:188-192); None elsewhere."""
+        self._flush()
+        parts = [self.compute.zeros(self.L) for _ in range(self.world)]
+        self.dist.all_gather(parts, self.slab, group=self.group)
+        if self.rank != 0:
+            return None
+        return np.concatenate([self.compute.to_numpy(p) for p in parts])
+
+
+# ---------------------------------------------------------------------------
+# bench.py --gpus N (torchrun): weak scaling, 2^26 amplitudes per GPU
+
+
+def bench_main(args) -> None:
+    import json
+
+    import torch
+    import torch.distributed as dist
+
+    from . import _lib, workloads
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world = dist.get_rank(), dist.get_world_size()
+    k = world.bit_length() - 1
+    n = 26 + k
+    layers = int(os.environ.get("SVB_BENCH_LAYERS", "200"))
+    circuit = workloads.random_layer_circuit(n, layers)
+    nops = len(circuit.ops)
+    eng = DistEngine(n)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        eng.slab.zero_()
+        if rank == 0:
+            eng.slab[0] = 1.0
+        eng.run(circuit)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    launches0 = _lib.launch_count()
+    stats0 = (eng.stats.exchanges, eng.stats.bytes_sent)
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    norm = eng.norm2()
+    if rank == 0:
+        ex = eng.stats.exchanges - stats0[0]
+        sent = eng.stats.bytes_sent - stats0[1]
+        line = {
+            "metric": "gate applications/s", "value": round(nops * args.steps / (ms / 1e3), 1),
+            "unit": "gate_apps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded circuit, |0...0>)",
+            "config": {"workload": f"random layer circuit n={n} ({layers} layers) over {world} GPUs, "
+                                   f"2^26 amplitudes per GPU, {k} global qubits",
+                       "n_qubits": n, "global_qubits": k, "parallelism": f"state partition x{world}"},
+            "exchanges_per_step": ex / args.steps,
+            "nvlink_bytes_sent_per_gpu_per_step": sent / args.steps,
+            "gpu_launches": _lib.launch_count() - launches0,
+            "check": {"norm": norm},
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
