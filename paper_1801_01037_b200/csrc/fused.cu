@@ -44,13 +44,27 @@ LaunchInfo launch_gate(double2 *a, int64_t n_amps, const Gate &g, int t, int c, 
 constexpr int FM = 12;                   // qubits per tile
 constexpr int FTILE = 1 << FM;           // 4096 amplitudes = 64 KiB
 constexpr int FTHREADS = FTILE / 8;      // 512 threads, 8 amplitudes each per group
-constexpr int FMAXG = 144;               // gates per pass
-constexpr int FMAXGRP = 64;              // register groups per pass
+constexpr int FMAXG = 160;               // gates per pass
+constexpr int FMAXGRP = 80;              // register groups per pass
 constexpr int FMAXROWS = FTILE / 8;      // rows when flow = 3
+
+// Gate opcodes.  Non-diagonal: op = (kind * 3 + tslot) * 3 + cmode, kind in
+// FK_*, tslot the register slot of the target, cmode 0 = no slot control,
+// 1/2 = control on slot (tslot + cmode) % 3.  Diagonal: op = FOP_DIAG +
+// (tpos * 4 + cpos) * 3 + var with tpos 0..2 = slot, 3 = a thread bit;
+// cpos 0 = none, 1..3 = slot cpos-1; var 0 = general diag, 1 = q11 == 1,
+// 2 = q11 == 1 and q22 in {+-1, +-i} (exact, no arithmetic).  A control on a
+// thread bit (not a slot) is the per-thread predicate `cl`.
+enum FKind { FK_GENERAL = 0, FK_REAL = 1, FK_ANTI = 2, FK_RX = 3, FK_UANTI = 4 };
+constexpr int FOP_DIAG = 64;
 
 struct FGate {
     double2 m[4];
-    int8_t kind, d0_one, diag, tslot, tl, cl, cslot, pad;
+    uint8_t op;
+    int8_t tl;    // target local bit (diag with a thread-bit target)
+    int8_t cl;    // control local bit when it is a thread bit, else -1
+    uint8_t u;    // unit codes: bits 0-1 q12 (or q22 for diag), bits 2-3 q21
+    int32_t pad;
 };
 struct FGroup {
     int8_t pos[3];  // local bits of the 3 register slots, ascending
@@ -74,26 +88,84 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-// apply one non-diagonal gate on register slot SLOT of the 8-amplitude block
-template <int KIND, int SLOT>
-__device__ __forceinline__ void reg_gate(double2 (&v)[8], const Gate &g, int cslot, bool thread_on) {
+// x * u for u in {1, i, -1, -i} (code 0..3): exact, and equal to the
+// reference's (ac - bd, ad + bc) with u's zero component (sign of 0 aside)
+__device__ __forceinline__ double2 unit_mul(int code, double2 x) {
+    double2 r = (code & 1) ? make_double2(-x.y, x.x) : x;
+    return (code & 2) ? make_double2(-r.x, -r.y) : r;
+}
+
+template <int KIND, int S, int CS>
+__device__ __forceinline__ void nd_gate(double2 (&v)[8], const FGate &fg) {
+    Gate g;
+    g.m[0] = fg.m[0];
+    g.m[1] = fg.m[1];
+    g.m[2] = fg.m[2];
+    g.m[3] = fg.m[3];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        if (i & (1 << SLOT)) continue;
-        bool on = thread_on && (cslot < 0 || ((i >> cslot) & 1));
-        if (on) pair_both<KIND>(g, v[i], v[i | (1 << SLOT)]);
+        if (i & (1 << S)) continue;
+        if (CS >= 0 && !((i >> CS) & 1)) continue;
+        double2 &lo = v[i];
+        double2 &hi = v[i | (1 << S)];
+        if (KIND == FK_UANTI) {
+            double2 a = lo;
+            lo = unit_mul(fg.u & 3, hi);
+            hi = unit_mul((fg.u >> 2) & 3, a);
+        } else if (KIND == FK_REAL) {
+            pair_both<K_REAL>(g, lo, hi);
+        } else if (KIND == FK_ANTI) {
+            pair_both<K_ANTI>(g, lo, hi);
+        } else if (KIND == FK_RX) {
+            pair_both<K_RX>(g, lo, hi);
+        } else {
+            pair_both<K_GENERAL>(g, lo, hi);
+        }
     }
 }
 
-template <int KIND>
-__device__ __forceinline__ void reg_gate_slot(double2 (&v)[8], const Gate &g, int slot, int cslot,
-                                              bool thread_on) {
-    if (slot == 0)
-        reg_gate<KIND, 0>(v, g, cslot, thread_on);
-    else if (slot == 1)
-        reg_gate<KIND, 1>(v, g, cslot, thread_on);
-    else
-        reg_gate<KIND, 2>(v, g, cslot, thread_on);
+template <int TP, int CP, int VAR>
+__device__ __forceinline__ void diag_gate(double2 (&v)[8], const FGate &fg, int l0) {
+    const bool tb = TP == 3 ? ((l0 >> fg.tl) & 1) : false;
+    const double2 d0 = fg.m[0], d1 = fg.m[3];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        if (CP > 0 && !((i >> (CP - 1)) & 1)) continue;
+        const bool b = TP == 3 ? tb : ((i >> TP) & 1);
+        if (VAR == 0) {
+            v[i] = cmul(b ? d1 : d0, v[i]);
+        } else if (VAR == 1) {
+            if (b) v[i] = cmul(d1, v[i]);
+        } else {
+            if (b) v[i] = unit_mul(fg.u & 3, v[i]);
+        }
+    }
+}
+
+#define SVB_ND3(K, S) \
+    case ((K)*3 + (S)) * 3 + 0: nd_gate<K, S, -1>(v, fg); break; \
+    case ((K)*3 + (S)) * 3 + 1: nd_gate<K, S, ((S) + 1) % 3>(v, fg); break; \
+    case ((K)*3 + (S)) * 3 + 2: nd_gate<K, S, ((S) + 2) % 3>(v, fg); break;
+#define SVB_ND(K) SVB_ND3(K, 0) SVB_ND3(K, 1) SVB_ND3(K, 2)
+#define SVB_DG3(TP, CP) \
+    case FOP_DIAG + ((TP)*4 + (CP)) * 3 + 0: diag_gate<TP, CP, 0>(v, fg, l0); break; \
+    case FOP_DIAG + ((TP)*4 + (CP)) * 3 + 1: diag_gate<TP, CP, 1>(v, fg, l0); break; \
+    case FOP_DIAG + ((TP)*4 + (CP)) * 3 + 2: diag_gate<TP, CP, 2>(v, fg, l0); break;
+#define SVB_DG(TP) SVB_DG3(TP, 0) SVB_DG3(TP, 1) SVB_DG3(TP, 2) SVB_DG3(TP, 3)
+
+__device__ __forceinline__ void run_gate(double2 (&v)[8], const FGate &fg, int l0) {
+    switch (fg.op) {
+        SVB_ND(FK_GENERAL)
+        SVB_ND(FK_REAL)
+        SVB_ND(FK_ANTI)
+        SVB_ND(FK_RX)
+        SVB_ND(FK_UANTI)
+        SVB_DG(0)
+        SVB_DG(1)
+        SVB_DG(2)
+        SVB_DG(3)
+        default: break;
+    }
 }
 
 __global__ void __launch_bounds__(FTHREADS, 1) k_fused(double2 *__restrict__ a, int64_t ntiles,
@@ -142,7 +214,7 @@ __global__ void __launch_bounds__(FTHREADS, 1) k_fused(double2 *__restrict__ a, 
             const FGroup &G = P.groups[gi];
             const int p0 = G.pos[0], p1 = G.pos[1], p2 = G.pos[2];
             // thread's base local index: tid with zeros inserted at p0 < p1 < p2
-            int l0 = (int)insert_bit(insert_bit(insert_bit(tid, p0, 0), p1, 0), p2, 0);
+            const int l0 = (int)insert_bit(insert_bit(insert_bit(tid, p0, 0), p1, 0), p2, 0);
             int li[8];
             double2 v[8];
 #pragma unroll
@@ -150,29 +222,11 @@ __global__ void __launch_bounds__(FTHREADS, 1) k_fused(double2 *__restrict__ a, 
                 li[i] = l0 | ((i & 1) << p0) | (((i >> 1) & 1) << p1) | (((i >> 2) & 1) << p2);
                 v[i] = buf[swz(li[i])];
             }
-            for (int q = G.first; q < G.first + G.count; ++q) {
+            const int qend = G.first + G.count;
+            for (int q = G.first; q < qend; ++q) {
                 const FGate &fg = P.gates[q];
-                Gate g;
-                g.m[0] = fg.m[0];
-                g.m[1] = fg.m[1];
-                g.m[2] = fg.m[2];
-                g.m[3] = fg.m[3];
-                if (fg.diag) {
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        bool on = fg.cl < 0 || ((li[i] >> fg.cl) & 1);
-                        bool b = (li[i] >> fg.tl) & 1;
-                        if (on && (b || !fg.d0_one)) v[i] = cmul(b ? g.m[3] : g.m[0], v[i]);
-                    }
-                    continue;
-                }
-                bool thread_on = fg.cslot >= 0 || fg.cl < 0 || ((l0 >> fg.cl) & 1);
-                switch (fg.kind) {
-                    case K_REAL: reg_gate_slot<K_REAL>(v, g, fg.tslot, fg.cslot, thread_on); break;
-                    case K_ANTI: reg_gate_slot<K_ANTI>(v, g, fg.tslot, fg.cslot, thread_on); break;
-                    case K_RX: reg_gate_slot<K_RX>(v, g, fg.tslot, fg.cslot, thread_on); break;
-                    default: reg_gate_slot<K_GENERAL>(v, g, fg.tslot, fg.cslot, thread_on); break;
-                }
+                if (fg.cl >= 0 && !((l0 >> fg.cl) & 1)) continue;  // thread-bit control clear
+                run_gate(v, fg, l0);
             }
 #pragma unroll
             for (int i = 0; i < 8; ++i) buf[swz(li[i])] = v[i];
@@ -192,9 +246,6 @@ __global__ void __launch_bounds__(FTHREADS, 1) k_fused(double2 *__restrict__ a, 
 // ---------------------------------------------------------------------------
 // planner
 
-struct PlanGate {
-    int op;  // index into ops
-};
 struct PlanPass {
     uint64_t S = 0;  // global qubits in the tile
     std::vector<int> ops;
@@ -263,7 +314,21 @@ static std::vector<PlanPass> plan(int n, const svb_op *ops, int nops, bool stric
     return passes;
 }
 
-// Build the kernel descriptor for one pass; returns false if it needs > FMAXGRP groups.
+static int unit_code(double2 z) {
+    if (z.x == 1.0 && z.y == 0.0) return 0;
+    if (z.x == 0.0 && z.y == 1.0) return 1;
+    if (z.x == -1.0 && z.y == 0.0) return 2;
+    if (z.x == 0.0 && z.y == -1.0) return 3;
+    return -1;
+}
+
+struct GateMeta {
+    Gate g;
+    int tl, cl;  // local bits (cl = -1: none)
+    bool diag;
+};
+
+// Build the kernel descriptor for one pass; false if it does not fit.
 static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P) {
     memset(&P, 0, sizeof(P));
     P.flow = flow_bits();
@@ -280,65 +345,89 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P) {
         }
     }
     P.ncomp = nc;
-    // groups: consecutive gates whose non-diagonal targets use <= 3 slots
-    int g = 0;
-    int cur_slots[3], nslots = 0;
-    int grp_first = 0;
-    bool overflow = false;
-    auto close_group = [&](int upto) {
-        if (upto == grp_first) return;
-        if (P.ngroups >= FMAXGRP) {
-            overflow = true;
-            return;
-        }
-        FGroup &G = P.groups[P.ngroups++];
-        // fill unused slots with the highest local bits not already used
-        int s[3], k = 0;
-        for (int i = 0; i < nslots; ++i) s[k++] = cur_slots[i];
-        for (int b = FM - 1; k < 3 && b >= 0; --b) {
-            bool used = false;
-            for (int i = 0; i < k; ++i) used |= s[i] == b;
-            if (!used) s[k++] = b;
-        }
-        std::sort(s, s + 3);
-        for (int i = 0; i < 3; ++i) G.pos[i] = (int8_t)s[i];
-        G.first = (int16_t)grp_first;
-        G.count = (int16_t)(upto - grp_first);
-        // resolve slots of this group's gates
-        for (int q = grp_first; q < upto; ++q) {
-            FGate &fg = P.gates[q];
-            fg.tslot = fg.cslot = -1;
-            for (int i = 0; i < 3; ++i) {
-                if (s[i] == fg.tl) fg.tslot = (int8_t)i;
-                if (fg.cl >= 0 && s[i] == fg.cl) fg.cslot = (int8_t)i;
-            }
-        }
-        grp_first = upto;
-        nslots = 0;
-    };
+    if ((int)pp.ops.size() > FMAXG) return false;
+    std::vector<GateMeta> meta;
     for (int oi : pp.ops) {
         const svb_op &o = ops[oi];
-        Gate gg = make_gate(o.q);
-        FGate &fg = P.gates[g];
-        for (int i = 0; i < 4; ++i) fg.m[i] = gg.m[i];
-        fg.kind = (int8_t)gg.kind;
-        fg.d0_one = (int8_t)gg.d0_one;
-        fg.diag = (int8_t)(gg.kind == K_DIAG);
-        fg.tl = (int8_t)local_of[o.target];
-        fg.cl = (int8_t)(o.kind == 1 ? local_of[o.control] : -1);
-        if (!fg.diag) {
+        GateMeta m;
+        m.g = make_gate(o.q);
+        m.tl = local_of[o.target];
+        m.cl = o.kind == 1 ? local_of[o.control] : -1;
+        m.diag = m.g.kind == K_DIAG;
+        meta.push_back(m);
+    }
+    // groups: consecutive gates whose non-diagonal targets use <= 3 slots
+    int first = 0;
+    const int ng = (int)meta.size();
+    while (first < ng) {
+        int slots[3], ns = 0, end = first;
+        for (; end < ng; ++end) {
+            if (meta[end].diag) continue;
             bool have = false;
-            for (int i = 0; i < nslots; ++i) have |= cur_slots[i] == fg.tl;
-            if (!have) {
-                if (nslots == 3) close_group(g);
-                cur_slots[nslots++] = fg.tl;
+            for (int i = 0; i < ns; ++i) have |= slots[i] == meta[end].tl;
+            if (have) continue;
+            if (ns == 3) break;
+            slots[ns++] = meta[end].tl;
+        }
+        for (int b = FM - 1; ns < 3 && b >= 0; --b) {
+            bool used = false;
+            for (int i = 0; i < ns; ++i) used |= slots[i] == b;
+            if (!used) slots[ns++] = b;
+        }
+        std::sort(slots, slots + 3);
+        if (P.ngroups >= FMAXGRP) return false;
+        FGroup &G = P.groups[P.ngroups++];
+        for (int i = 0; i < 3; ++i) G.pos[i] = (int8_t)slots[i];
+        G.first = (int16_t)first;
+        G.count = (int16_t)(end - first);
+        auto slot_of = [&](int l) {
+            for (int i = 0; i < 3; ++i)
+                if (slots[i] == l) return i;
+            return -1;
+        };
+        for (int q = first; q < end; ++q) {
+            const GateMeta &m = meta[q];
+            FGate &fg = P.gates[q];
+            for (int i = 0; i < 4; ++i) fg.m[i] = m.g.m[i];
+            fg.tl = (int8_t)m.tl;
+            fg.u = 0;
+            int cs = m.cl >= 0 ? slot_of(m.cl) : -1;
+            fg.cl = (int8_t)(m.cl >= 0 && cs < 0 ? m.cl : -1);
+            if (m.diag) {
+                int ts = slot_of(m.tl);
+                int tpos = ts >= 0 ? ts : 3;
+                int cpos = cs >= 0 ? cs + 1 : 0;
+                int var = 0;
+                if (m.g.d0_one) {
+                    int uc = unit_code(m.g.m[3]);
+                    var = uc >= 0 ? 2 : 1;
+                    if (uc >= 0) fg.u = (uint8_t)uc;
+                }
+                fg.op = (uint8_t)(FOP_DIAG + (tpos * 4 + cpos) * 3 + var);
+            } else {
+                int ts = slot_of(m.tl);
+                int kind;
+                switch (m.g.kind) {
+                    case K_REAL: kind = FK_REAL; break;
+                    case K_ANTI: kind = FK_ANTI; break;
+                    case K_RX: kind = FK_RX; break;
+                    default: kind = FK_GENERAL; break;
+                }
+                if (m.g.kind == K_ANTI) {
+                    int u12 = unit_code(m.g.m[1]), u21 = unit_code(m.g.m[2]);
+                    if (u12 >= 0 && u21 >= 0) {
+                        kind = FK_UANTI;
+                        fg.u = (uint8_t)(u12 | (u21 << 2));
+                    }
+                }
+                int cmode = cs >= 0 ? (cs - ts + 3) % 3 : 0;
+                fg.op = (uint8_t)((kind * 3 + ts) * 3 + cmode);
             }
         }
-        ++g;
+        first = end;
     }
-    P.ngates = g;
-    close_group(g);
-    return !overflow;
+    P.ngates = ng;
+    return true;
 }
 
 static size_t fused_smem() { return 2 * FTILE * sizeof(double2) + FMAXROWS * sizeof(int64_t); }

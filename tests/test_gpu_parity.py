@@ -14,6 +14,7 @@ from paper_1801_01037_b200 import (
     SCHEME_A,
     SCHEME_B,
     Circuit,
+    Gate2x2,
     GateOp,
     PartitionPlan,
     StateVector,
@@ -130,6 +131,32 @@ def test_fused_random_layers_vs_oracle(cuda_ok, n):
         assert err <= TOL, (fuse, strict, err)
         if not fuse or strict:
             assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("n", [14, 17])
+def test_fused_every_gate_class_strict_bit_exact(cuda_ok, n):
+    # every fused opcode family: general / real / anti / Rx / unit-anti gates on
+    # any slot, controls on slots and on thread bits, diagonal gates with slot or
+    # thread targets, unit (Z, S, S-dagger) and general phases
+    rng = np.random.default_rng(300 + n)
+    pool = all_gates(rng) + [Gate2x2(1, 0, 0, -1j), Gate2x2(0, 1j, 1j, 0), Gate2x2(0, -1, 1, 0),
+                             Gate2x2(1j, 0, 0, 1), rz(0.4)]
+    ops = []
+    for _ in range(400):
+        g = pool[int(rng.integers(len(pool)))]
+        if rng.random() < 0.4:
+            c, t = rng.choice(n, size=2, replace=False)
+            ops.append(GateOp("controlled", g, int(t), int(c)))
+        else:
+            ops.append(GateOp("single", g, int(rng.integers(n))))
+    circ = Circuit(n, tuple(ops))
+    a = w.random_state_array(rng, n)
+    want = oracle.run_ops(a.copy(), w.oracle_ops(circ))
+    strict = device.simulate(circ, a.copy(), fuse=True, strict_order=True)
+    assert np.array_equal(strict, want)
+    loose = device.simulate(circ, a.copy(), fuse=True)
+    assert np.max(np.abs(loose - want)) <= TOL
+    assert device.plan_passes(n, circ, fuse=True) < len(ops)
 
 
 def test_random_reference_circuits_vs_oracle(cuda_ok):
