@@ -83,9 +83,11 @@ int svb_apply_c1q(void *amps, int64_t n_amps, const double q[8], int control, in
 int svb_run_ops(void *amps, int64_t n_amps, const svb_op *ops, int nops, unsigned flags,
                 void *stream);
 
-/* Number of HBM passes svb_run_ops would make for these ops (planner only,
- * no device work). */
-int svb_plan_passes(int n_qubits, const svb_op *ops, int nops, unsigned flags, int *passes);
+/* Number of HBM passes svb_run_ops would make for these ops, and (groups,
+ * may be NULL) the total shared-memory register groups of the fused passes.
+ * Planner only, no device work. */
+int svb_plan_passes(int n_qubits, const svb_op *ops, int nops, unsigned flags, int *passes,
+                    int *groups);
 
 /* sum |a_j|^2 -> *out (host).  Synchronises `stream`.  Replaces norm2
  * (core.py:171-174) / _dist_norm2 for one slab (engine.py:453-454). */

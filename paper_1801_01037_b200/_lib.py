@@ -49,7 +49,8 @@ _SIGS = {
     "svb_apply_1q": ([_vp, _i64, _dp, _int, _vp], _int),
     "svb_apply_c1q": ([_vp, _i64, _dp, _int, _int, _vp], _int),
     "svb_run_ops": ([_vp, _i64, ctypes.POINTER(SvbOp), _int, ctypes.c_uint, _vp], _int),
-    "svb_plan_passes": ([_int, ctypes.POINTER(SvbOp), _int, ctypes.c_uint, ctypes.POINTER(_int)], _int),
+    "svb_plan_passes": ([_int, ctypes.POINTER(SvbOp), _int, ctypes.c_uint, ctypes.POINTER(_int),
+                         ctypes.POINTER(_int)], _int),
     "svb_norm2": ([_vp, _i64, _dp, _vp], _int),
     "svb_probs": ([_vp, _i64, _vp, _vp], _int),
     "svb_exchange_own_row": ([_vp, _vp, _i64, _dp, _int, _int, _i64, _vp], _int),

@@ -32,7 +32,7 @@ LaunchInfo launch_exchange_packed(double2 *own, const double2 *other, int64_t co
                                   int own_is_low, int cbit, int64_t offset, cudaStream_t s);
 int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsigned flags,
                    cudaStream_t s, int64_t *launches);
-int plan_passes(int n, const svb_op *ops, int nops, unsigned flags);
+int plan_passes(int n, const svb_op *ops, int nops, unsigned flags, int *groups);
 
 static thread_local char g_err[512];
 std::atomic<int64_t> g_launches{0};
@@ -231,14 +231,15 @@ int svb_run_ops(void *amps, int64_t n_amps, const svb_op *ops, int nops, unsigne
     return SVB_OK;
 }
 
-int svb_plan_passes(int n_qubits, const svb_op *ops, int nops, unsigned flags, int *passes) {
+int svb_plan_passes(int n_qubits, const svb_op *ops, int nops, unsigned flags, int *passes,
+                    int *groups) {
     if (n_qubits < 1 || n_qubits > 62 || !passes) {
         set_error("bad arguments to svb_plan_passes");
         return SVB_EINVAL;
     }
     int r = check_ops(n_qubits, ops, nops);
     if (r != SVB_OK) return r;
-    *passes = plan_passes(n_qubits, ops, nops, flags);
+    *passes = plan_passes(n_qubits, ops, nops, flags, groups);
     return SVB_OK;
 }
 

@@ -446,9 +446,16 @@ static bool fuse_enabled(int n, unsigned flags) {
     return (flags & SVB_RUN_FUSE) && n >= FM + 2;
 }
 
-int plan_passes(int n, const svb_op *ops, int nops, unsigned flags) {
+int plan_passes(int n, const svb_op *ops, int nops, unsigned flags, int *groups) {
+    if (groups) *groups = 0;
     if (!fuse_enabled(n, flags)) return nops;
     auto passes = plan(n, ops, nops, flags & SVB_RUN_STRICT_ORDER);
+    if (groups) {
+        FPass P;
+        for (const PlanPass &pp : passes) {
+            if (pp.ops.size() > 1 && build_pass(n, ops, pp, P)) *groups += P.ngroups;
+        }
+    }
     return (int)passes.size();
 }
 

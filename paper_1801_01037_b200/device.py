@@ -134,15 +134,21 @@ def run_ops(s, ops, fuse: bool = True, strict_order: bool = False):
     return s
 
 
-def plan_passes(n: int, ops, fuse: bool = True, strict_order: bool = False) -> int:
+def plan_stats(n: int, ops, fuse: bool = True, strict_order: bool = False) -> tuple[int, int]:
+    """(HBM passes, shared-memory register groups) the planner makes (host only)."""
     lib = _lib.load(require_cuda=False)
     if isinstance(ops, Circuit):
         ops = ops.ops
     arr, nops = _lib.ops_array(ops)
     flags = (_lib.RUN_FUSE if fuse else 0) | (_lib.RUN_STRICT_ORDER if strict_order else 0)
-    out = ctypes.c_int(0)
-    _lib.check(lib.svb_plan_passes(int(n), arr, nops, flags, ctypes.byref(out)), "plan_passes")
-    return out.value
+    out, groups = ctypes.c_int(0), ctypes.c_int(0)
+    _lib.check(lib.svb_plan_passes(int(n), arr, nops, flags, ctypes.byref(out), ctypes.byref(groups)),
+               "plan_passes")
+    return out.value, groups.value
+
+
+def plan_passes(n: int, ops, fuse: bool = True, strict_order: bool = False) -> int:
+    return plan_stats(n, ops, fuse, strict_order)[0]
 
 
 def norm2(s) -> float:
