@@ -2,31 +2,31 @@
 //
 // run_circuit applies one gate per sweep over the state (engine.py:483-494,
 // _stride_cy.pyx:24-90): 7,800 full read+write passes for the configs[1]
-// circuit.  Here a host-side planner (plan()) packs consecutive gates whose
-// qubits fit in a set S of FM = 12 qubits into one pass; k_fused then
-// streams the state tile by tile -- a tile is the 2^12 amplitudes that share
-// all bits outside S -- through shared memory and applies every gate of the
-// pass to it before writing it back: one HBM read + one write per pass.
+// circuit.  Here a host-side planner packs gates whose qubits fit in a set S
+// of FM = 12 qubits into one pass; k_fused streams the state tile by tile --
+// a tile is the 2^12 amplitudes sharing every bit outside S -- through
+// shared memory and applies all gates of the pass before writing it back:
+// one HBM read + one HBM write per pass instead of per gate.
 //
-//  * S always contains qubits 0..flow-1, so a tile is 2^(12-flow) runs of
-//    2^flow contiguous amplitudes (flow = 4: 256 B runs) and every global
-//    load/store is a coalesced 16 B-per-lane access.
-//  * Loads are cp.async (LDGSTS, 16 B) into one of two 64 KiB tile buffers,
-//    so tile i+1 streams in while tile i is computed (1 CTA of 512 threads
-//    per SM, persistent over tiles).  Shared memory uses the 128 B XOR
-//    swizzle phys(l) = l ^ ((l >> 3) & 7) so register-group reads are
-//    bank-conflict free for any slot positions >= 3 or < 3 with lane spread.
-//  * Gates are applied in "groups": each thread owns 8 amplitudes spanning 3
-//    local bits (the group's slots); every non-diagonal gate of the group
-//    targets a slot bit and runs entirely in registers; diagonal gates
-//    (Z S T Rz CP) need no pairing and join any group; a control bit needs no
-//    slot (it is a per-register or per-thread predicate).  Shared memory is
-//    read and written once per group, not once per gate.
-//  * Gate order: gates are applied in plan order with the exact single-gate
-//    arithmetic (svb_common.cuh), so a strict-order plan is bit-identical to
-//    op-by-op application.  The default plan may hoist a gate over earlier
-//    gates on disjoint qubits (they commute); results then agree to a few ulp
-//    (tested <= 1e-12, the north-star tolerance).
+//  * S always holds qubits 0..flow-1 (flow = 4 by default), so a tile is
+//    2^(12-flow) runs of 2^flow contiguous amplitudes and every global access
+//    is a coalesced 16 B-per-lane cp.async (load) / store.
+//  * Gates run in "register groups": each of the 256 threads of a CTA holds
+//    16 amplitudes spanning 4 local bits (the group's slots).  Every
+//    non-diagonal gate of a group targets a slot, so its pair updates are
+//    register-to-register; a control bit needs no slot (it is a register mask
+//    or a per-thread predicate); diagonal gates (Z S T Rz CP) need no pairing
+//    at all.  Shared memory is read and written once per group.
+//  * The other 8 local bits index threads through a per-group map chosen so
+//    the 8 lanes of each LDS.128/STS.128 phase hit distinct 16 B bank groups
+//    under the swizzle phys(l) = l ^ fold3(l >> 3).
+//  * X / CNOT are register renames, Y / Z / S / S^dag are exact sign and
+//    re/im swaps; the rest use the exact single-gate arithmetic of
+//    svb_common.cuh.  A strict-order plan is therefore bit-identical to
+//    op-by-op application; the default plan may hoist a gate over earlier
+//    gates on disjoint qubits (they commute) and agrees to a few ulp.
+//  * Two persistent CTAs per SM (64 KiB tile each): one streams its next
+//    tile while the other computes.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -41,45 +41,48 @@ namespace svb {
 
 LaunchInfo launch_gate(double2 *a, int64_t n_amps, const Gate &g, int t, int c, cudaStream_t s);
 
-constexpr int FM = 12;                   // qubits per tile
-constexpr int FTILE = 1 << FM;           // 4096 amplitudes = 64 KiB
-constexpr int FTHREADS = FTILE / 8;      // 512 threads, 8 amplitudes each per group
-constexpr int FMAXG = 160;               // gates per pass
-constexpr int FMAXGRP = 80;              // register groups per pass
-constexpr int FMAXROWS = FTILE / 8;      // rows when flow = 3
+constexpr int FM = 12;                 // qubits per tile
+constexpr int FTILE = 1 << FM;         // 4096 amplitudes = 64 KiB
+constexpr int FSLOTS = 4;              // register bits per thread
+constexpr int FREGS = 1 << FSLOTS;     // 16 amplitudes per thread
+constexpr int FTHREADS = FTILE / FREGS;  // 256 threads
+constexpr int FTBITS = FM - FSLOTS;    // 8 thread bits
+constexpr int FMAXG = 192;             // gates per pass
+constexpr int FMAXGRP = 64;            // register groups per pass
+constexpr int FMAXROWS = FTILE / 8;    // rows when flow = 3
+constexpr int FCTAS_PER_SM = 2;
 
-// Gate opcodes.  Non-diagonal: op = (kind * 3 + tslot) * 3 + cmode, kind in
-// FK_*, tslot the register slot of the target, cmode 0 = no slot control,
-// 1/2 = control on slot (tslot + cmode) % 3.  Diagonal: op = FOP_DIAG +
-// (tpos * 4 + cpos) * 3 + var with tpos 0..2 = slot, 3 = a thread bit;
-// cpos 0 = none, 1..3 = slot cpos-1; var 0 = general diag, 1 = q11 == 1,
-// 2 = q11 == 1 and q22 in {+-1, +-i} (exact, no arithmetic).  A control on a
-// thread bit (not a slot) is the per-thread predicate `cl`.
-enum FKind { FK_GENERAL = 0, FK_REAL = 1, FK_ANTI = 2, FK_RX = 3, FK_UANTI = 4 };
-constexpr int FOP_DIAG = 64;
+// Non-diagonal opcodes: op = kind * FSLOTS + tslot.  Diagonal: FOP_DIAG + var.
+enum FKind { FK_GENERAL = 0, FK_REAL = 1, FK_ANTI = 2, FK_RX = 3, FK_UANTI = 4, FK_X = 5, FK_NKIND = 6 };
+enum FDiag { FD_GENERAL = 0, FD_D1 = 1, FD_Z = 2, FD_S = 3, FD_SDG = 4, FD_NVAR = 5 };
+constexpr int FOP_DIAG = FK_NKIND * FSLOTS;
 
 struct FGate {
     double2 m[4];
     uint8_t op;
-    int8_t tl;    // target local bit (diag with a thread-bit target)
-    int8_t cl;    // control local bit when it is a thread bit, else -1
-    uint8_t u;    // unit codes: bits 0-1 q12 (or q22 for diag), bits 2-3 q21
-    int32_t pad;
+    int8_t tl;       // diag with a thread-bit target: its local bit, else -1
+    int8_t cl;       // control on a thread bit: its local bit, else -1
+    uint8_t u;       // FK_UANTI unit codes: bits 0-1 q12, bits 2-3 q21
+    uint16_t cmask;  // registers that may change (control slot set), lo-register mask for pairs
+    uint16_t bmask;  // diag with a slot target: registers whose target bit is 1
 };
 struct FGroup {
-    int8_t pos[3];  // local bits of the 3 register slots, ascending
-    int8_t pad;
+    int8_t pos[FSLOTS];  // slot -> local bit
+    int8_t tmap[FTBITS]; // thread bit -> local bit
     int16_t first, count;
 };
 struct FPass {
     int ngates, ngroups, ncomp, flow;
-    int8_t comp[64];        // tile-index bit j -> global qubit comp[j]
-    int8_t rowbit[FM];      // local bit flow+j -> global qubit rowbit[j]
+    int8_t comp[64];      // tile-index bit j -> global qubit comp[j]
+    int8_t rowbit[FM];    // local bit flow+j -> global qubit rowbit[j]
     FGroup groups[FMAXGRP];
     FGate gates[FMAXG];
 };
 
-__device__ __forceinline__ int swz(int l) { return l ^ ((l >> 3) & 7); }
+// 16 B-granular XOR swizzle: bits 3-5, 6-8, 9-11 fold into bits 0-2, so local
+// bit j moves the 16 B chunk inside a 128 B line along axis (j mod 3).
+__host__ __device__ __forceinline__ int fold3(int x) { return (x ^ (x >> 3) ^ (x >> 6)) & 7; }
+__device__ __forceinline__ int swz(int l) { return l ^ fold3(l >> 3); }
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
     unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -88,91 +91,94 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-// x * u for u in {1, i, -1, -i} (code 0..3): exact, and equal to the
-// reference's (ac - bd, ad + bc) with u's zero component (sign of 0 aside)
+// x * u for u in {1, i, -1, -i} (code 0..3): exact, equal to the reference's
+// (ac - bd, ad + bc) up to the sign of zero
 __device__ __forceinline__ double2 unit_mul(int code, double2 x) {
     double2 r = (code & 1) ? make_double2(-x.y, x.x) : x;
     return (code & 2) ? make_double2(-r.x, -r.y) : r;
 }
 
-template <int KIND, int S, int CS>
-__device__ __forceinline__ void nd_gate(double2 (&v)[8], const FGate &fg) {
-    Gate g;
-    g.m[0] = fg.m[0];
-    g.m[1] = fg.m[1];
-    g.m[2] = fg.m[2];
-    g.m[3] = fg.m[3];
+template <int KIND, int S>
+__device__ __forceinline__ void nd_gate(double2 (&v)[FREGS], const FGate &fg) {
+    const unsigned cm = fg.cmask;
+    double2 q11 = make_double2(0, 0), q12 = q11, q21 = q11, q22 = q11;
+    if (KIND != FK_X && KIND != FK_UANTI) {
+        q11 = fg.m[0];
+        q12 = fg.m[1];
+        q21 = fg.m[2];
+        q22 = fg.m[3];
+    }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < FREGS; ++i) {
         if (i & (1 << S)) continue;
-        if (CS >= 0 && !((i >> CS) & 1)) continue;
+        if (!((cm >> i) & 1)) continue;
         double2 &lo = v[i];
         double2 &hi = v[i | (1 << S)];
-        if (KIND == FK_UANTI) {
-            double2 a = lo;
+        if (KIND == FK_X) {
+            double2 t = lo;
+            lo = hi;
+            hi = t;
+        } else if (KIND == FK_UANTI) {
+            double2 t = lo;
             lo = unit_mul(fg.u & 3, hi);
-            hi = unit_mul((fg.u >> 2) & 3, a);
+            hi = unit_mul((fg.u >> 2) & 3, t);
         } else if (KIND == FK_REAL) {
-            pair_both<K_REAL>(g, lo, hi);
+            pair_both_c<K_REAL>(q11, q12, q21, q22, lo, hi);
         } else if (KIND == FK_ANTI) {
-            pair_both<K_ANTI>(g, lo, hi);
+            pair_both_c<K_ANTI>(q11, q12, q21, q22, lo, hi);
         } else if (KIND == FK_RX) {
-            pair_both<K_RX>(g, lo, hi);
+            pair_both_c<K_RX>(q11, q12, q21, q22, lo, hi);
         } else {
-            pair_both<K_GENERAL>(g, lo, hi);
+            pair_both_c<K_GENERAL>(q11, q12, q21, q22, lo, hi);
         }
     }
 }
 
-template <int TP, int CP, int VAR>
-__device__ __forceinline__ void diag_gate(double2 (&v)[8], const FGate &fg, int l0) {
-    const bool tb = TP == 3 ? ((l0 >> fg.tl) & 1) : false;
+template <int VAR>
+__device__ __forceinline__ void diag_gate(double2 (&v)[FREGS], const FGate &fg, int l0) {
+    unsigned bm = fg.bmask;
+    if (fg.tl >= 0) bm = ((l0 >> fg.tl) & 1) ? 0xffffu : 0u;
+    const unsigned am = VAR == FD_GENERAL ? fg.cmask : (fg.cmask & bm);
     const double2 d0 = fg.m[0], d1 = fg.m[3];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        if (CP > 0 && !((i >> (CP - 1)) & 1)) continue;
-        const bool b = TP == 3 ? tb : ((i >> TP) & 1);
-        if (VAR == 0) {
-            v[i] = cmul(b ? d1 : d0, v[i]);
-        } else if (VAR == 1) {
-            if (b) v[i] = cmul(d1, v[i]);
-        } else {
-            if (b) v[i] = unit_mul(fg.u & 3, v[i]);
-        }
+    for (int i = 0; i < FREGS; ++i) {
+        if (!((am >> i) & 1)) continue;
+        if (VAR == FD_GENERAL) v[i] = cmul(((bm >> i) & 1) ? d1 : d0, v[i]);
+        if (VAR == FD_D1) v[i] = cmul(d1, v[i]);
+        if (VAR == FD_Z) v[i] = make_double2(-v[i].x, -v[i].y);
+        if (VAR == FD_S) v[i] = make_double2(-v[i].y, v[i].x);
+        if (VAR == FD_SDG) v[i] = make_double2(v[i].y, -v[i].x);
     }
 }
 
-#define SVB_ND3(K, S) \
-    case ((K)*3 + (S)) * 3 + 0: nd_gate<K, S, -1>(v, fg); break; \
-    case ((K)*3 + (S)) * 3 + 1: nd_gate<K, S, ((S) + 1) % 3>(v, fg); break; \
-    case ((K)*3 + (S)) * 3 + 2: nd_gate<K, S, ((S) + 2) % 3>(v, fg); break;
-#define SVB_ND(K) SVB_ND3(K, 0) SVB_ND3(K, 1) SVB_ND3(K, 2)
-#define SVB_DG3(TP, CP) \
-    case FOP_DIAG + ((TP)*4 + (CP)) * 3 + 0: diag_gate<TP, CP, 0>(v, fg, l0); break; \
-    case FOP_DIAG + ((TP)*4 + (CP)) * 3 + 1: diag_gate<TP, CP, 1>(v, fg, l0); break; \
-    case FOP_DIAG + ((TP)*4 + (CP)) * 3 + 2: diag_gate<TP, CP, 2>(v, fg, l0); break;
-#define SVB_DG(TP) SVB_DG3(TP, 0) SVB_DG3(TP, 1) SVB_DG3(TP, 2) SVB_DG3(TP, 3)
+#define SVB_ND(K)                                         \
+    case (K)*FSLOTS + 0: nd_gate<K, 0>(v, fg); break; \
+    case (K)*FSLOTS + 1: nd_gate<K, 1>(v, fg); break; \
+    case (K)*FSLOTS + 2: nd_gate<K, 2>(v, fg); break; \
+    case (K)*FSLOTS + 3: nd_gate<K, 3>(v, fg); break;
 
-__device__ __forceinline__ void run_gate(double2 (&v)[8], const FGate &fg, int l0) {
+__device__ __forceinline__ void run_gate(double2 (&v)[FREGS], const FGate &fg, int l0) {
     switch (fg.op) {
         SVB_ND(FK_GENERAL)
         SVB_ND(FK_REAL)
         SVB_ND(FK_ANTI)
         SVB_ND(FK_RX)
         SVB_ND(FK_UANTI)
-        SVB_DG(0)
-        SVB_DG(1)
-        SVB_DG(2)
-        SVB_DG(3)
+        SVB_ND(FK_X)
+        case FOP_DIAG + FD_GENERAL: diag_gate<FD_GENERAL>(v, fg, l0); break;
+        case FOP_DIAG + FD_D1: diag_gate<FD_D1>(v, fg, l0); break;
+        case FOP_DIAG + FD_Z: diag_gate<FD_Z>(v, fg, l0); break;
+        case FOP_DIAG + FD_S: diag_gate<FD_S>(v, fg, l0); break;
+        case FOP_DIAG + FD_SDG: diag_gate<FD_SDG>(v, fg, l0); break;
         default: break;
     }
 }
 
-__global__ void __launch_bounds__(FTHREADS, 1) k_fused(double2 *__restrict__ a, int64_t ntiles,
-                                                       const __grid_constant__ FPass P) {
+__global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__restrict__ a, int64_t ntiles,
+                                                                  const __grid_constant__ FPass P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double2 *tiles = reinterpret_cast<double2 *>(smem_raw);  // [2][FTILE]
-    int64_t *rowoff = reinterpret_cast<int64_t *>(smem_raw + 2 * FTILE * sizeof(double2));
+    double2 *buf = reinterpret_cast<double2 *>(smem_raw);
+    int64_t *rowoff = reinterpret_cast<int64_t *>(smem_raw + FTILE * sizeof(double2));
     const int tid = threadIdx.x;
     const int flow = P.flow;
     const int nrows = FTILE >> flow;
@@ -185,42 +191,30 @@ __global__ void __launch_bounds__(FTHREADS, 1) k_fused(double2 *__restrict__ a, 
     }
     __syncthreads();
 
-    auto tile_base = [&](int64_t tix) {
-        int64_t b = 0;
+    for (int64_t tix = blockIdx.x; tix < ntiles; tix += gridDim.x) {
+        int64_t base = 0;
         for (int j = 0; j < P.ncomp; ++j)
-            if ((tix >> j) & 1) b |= int64_t(1) << P.comp[j];
-        return b;
-    };
-    auto issue_load = [&](int64_t tix, double2 *buf) {
-        const int64_t base = tile_base(tix);
+            if ((tix >> j) & 1) base |= int64_t(1) << P.comp[j];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < FREGS; ++k) {
             int e = tid + k * FTHREADS;
             cp_async16(&buf[swz(e)], &a[base + rowoff[e >> flow] + (e & colmask)]);
         }
         cp_async_commit();
-    };
-
-    int64_t tix = blockIdx.x;
-    if (tix < ntiles) issue_load(tix, tiles);
-    for (int it = 0; tix < ntiles; ++it, tix += gridDim.x) {
-        double2 *buf = tiles + (it & 1) * FTILE;
         cp_async_wait_all();
-        __syncthreads();  // tile `tix` resident; previous tile's buffer free
-        const int64_t next = tix + gridDim.x;
-        if (next < ntiles) issue_load(next, tiles + ((it + 1) & 1) * FTILE);
+        __syncthreads();
 
         for (int gi = 0; gi < P.ngroups; ++gi) {
             const FGroup &G = P.groups[gi];
-            const int p0 = G.pos[0], p1 = G.pos[1], p2 = G.pos[2];
-            // thread's base local index: tid with zeros inserted at p0 < p1 < p2
-            const int l0 = (int)insert_bit(insert_bit(insert_bit(tid, p0, 0), p1, 0), p2, 0);
-            int li[8];
-            double2 v[8];
+            int l0 = 0;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                li[i] = l0 | ((i & 1) << p0) | (((i >> 1) & 1) << p1) | (((i >> 2) & 1) << p2);
-                v[i] = buf[swz(li[i])];
+            for (int j = 0; j < FTBITS; ++j) l0 |= ((tid >> j) & 1) << G.tmap[j];
+            const int d0 = 1 << G.pos[0], d1 = 1 << G.pos[1], d2 = 1 << G.pos[2], d3 = 1 << G.pos[3];
+            double2 v[FREGS];
+#pragma unroll
+            for (int i = 0; i < FREGS; ++i) {
+                int l = l0 | ((i & 1) ? d0 : 0) | ((i & 2) ? d1 : 0) | ((i & 4) ? d2 : 0) | ((i & 8) ? d3 : 0);
+                v[i] = buf[swz(l)];
             }
             const int qend = G.first + G.count;
             for (int q = G.first; q < qend; ++q) {
@@ -228,19 +222,29 @@ __global__ void __launch_bounds__(FTHREADS, 1) k_fused(double2 *__restrict__ a, 
                 if (fg.cl >= 0 && !((l0 >> fg.cl) & 1)) continue;  // thread-bit control clear
                 run_gate(v, fg, l0);
             }
+            // recompute (not keep) the 16 addresses: holding them across the
+            // gate loop costs 16 registers and forces spills
+            int l0s = l0;
+            asm volatile("" : "+r"(l0s));
+            int e0 = 1 << G.pos[0], e1 = 1 << G.pos[1], e2 = 1 << G.pos[2], e3 = 1 << G.pos[3];
+            asm volatile("" : "+r"(e0), "+r"(e1), "+r"(e2), "+r"(e3));
 #pragma unroll
-            for (int i = 0; i < 8; ++i) buf[swz(li[i])] = v[i];
+            for (int i = 0; i < FREGS; ++i) {
+                int l = l0s | ((i & 1) ? e0 : 0) | ((i & 2) ? e1 : 0) | ((i & 4) ? e2 : 0) | ((i & 8) ? e3 : 0);
+                buf[swz(l)] = v[i];
+            }
             __syncthreads();
         }
 
-        const int64_t base = tile_base(tix);
+        int64_t base_s = base;  // recompute store addresses rather than keep 16 live
+        asm volatile("" : "+l"(base_s));
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < FREGS; ++k) {
             int e = tid + k * FTHREADS;
-            a[base + rowoff[e >> flow] + (e & colmask)] = buf[swz(e)];
+            a[base_s + rowoff[e >> flow] + (e & colmask)] = buf[swz(e)];
         }
+        __syncthreads();  // buffer free for the next tile's loads
     }
-    cp_async_wait_all();
 }
 
 // ---------------------------------------------------------------------------
@@ -262,10 +266,6 @@ static int flow_bits() {
     return f;
 }
 
-static bool is_diag(const svb_op &o) {
-    return o.q[2] == 0.0 && o.q[3] == 0.0 && o.q[4] == 0.0 && o.q[5] == 0.0;
-}
-
 static uint64_t op_mask(const svb_op &o) {
     uint64_t m = uint64_t(1) << o.target;
     if (o.kind == 1) m |= uint64_t(1) << o.control;
@@ -277,21 +277,19 @@ static uint64_t op_mask(const svb_op &o) {
 // it shares no qubit with any skipped op (so every qubit keeps its order).
 static std::vector<PlanPass> plan(int n, const svb_op *ops, int nops, bool strict) {
     std::vector<PlanPass> passes;
-    const int flow = flow_bits();
-    const uint64_t low = (uint64_t(1) << flow) - 1;
+    const uint64_t low = (uint64_t(1) << flow_bits()) - 1;
+    const uint64_t all = n >= 64 ? ~uint64_t(0) : ((uint64_t(1) << n) - 1);
     std::vector<char> done(nops, 0);
     int first = 0;
-    const int window = 4096;
+    const int window = 8192;
     while (first < nops) {
         PlanPass p;
         p.S = low;
         uint64_t blocked = 0;
-        int ngroups_est = 0;
-        (void)ngroups_est;
         for (int i = first; i < nops && i < first + window; ++i) {
             if (done[i]) continue;
             uint64_t m = op_mask(ops[i]);
-            bool fits = (m & blocked) == 0 && popc(p.S | m) <= FM && (int)p.ops.size() < FMAXG - 8;
+            bool fits = (m & blocked) == 0 && popc(p.S | m) <= FM && (int)p.ops.size() < FMAXG;
             if (fits) {
                 p.S |= m;
                 p.ops.push_back(i);
@@ -299,15 +297,14 @@ static std::vector<PlanPass> plan(int n, const svb_op *ops, int nops, bool stric
             } else {
                 if (strict) break;
                 blocked |= m;
-                if (popc(blocked | p.S) >= n) {
-                    // every qubit is either in S or blocked: nothing later can join
-                    bool any_free = false;
-                    (void)any_free;
+                if ((blocked | p.S) == all && popc(p.S) == FM) {
+                    // nothing outside S can join and every S qubit is blocked or
+                    // free; keep scanning only while S-internal ops remain possible
+                    if ((blocked & p.S) == p.S) break;
                 }
             }
         }
         while (first < nops && done[first]) ++first;
-        // pad S to exactly FM qubits (lowest unused qubits)
         for (int q = 0; q < n && popc(p.S) < FM; ++q) p.S |= uint64_t(1) << q;
         passes.push_back(std::move(p));
     }
@@ -322,14 +319,48 @@ static int unit_code(double2 z) {
     return -1;
 }
 
+// registers (0..15) whose slot-s bit is set
+static unsigned slot_pattern(int s) {
+    unsigned m = 0;
+    for (int i = 0; i < FREGS; ++i)
+        if ((i >> s) & 1) m |= 1u << i;
+    return m;
+}
+
 struct GateMeta {
     Gate g;
     int tl, cl;  // local bits (cl = -1: none)
     bool diag;
 };
 
+// Thread-bit -> local-bit map for a group: the 3 lowest thread bits (which
+// vary across the 8 lanes of an LDS.128 phase) go to non-slot local bits
+// with distinct (bit mod 3) so the swizzle spreads them over 8 chunks.
+static void thread_map(const int *slots, int8_t *tmap) {
+    bool is_slot[FM] = {};
+    for (int i = 0; i < FSLOTS; ++i) is_slot[slots[i]] = true;
+    std::vector<int> free_bits;
+    for (int b = 0; b < FM; ++b)
+        if (!is_slot[b]) free_bits.push_back(b);
+    int pick[3] = {-1, -1, -1};
+    for (int r = 0; r < 3; ++r)
+        for (int b : free_bits)
+            if (b % 3 == r) {
+                pick[r] = b;
+                break;
+            }
+    std::vector<int> order;
+    if (pick[0] >= 0 && pick[1] >= 0 && pick[2] >= 0) {
+        order = {pick[0], pick[1], pick[2]};
+        std::sort(order.begin(), order.end());
+    }
+    for (int b : free_bits)
+        if (std::find(order.begin(), order.end(), b) == order.end()) order.push_back(b);
+    for (int j = 0; j < FTBITS; ++j) tmap[j] = (int8_t)order[j];
+}
+
 // Build the kernel descriptor for one pass; false if it does not fit.
-static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P) {
+static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, bool strict) {
     memset(&P, 0, sizeof(P));
     P.flow = flow_bits();
     int local_of[64];
@@ -356,54 +387,111 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P) {
         m.diag = m.g.kind == K_DIAG;
         meta.push_back(m);
     }
-    // groups: consecutive gates whose non-diagonal targets use <= 3 slots
-    int first = 0;
+    // Order gates into register groups.  strict: keep pass order and cut a
+    // group when a 5th distinct target appears.  Otherwise repeatedly pick
+    // up to 4 target slots greedily from the ready gates (all earlier gates
+    // on shared qubits already placed) and take every ready gate they allow.
     const int ng = (int)meta.size();
-    while (first < ng) {
-        int slots[3], ns = 0, end = first;
-        for (; end < ng; ++end) {
-            if (meta[end].diag) continue;
-            bool have = false;
-            for (int i = 0; i < ns; ++i) have |= slots[i] == meta[end].tl;
-            if (have) continue;
-            if (ns == 3) break;
-            slots[ns++] = meta[end].tl;
+    std::vector<int> order;
+    std::vector<std::pair<int, int>> groups;  // [first, end) in `order`
+    std::vector<std::vector<int>> group_slots;
+    if (strict) {
+        int first = 0;
+        while (first < ng) {
+            std::vector<int> sl;
+            int end = first;
+            for (; end < ng; ++end) {
+                if (meta[end].diag) continue;
+                if (std::find(sl.begin(), sl.end(), meta[end].tl) != sl.end()) continue;
+                if ((int)sl.size() == FSLOTS) break;
+                sl.push_back(meta[end].tl);
+            }
+            for (int q = first; q < end; ++q) order.push_back(q);
+            groups.push_back({first, end});
+            group_slots.push_back(sl);
+            first = end;
         }
-        for (int b = FM - 1; ns < 3 && b >= 0; --b) {
+    } else {
+        std::vector<char> placed(ng, 0);
+        int left = ng;
+        while (left > 0) {
+            std::vector<int> sl;
+            int gfirst = (int)order.size();
+            bool progress = true;
+            while (progress) {
+                progress = false;
+                uint64_t blocked = 0;  // local bits touched by an unplaced earlier gate
+                for (int q = 0; q < ng; ++q) {
+                    if (placed[q]) continue;
+                    const GateMeta &m = meta[q];
+                    uint64_t bits = (uint64_t(1) << m.tl) | (m.cl >= 0 ? uint64_t(1) << m.cl : 0);
+                    bool ready = (bits & blocked) == 0;
+                    bool fits = m.diag || std::find(sl.begin(), sl.end(), m.tl) != sl.end() ||
+                                (int)sl.size() < FSLOTS;
+                    if (ready && fits) {
+                        if (!m.diag && std::find(sl.begin(), sl.end(), m.tl) == sl.end()) sl.push_back(m.tl);
+                        placed[q] = 1;
+                        order.push_back(q);
+                        --left;
+                        progress = true;
+                    } else {
+                        blocked |= bits;
+                    }
+                }
+            }
+            groups.push_back({gfirst, (int)order.size()});
+            group_slots.push_back(sl);
+        }
+    }
+    if ((int)groups.size() > FMAXGRP) return false;
+    P.ngroups = (int)groups.size();
+    P.ngates = ng;
+    for (int gi = 0; gi < P.ngroups; ++gi) {
+        int slots[FSLOTS];
+        int ns = 0;
+        for (int s : group_slots[gi]) slots[ns++] = s;
+        for (int b = FM - 1; ns < FSLOTS && b >= 0; --b) {
             bool used = false;
             for (int i = 0; i < ns; ++i) used |= slots[i] == b;
             if (!used) slots[ns++] = b;
         }
-        std::sort(slots, slots + 3);
-        if (P.ngroups >= FMAXGRP) return false;
-        FGroup &G = P.groups[P.ngroups++];
-        for (int i = 0; i < 3; ++i) G.pos[i] = (int8_t)slots[i];
-        G.first = (int16_t)first;
-        G.count = (int16_t)(end - first);
+        std::sort(slots, slots + FSLOTS);
+        FGroup &G = P.groups[gi];
+        for (int i = 0; i < FSLOTS; ++i) G.pos[i] = (int8_t)slots[i];
+        thread_map(slots, G.tmap);
+        G.first = (int16_t)groups[gi].first;
+        G.count = (int16_t)(groups[gi].second - groups[gi].first);
         auto slot_of = [&](int l) {
-            for (int i = 0; i < 3; ++i)
+            for (int i = 0; i < FSLOTS; ++i)
                 if (slots[i] == l) return i;
             return -1;
         };
-        for (int q = first; q < end; ++q) {
-            const GateMeta &m = meta[q];
-            FGate &fg = P.gates[q];
+        for (int k = groups[gi].first; k < groups[gi].second; ++k) {
+            const GateMeta &m = meta[order[k]];
+            FGate &fg = P.gates[k];
             for (int i = 0; i < 4; ++i) fg.m[i] = m.g.m[i];
-            fg.tl = (int8_t)m.tl;
             fg.u = 0;
+            fg.tl = -1;
+            fg.bmask = 0;
             int cs = m.cl >= 0 ? slot_of(m.cl) : -1;
             fg.cl = (int8_t)(m.cl >= 0 && cs < 0 ? m.cl : -1);
+            fg.cmask = (uint16_t)(cs >= 0 ? slot_pattern(cs) : 0xffffu);
             if (m.diag) {
                 int ts = slot_of(m.tl);
-                int tpos = ts >= 0 ? ts : 3;
-                int cpos = cs >= 0 ? cs + 1 : 0;
-                int var = 0;
+                if (ts >= 0)
+                    fg.bmask = (uint16_t)slot_pattern(ts);
+                else
+                    fg.tl = (int8_t)m.tl;
+                int var = FD_GENERAL;
                 if (m.g.d0_one) {
-                    int uc = unit_code(m.g.m[3]);
-                    var = uc >= 0 ? 2 : 1;
-                    if (uc >= 0) fg.u = (uint8_t)uc;
+                    switch (unit_code(m.g.m[3])) {
+                        case 2: var = FD_Z; break;
+                        case 1: var = FD_S; break;
+                        case 3: var = FD_SDG; break;
+                        default: var = FD_D1; break;
+                    }
                 }
-                fg.op = (uint8_t)(FOP_DIAG + (tpos * 4 + cpos) * 3 + var);
+                fg.op = (uint8_t)(FOP_DIAG + var);
             } else {
                 int ts = slot_of(m.tl);
                 int kind;
@@ -415,22 +503,23 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P) {
                 }
                 if (m.g.kind == K_ANTI) {
                     int u12 = unit_code(m.g.m[1]), u21 = unit_code(m.g.m[2]);
-                    if (u12 >= 0 && u21 >= 0) {
+                    if (u12 == 0 && u21 == 0) {
+                        kind = FK_X;
+                    } else if (u12 >= 0 && u21 >= 0) {
                         kind = FK_UANTI;
                         fg.u = (uint8_t)(u12 | (u21 << 2));
                     }
                 }
-                int cmode = cs >= 0 ? (cs - ts + 3) % 3 : 0;
-                fg.op = (uint8_t)((kind * 3 + ts) * 3 + cmode);
+                // pair loops visit lo registers (slot bit clear) whose control holds
+                fg.cmask = (uint16_t)(fg.cmask & ~slot_pattern(ts));
+                fg.op = (uint8_t)(kind * FSLOTS + ts);
             }
         }
-        first = end;
     }
-    P.ngates = ng;
     return true;
 }
 
-static size_t fused_smem() { return 2 * FTILE * sizeof(double2) + FMAXROWS * sizeof(int64_t); }
+static size_t fused_smem() { return FTILE * sizeof(double2) + FMAXROWS * sizeof(int64_t); }
 
 static int fused_grid(int64_t ntiles) {
     static int sms = [] {
@@ -439,22 +528,20 @@ static int fused_grid(int64_t ntiles) {
         cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
         return v;
     }();
-    return (int)std::min<int64_t>(ntiles, sms);
+    return (int)std::min<int64_t>(ntiles, int64_t(sms) * FCTAS_PER_SM);
 }
 
-static bool fuse_enabled(int n, unsigned flags) {
-    return (flags & SVB_RUN_FUSE) && n >= FM + 2;
-}
+static bool fuse_enabled(int n, unsigned flags) { return (flags & SVB_RUN_FUSE) && n >= FM + 2; }
 
 int plan_passes(int n, const svb_op *ops, int nops, unsigned flags, int *groups) {
     if (groups) *groups = 0;
     if (!fuse_enabled(n, flags)) return nops;
-    auto passes = plan(n, ops, nops, flags & SVB_RUN_STRICT_ORDER);
+    const bool strict = flags & SVB_RUN_STRICT_ORDER;
+    auto passes = plan(n, ops, nops, strict);
     if (groups) {
         FPass P;
-        for (const PlanPass &pp : passes) {
-            if (pp.ops.size() > 1 && build_pass(n, ops, pp, P)) *groups += P.ngroups;
-        }
+        for (const PlanPass &pp : passes)
+            if (pp.ops.size() > 1 && build_pass(n, ops, pp, P, strict)) *groups += P.ngroups;
     }
     return (int)passes.size();
 }
@@ -478,15 +565,16 @@ int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsi
         cudaFuncSetAttribute(k_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem());
         attr_set = true;
     }
-    auto passes = plan(n, ops, nops, flags & SVB_RUN_STRICT_ORDER);
+    const bool strict = flags & SVB_RUN_STRICT_ORDER;
+    auto passes = plan(n, ops, nops, strict);
     const int64_t ntiles = n_amps >> FM;
-    FPass P;  // ~11 KiB, passed by value as a __grid_constant__ kernel parameter
+    FPass P;  // ~17 KiB, passed by value as a __grid_constant__ kernel parameter
     for (const PlanPass &pp : passes) {
         if (pp.ops.size() == 1) {
             single(ops[pp.ops[0]]);
             continue;
         }
-        if (!build_pass(n, ops, pp, P)) {
+        if (!build_pass(n, ops, pp, P, strict)) {
             for (int oi : pp.ops) single(ops[oi]);
             continue;
         }

@@ -83,6 +83,29 @@ __device__ __forceinline__ double2 row(const Gate &g, bool hi_row, double2 lo, d
     return cadd(rmul(ca.x, lo), imul(cb.y, hi));
 }
 
+// Both rows with the coefficients passed by value (keeps them in registers).
+template <int KIND>
+__device__ __forceinline__ void pair_both_c(double2 q11, double2 q12, double2 q21, double2 q22,
+                                            double2 &lo, double2 &hi) {
+    const double2 a = lo, b = hi;
+    if (KIND == K_GENERAL) {
+        lo = cadd(cmul(q11, a), cmul(q12, b));
+        hi = cadd(cmul(q21, a), cmul(q22, b));
+    } else if (KIND == K_REAL) {
+        lo = cadd(rmul(q11.x, a), rmul(q12.x, b));
+        hi = cadd(rmul(q21.x, a), rmul(q22.x, b));
+    } else if (KIND == K_DIAG) {
+        lo = cmul(q11, a);
+        hi = cmul(q22, b);
+    } else if (KIND == K_ANTI) {
+        lo = cmul(q12, b);
+        hi = cmul(q21, a);
+    } else {  // K_RX
+        lo = cadd(rmul(q11.x, a), imul(q12.y, b));
+        hi = cadd(imul(q21.y, a), rmul(q22.x, b));
+    }
+}
+
 template <int KIND>
 __device__ __forceinline__ void pair_both(const Gate &g, double2 &lo, double2 &hi) {
     double2 a = lo, b = hi;
