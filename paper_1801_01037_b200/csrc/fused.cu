@@ -52,19 +52,23 @@ constexpr int FMAXGRP = 64;            // register groups per pass
 constexpr int FMAXROWS = FTILE / 8;    // rows when flow = 3
 constexpr int FCTAS_PER_SM = 2;
 
-// Non-diagonal opcodes: op = kind * FSLOTS + tslot.  Diagonal: FOP_DIAG + var.
-enum FKind { FK_GENERAL = 0, FK_REAL = 1, FK_ANTI = 2, FK_RX = 3, FK_UANTI = 4, FK_X = 5, FK_NKIND = 6 };
-enum FDiag { FD_GENERAL = 0, FD_D1 = 1, FD_Z = 2, FD_S = 3, FD_SDG = 4, FD_NVAR = 5 };
-constexpr int FOP_DIAG = FK_NKIND * FSLOTS;
+// Opcodes.  Non-diagonal: op = (kind * FSLOTS + tslot) * 2 + ctrl.
+// Diagonal: FOP_DIAG + (var * (FSLOTS + 1) + tpos) * 2 + ctrl, tpos = FSLOTS
+// meaning the target is a thread bit (one factor for all 16 registers).
+// ctrl = 1: a control on a slot, applied through the register mask cmask; a
+// control on a thread bit is the per-thread predicate `cl`.
+enum FKind { FK_GENERAL = 0, FK_REAL, FK_ANTI, FK_RX, FK_UANTI, FK_X, FK_Y, FK_NKIND };
+enum FDiag { FD_GENERAL = 0, FD_D1, FD_Z, FD_S, FD_SDG, FD_NVAR };
+constexpr int FOP_DIAG = FK_NKIND * FSLOTS * 2;
 
 struct FGate {
     double2 m[4];
     uint8_t op;
-    int8_t tl;       // diag with a thread-bit target: its local bit, else -1
+    int8_t tl;       // diag with a thread-bit target: its local bit
     int8_t cl;       // control on a thread bit: its local bit, else -1
     uint8_t u;       // FK_UANTI unit codes: bits 0-1 q12, bits 2-3 q21
-    uint16_t cmask;  // registers that may change (control slot set), lo-register mask for pairs
-    uint16_t bmask;  // diag with a slot target: registers whose target bit is 1
+    uint16_t cmask;  // ctrl = 1: registers (pairs: lo registers) the control allows
+    uint16_t pad;
 };
 struct FGroup {
     int8_t pos[FSLOTS];  // slot -> local bit
@@ -80,9 +84,10 @@ struct FPass {
 };
 
 // 16 B-granular XOR swizzle: bits 3-5, 6-8, 9-11 fold into bits 0-2, so local
-// bit j moves the 16 B chunk inside a 128 B line along axis (j mod 3).
+// bit j moves the 16 B chunk inside a 128 B line along axis (j mod 3).  It is
+// linear over XOR, so swz(l0 | d) = swz(l0) ^ swz(d) for disjoint bits.
 __host__ __device__ __forceinline__ int fold3(int x) { return (x ^ (x >> 3) ^ (x >> 6)) & 7; }
-__device__ __forceinline__ int swz(int l) { return l ^ fold3(l >> 3); }
+__host__ __device__ __forceinline__ int swz(int l) { return l ^ fold3(l >> 3); }
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
     unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -98,11 +103,11 @@ __device__ __forceinline__ double2 unit_mul(int code, double2 x) {
     return (code & 2) ? make_double2(-r.x, -r.y) : r;
 }
 
-template <int KIND, int S>
+template <int KIND, int S, int CTRL>
 __device__ __forceinline__ void nd_gate(double2 (&v)[FREGS], const FGate &fg) {
     const unsigned cm = fg.cmask;
     double2 q11 = make_double2(0, 0), q12 = q11, q21 = q11, q22 = q11;
-    if (KIND != FK_X && KIND != FK_UANTI) {
+    if (KIND != FK_X && KIND != FK_Y && KIND != FK_UANTI) {
         q11 = fg.m[0];
         q12 = fg.m[1];
         q21 = fg.m[2];
@@ -111,15 +116,17 @@ __device__ __forceinline__ void nd_gate(double2 (&v)[FREGS], const FGate &fg) {
 #pragma unroll
     for (int i = 0; i < FREGS; ++i) {
         if (i & (1 << S)) continue;
-        if (!((cm >> i) & 1)) continue;
+        if (CTRL && !((cm >> i) & 1)) continue;
         double2 &lo = v[i];
         double2 &hi = v[i | (1 << S)];
+        const double2 t = lo;
         if (KIND == FK_X) {
-            double2 t = lo;
             lo = hi;
             hi = t;
+        } else if (KIND == FK_Y) {  // lo' = -i*hi, hi' = i*lo
+            lo = make_double2(hi.y, -hi.x);
+            hi = make_double2(-t.y, t.x);
         } else if (KIND == FK_UANTI) {
-            double2 t = lo;
             lo = unit_mul(fg.u & 3, hi);
             hi = unit_mul((fg.u >> 2) & 3, t);
         } else if (KIND == FK_REAL) {
@@ -134,28 +141,38 @@ __device__ __forceinline__ void nd_gate(double2 (&v)[FREGS], const FGate &fg) {
     }
 }
 
-template <int VAR>
+template <int VAR, int TP, int CTRL>
 __device__ __forceinline__ void diag_gate(double2 (&v)[FREGS], const FGate &fg, int l0) {
-    unsigned bm = fg.bmask;
-    if (fg.tl >= 0) bm = ((l0 >> fg.tl) & 1) ? 0xffffu : 0u;
-    const unsigned am = VAR == FD_GENERAL ? fg.cmask : (fg.cmask & bm);
+    const unsigned cm = fg.cmask;
     const double2 d0 = fg.m[0], d1 = fg.m[3];
+    bool tb = false;
+    if (TP == FSLOTS) {
+        tb = (l0 >> fg.tl) & 1;
+        if (VAR != FD_GENERAL && !tb) return;  // q11 == 1: the |0> half is untouched
+    }
+    const double2 f = (TP == FSLOTS && VAR == FD_GENERAL) ? (tb ? d1 : d0) : d1;
 #pragma unroll
     for (int i = 0; i < FREGS; ++i) {
-        if (!((am >> i) & 1)) continue;
-        if (VAR == FD_GENERAL) v[i] = cmul(((bm >> i) & 1) ? d1 : d0, v[i]);
-        if (VAR == FD_D1) v[i] = cmul(d1, v[i]);
-        if (VAR == FD_Z) v[i] = make_double2(-v[i].x, -v[i].y);
-        if (VAR == FD_S) v[i] = make_double2(-v[i].y, v[i].x);
-        if (VAR == FD_SDG) v[i] = make_double2(v[i].y, -v[i].x);
+        if (CTRL && !((cm >> i) & 1)) continue;
+        const bool b = TP == FSLOTS ? true : ((i >> TP) & 1);
+        if (VAR != FD_GENERAL && !b) continue;
+        double2 &x = v[i];
+        if (VAR == FD_GENERAL) x = cmul(TP == FSLOTS ? f : (b ? d1 : d0), x);
+        if (VAR == FD_D1) x = cmul(f, x);
+        if (VAR == FD_Z) x = make_double2(-x.x, -x.y);
+        if (VAR == FD_S) x = make_double2(-x.y, x.x);
+        if (VAR == FD_SDG) x = make_double2(x.y, -x.x);
     }
 }
 
-#define SVB_ND(K)                                         \
-    case (K)*FSLOTS + 0: nd_gate<K, 0>(v, fg); break; \
-    case (K)*FSLOTS + 1: nd_gate<K, 1>(v, fg); break; \
-    case (K)*FSLOTS + 2: nd_gate<K, 2>(v, fg); break; \
-    case (K)*FSLOTS + 3: nd_gate<K, 3>(v, fg); break;
+#define SVB_ND2(K, S) \
+    case ((K)*FSLOTS + (S)) * 2 + 0: nd_gate<K, S, 0>(v, fg); break; \
+    case ((K)*FSLOTS + (S)) * 2 + 1: nd_gate<K, S, 1>(v, fg); break;
+#define SVB_ND(K) SVB_ND2(K, 0) SVB_ND2(K, 1) SVB_ND2(K, 2) SVB_ND2(K, 3)
+#define SVB_DG2(V, T) \
+    case FOP_DIAG + ((V) * (FSLOTS + 1) + (T)) * 2 + 0: diag_gate<V, T, 0>(v, fg, l0); break; \
+    case FOP_DIAG + ((V) * (FSLOTS + 1) + (T)) * 2 + 1: diag_gate<V, T, 1>(v, fg, l0); break;
+#define SVB_DG(V) SVB_DG2(V, 0) SVB_DG2(V, 1) SVB_DG2(V, 2) SVB_DG2(V, 3) SVB_DG2(V, 4)
 
 __device__ __forceinline__ void run_gate(double2 (&v)[FREGS], const FGate &fg, int l0) {
     switch (fg.op) {
@@ -165,11 +182,12 @@ __device__ __forceinline__ void run_gate(double2 (&v)[FREGS], const FGate &fg, i
         SVB_ND(FK_RX)
         SVB_ND(FK_UANTI)
         SVB_ND(FK_X)
-        case FOP_DIAG + FD_GENERAL: diag_gate<FD_GENERAL>(v, fg, l0); break;
-        case FOP_DIAG + FD_D1: diag_gate<FD_D1>(v, fg, l0); break;
-        case FOP_DIAG + FD_Z: diag_gate<FD_Z>(v, fg, l0); break;
-        case FOP_DIAG + FD_S: diag_gate<FD_S>(v, fg, l0); break;
-        case FOP_DIAG + FD_SDG: diag_gate<FD_SDG>(v, fg, l0); break;
+        SVB_ND(FK_Y)
+        SVB_DG(FD_GENERAL)
+        SVB_DG(FD_D1)
+        SVB_DG(FD_Z)
+        SVB_DG(FD_S)
+        SVB_DG(FD_SDG)
         default: break;
     }
 }
@@ -209,30 +227,26 @@ __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__res
             int l0 = 0;
 #pragma unroll
             for (int j = 0; j < FTBITS; ++j) l0 |= ((tid >> j) & 1) << G.tmap[j];
-            const int d0 = 1 << G.pos[0], d1 = 1 << G.pos[1], d2 = 1 << G.pos[2], d3 = 1 << G.pos[3];
+            // register i lives at swz(l0 | dep(i)) = swz(l0) ^ XOR of swz(slot bits)
+            const int a0 = swz(l0);
+            const int s0 = swz(1 << G.pos[0]), s1 = swz(1 << G.pos[1]);
+            const int s2 = swz(1 << G.pos[2]), s3 = swz(1 << G.pos[3]);
             double2 v[FREGS];
 #pragma unroll
-            for (int i = 0; i < FREGS; ++i) {
-                int l = l0 | ((i & 1) ? d0 : 0) | ((i & 2) ? d1 : 0) | ((i & 4) ? d2 : 0) | ((i & 8) ? d3 : 0);
-                v[i] = buf[swz(l)];
-            }
+            for (int i = 0; i < FREGS; ++i)
+                v[i] = buf[a0 ^ ((i & 1) ? s0 : 0) ^ ((i & 2) ? s1 : 0) ^ ((i & 4) ? s2 : 0) ^ ((i & 8) ? s3 : 0)];
             const int qend = G.first + G.count;
             for (int q = G.first; q < qend; ++q) {
                 const FGate &fg = P.gates[q];
                 if (fg.cl >= 0 && !((l0 >> fg.cl) & 1)) continue;  // thread-bit control clear
                 run_gate(v, fg, l0);
             }
-            // recompute (not keep) the 16 addresses: holding them across the
-            // gate loop costs 16 registers and forces spills
-            int l0s = l0;
-            asm volatile("" : "+r"(l0s));
-            int e0 = 1 << G.pos[0], e1 = 1 << G.pos[1], e2 = 1 << G.pos[2], e3 = 1 << G.pos[3];
-            asm volatile("" : "+r"(e0), "+r"(e1), "+r"(e2), "+r"(e3));
+            // recompute (not keep) the addresses: 16 more live registers spill
+            int b0 = a0, t0 = s0, t1 = s1, t2 = s2, t3 = s3;
+            asm volatile("" : "+r"(b0), "+r"(t0), "+r"(t1), "+r"(t2), "+r"(t3));
 #pragma unroll
-            for (int i = 0; i < FREGS; ++i) {
-                int l = l0s | ((i & 1) ? e0 : 0) | ((i & 2) ? e1 : 0) | ((i & 4) ? e2 : 0) | ((i & 8) ? e3 : 0);
-                buf[swz(l)] = v[i];
-            }
+            for (int i = 0; i < FREGS; ++i)
+                buf[b0 ^ ((i & 1) ? t0 : 0) ^ ((i & 2) ? t1 : 0) ^ ((i & 4) ? t2 : 0) ^ ((i & 8) ? t3 : 0)] = v[i];
             __syncthreads();
         }
 
@@ -472,16 +486,14 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
             for (int i = 0; i < 4; ++i) fg.m[i] = m.g.m[i];
             fg.u = 0;
             fg.tl = -1;
-            fg.bmask = 0;
+            fg.pad = 0;
             int cs = m.cl >= 0 ? slot_of(m.cl) : -1;
             fg.cl = (int8_t)(m.cl >= 0 && cs < 0 ? m.cl : -1);
             fg.cmask = (uint16_t)(cs >= 0 ? slot_pattern(cs) : 0xffffu);
             if (m.diag) {
                 int ts = slot_of(m.tl);
-                if (ts >= 0)
-                    fg.bmask = (uint16_t)slot_pattern(ts);
-                else
-                    fg.tl = (int8_t)m.tl;
+                int tpos = ts >= 0 ? ts : FSLOTS;
+                fg.tl = (int8_t)m.tl;
                 int var = FD_GENERAL;
                 if (m.g.d0_one) {
                     switch (unit_code(m.g.m[3])) {
@@ -491,7 +503,7 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
                         default: var = FD_D1; break;
                     }
                 }
-                fg.op = (uint8_t)(FOP_DIAG + var);
+                fg.op = (uint8_t)(FOP_DIAG + (var * (FSLOTS + 1) + tpos) * 2 + (cs >= 0 ? 1 : 0));
             } else {
                 int ts = slot_of(m.tl);
                 int kind;
@@ -505,6 +517,8 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
                     int u12 = unit_code(m.g.m[1]), u21 = unit_code(m.g.m[2]);
                     if (u12 == 0 && u21 == 0) {
                         kind = FK_X;
+                    } else if (u12 == 3 && u21 == 1) {
+                        kind = FK_Y;
                     } else if (u12 >= 0 && u21 >= 0) {
                         kind = FK_UANTI;
                         fg.u = (uint8_t)(u12 | (u21 << 2));
@@ -512,7 +526,7 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
                 }
                 // pair loops visit lo registers (slot bit clear) whose control holds
                 fg.cmask = (uint16_t)(fg.cmask & ~slot_pattern(ts));
-                fg.op = (uint8_t)(kind * FSLOTS + ts);
+                fg.op = (uint8_t)((kind * FSLOTS + ts) * 2 + (cs >= 0 ? 1 : 0));
             }
         }
     }
