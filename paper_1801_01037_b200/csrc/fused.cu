@@ -174,20 +174,32 @@ __device__ __forceinline__ void diag_gate(double2 (&v)[FREGS], const FGate &fg, 
     case FOP_DIAG + ((V) * (FSLOTS + 1) + (T)) * 2 + 1: diag_gate<V, T, 1>(v, fg, l0); break;
 #define SVB_DG(V) SVB_DG2(V, 0) SVB_DG2(V, 1) SVB_DG2(V, 2) SVB_DG2(V, 3) SVB_DG2(V, 4)
 
+// Register-permuting ops (X, Y, unit phases) as their own cases make every
+// switch arm end with v[] in different physical registers, and ptxas then
+// re-shuffles all 64 registers at the loop head on EVERY gate.  With
+// SVB_FUSED_PERM_OPS 0 they run through the arithmetic arms instead (still
+// exact: products with +-1 / +-i are exact).
+#ifndef SVB_FUSED_PERM_OPS
+#define SVB_FUSED_PERM_OPS 0
+#endif
+constexpr bool kPermOps = SVB_FUSED_PERM_OPS != 0;
+
 __device__ __forceinline__ void run_gate(double2 (&v)[FREGS], const FGate &fg, int l0) {
     switch (fg.op) {
         SVB_ND(FK_GENERAL)
         SVB_ND(FK_REAL)
         SVB_ND(FK_ANTI)
         SVB_ND(FK_RX)
+#if SVB_FUSED_PERM_OPS
         SVB_ND(FK_UANTI)
         SVB_ND(FK_X)
         SVB_ND(FK_Y)
-        SVB_DG(FD_GENERAL)
-        SVB_DG(FD_D1)
         SVB_DG(FD_Z)
         SVB_DG(FD_S)
         SVB_DG(FD_SDG)
+#endif
+        SVB_DG(FD_GENERAL)
+        SVB_DG(FD_D1)
         default: break;
     }
 }
@@ -496,7 +508,7 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
                 fg.tl = (int8_t)m.tl;
                 int var = FD_GENERAL;
                 if (m.g.d0_one) {
-                    switch (unit_code(m.g.m[3])) {
+                    switch (kPermOps ? unit_code(m.g.m[3]) : -1) {
                         case 2: var = FD_Z; break;
                         case 1: var = FD_S; break;
                         case 3: var = FD_SDG; break;
@@ -513,7 +525,7 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
                     case K_RX: kind = FK_RX; break;
                     default: kind = FK_GENERAL; break;
                 }
-                if (m.g.kind == K_ANTI) {
+                if (kPermOps && m.g.kind == K_ANTI) {
                     int u12 = unit_code(m.g.m[1]), u21 = unit_code(m.g.m[2]);
                     if (u12 == 0 && u21 == 0) {
                         kind = FK_X;
