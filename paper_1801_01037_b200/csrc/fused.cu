@@ -74,6 +74,10 @@ struct FGroup {
     int8_t pos[FSLOTS];  // slot -> local bit
     int8_t tmap[FTBITS]; // thread bit -> local bit
     int16_t first, count;
+    // X / CNOT gates of the group, as the affine bit map P(l) = M l ^ mb they
+    // induce on local indices: applied for free by storing register l at P(l)
+    int16_t mb;
+    int16_t mcol[FM];    // column j of M = P(e_j) ^ mb
 };
 struct FPass {
     int ngates, ngroups, ncomp, flow;
@@ -194,10 +198,10 @@ __device__ __forceinline__ void run_gate(double2 (&v)[FREGS], const FGate &fg, i
         SVB_ND(FK_UANTI)
         SVB_ND(FK_X)
         SVB_ND(FK_Y)
-        SVB_DG(FD_Z)
         SVB_DG(FD_S)
         SVB_DG(FD_SDG)
 #endif
+        SVB_DG(FD_Z)  // negation in place: no register renaming
         SVB_DG(FD_GENERAL)
         SVB_DG(FD_D1)
         default: break;
@@ -253,9 +257,17 @@ __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__res
                 if (fg.cl >= 0 && !((l0 >> fg.cl) & 1)) continue;  // thread-bit control clear
                 run_gate(v, fg, l0);
             }
-            // recompute (not keep) the addresses: 16 more live registers spill
-            int b0 = a0, t0 = s0, t1 = s1, t2 = s2, t3 = s3;
-            asm volatile("" : "+r"(b0), "+r"(t0), "+r"(t1), "+r"(t2), "+r"(t3));
+            // Store register l at P(l) = M l ^ mb (identity unless the group
+            // ends with X/CNOT gates).  P is linear, so P(l0 | dep(i)) =
+            // P(l0) ^ M dep(i); recomputing (not keeping) the addresses saves
+            // 16 live registers.
+            int ml0 = G.mb;
+#pragma unroll
+            for (int j = 0; j < FTBITS; ++j)
+                if ((tid >> j) & 1) ml0 ^= G.mcol[G.tmap[j]];
+            const int b0 = swz(ml0);
+            const int t0 = swz(G.mcol[G.pos[0]]), t1 = swz(G.mcol[G.pos[1]]);
+            const int t2 = swz(G.mcol[G.pos[2]]), t3 = swz(G.mcol[G.pos[3]]);
 #pragma unroll
             for (int i = 0; i < FREGS; ++i)
                 buf[b0 ^ ((i & 1) ? t0 : 0) ^ ((i & 2) ? t1 : 0) ^ ((i & 4) ? t2 : 0) ^ ((i & 8) ? t3 : 0)] = v[i];
@@ -288,6 +300,16 @@ static int flow_bits() {
         const char *e = getenv("SVB_FUSE_FLOW");
         int v = e ? atoi(e) : 4;
         return v < 3 ? 3 : (v > 5 ? 5 : v);
+    }();
+    return f;
+}
+
+// SVB_FUSE_PERM=0 runs X/CNOT through the arithmetic arms instead of folding
+// them into the store map (both exact; for measurement).
+static bool perm_fold() {
+    static bool f = [] {
+        const char *e = getenv("SVB_FUSE_PERM");
+        return !(e && atoi(e) == 0);
     }();
     return f;
 }
@@ -357,6 +379,7 @@ struct GateMeta {
     Gate g;
     int tl, cl;  // local bits (cl = -1: none)
     bool diag;
+    bool perm;
 };
 
 // Thread-bit -> local-bit map for a group: the 3 lowest thread bits (which
@@ -411,71 +434,110 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
         m.tl = local_of[o.target];
         m.cl = o.kind == 1 ? local_of[o.control] : -1;
         m.diag = m.g.kind == K_DIAG;
+        // X and CNOT are bit permutations: folded into the group's store map
+        m.perm = perm_fold() && m.g.kind == K_ANTI && unit_code(m.g.m[1]) == 0 &&
+                 unit_code(m.g.m[2]) == 0;
         meta.push_back(m);
     }
-    // Order gates into register groups.  strict: keep pass order and cut a
-    // group when a 5th distinct target appears.  Otherwise repeatedly pick
-    // up to 4 target slots greedily from the ready gates (all earlier gates
-    // on shared qubits already placed) and take every ready gate they allow.
+    // Order gates into register groups.  A group holds at most 4 target slots
+    // of arithmetic gates; its X/CNOT gates are deferred to the group's end
+    // (applied by the store map), which is exact because a pure permutation
+    // commutes with every gate on other qubits -- so once a permutation is
+    // deferred, later gates sharing its qubits wait for the next group.
+    // strict: pass order, cut at a 5th slot or a permutation conflict.
+    // Otherwise: repeated scans taking every ready gate (all earlier gates on
+    // its qubits already placed) that fits.
     const int ng = (int)meta.size();
-    std::vector<int> order;
-    std::vector<std::pair<int, int>> groups;  // [first, end) in `order`
-    std::vector<std::vector<int>> group_slots;
+    struct GroupPlan {
+        std::vector<int> gates;  // indices into meta, execution order (no perms)
+        std::vector<int> slots;
+        int mcol[FM];
+        int mb = 0;
+        uint64_t permq = 0;
+    };
+    std::vector<GroupPlan> gps;
+    auto new_group = [&]() {
+        GroupPlan g;
+        for (int j = 0; j < FM; ++j) g.mcol[j] = 1 << j;
+        gps.push_back(g);
+        return &gps.back();
+    };
+    auto defer_perm = [&](GroupPlan &g, const GateMeta &m) {
+        // compose C(x) = x ^ (x_c << t) (X: c = -1, always) after the current map
+        auto C = [&](int x) { return (m.cl < 0 || ((x >> m.cl) & 1)) ? x ^ (1 << m.tl) : x; };
+        auto Cl = [&](int x) { return (m.cl >= 0 && ((x >> m.cl) & 1)) ? x ^ (1 << m.tl) : x; };
+        for (int j = 0; j < FM; ++j) g.mcol[j] = Cl(g.mcol[j]);
+        g.mb = C(g.mb);
+        g.permq |= (uint64_t(1) << m.tl) | (m.cl >= 0 ? uint64_t(1) << m.cl : 0);
+    };
+    auto gbits = [&](const GateMeta &m) {
+        return (uint64_t(1) << m.tl) | (m.cl >= 0 ? uint64_t(1) << m.cl : 0);
+    };
+    auto fits = [&](const GroupPlan &g, const GateMeta &m) {
+        return m.diag || std::find(g.slots.begin(), g.slots.end(), m.tl) != g.slots.end() ||
+               (int)g.slots.size() < FSLOTS;
+    };
+    auto take = [&](GroupPlan &g, int q) {
+        const GateMeta &m = meta[q];
+        if (m.perm) {
+            defer_perm(g, m);
+            return;
+        }
+        if (!m.diag && std::find(g.slots.begin(), g.slots.end(), m.tl) == g.slots.end()) g.slots.push_back(m.tl);
+        g.gates.push_back(q);
+    };
     if (strict) {
-        int first = 0;
-        while (first < ng) {
-            std::vector<int> sl;
-            int end = first;
-            for (; end < ng; ++end) {
-                if (meta[end].diag) continue;
-                if (std::find(sl.begin(), sl.end(), meta[end].tl) != sl.end()) continue;
-                if ((int)sl.size() == FSLOTS) break;
-                sl.push_back(meta[end].tl);
-            }
-            for (int q = first; q < end; ++q) order.push_back(q);
-            groups.push_back({first, end});
-            group_slots.push_back(sl);
-            first = end;
+        GroupPlan *g = new_group();
+        for (int q = 0; q < ng; ++q) {
+            const GateMeta &m = meta[q];
+            bool ok = m.perm || ((gbits(m) & g->permq) == 0 && fits(*g, m));
+            if (!ok) g = new_group();
+            take(*g, q);
         }
     } else {
         std::vector<char> placed(ng, 0);
         int left = ng;
         while (left > 0) {
-            std::vector<int> sl;
-            int gfirst = (int)order.size();
-            bool progress = true;
-            while (progress) {
-                progress = false;
+            GroupPlan *g = new_group();
+            // allow_perm = false: take arithmetic gates only (an unplaced
+            // permutation blocks its qubits like any unplaced gate); only when
+            // that stalls, admit permutations -- each one closes its qubits
+            // for the rest of the group, so they go last.
+            auto scan = [&](bool allow_perm) {
+                bool progress = false;
                 uint64_t blocked = 0;  // local bits touched by an unplaced earlier gate
                 for (int q = 0; q < ng; ++q) {
                     if (placed[q]) continue;
                     const GateMeta &m = meta[q];
-                    uint64_t bits = (uint64_t(1) << m.tl) | (m.cl >= 0 ? uint64_t(1) << m.cl : 0);
-                    bool ready = (bits & blocked) == 0;
-                    bool fits = m.diag || std::find(sl.begin(), sl.end(), m.tl) != sl.end() ||
-                                (int)sl.size() < FSLOTS;
-                    if (ready && fits) {
-                        if (!m.diag && std::find(sl.begin(), sl.end(), m.tl) == sl.end()) sl.push_back(m.tl);
+                    const uint64_t bits = gbits(m);
+                    bool ok = (bits & blocked) == 0 &&
+                              (m.perm ? allow_perm : ((bits & g->permq) == 0 && fits(*g, m)));
+                    if (ok) {
+                        take(*g, q);
                         placed[q] = 1;
-                        order.push_back(q);
                         --left;
                         progress = true;
                     } else {
                         blocked |= bits;
                     }
                 }
+                return progress;
+            };
+            for (;;) {
+                while (scan(false)) {
+                }
+                if (!scan(true)) break;
             }
-            groups.push_back({gfirst, (int)order.size()});
-            group_slots.push_back(sl);
         }
     }
-    if ((int)groups.size() > FMAXGRP) return false;
-    P.ngroups = (int)groups.size();
-    P.ngates = ng;
+    if ((int)gps.size() > FMAXGRP) return false;
+    P.ngroups = (int)gps.size();
+    int k0 = 0;
     for (int gi = 0; gi < P.ngroups; ++gi) {
+        const GroupPlan &gp = gps[gi];
         int slots[FSLOTS];
         int ns = 0;
-        for (int s : group_slots[gi]) slots[ns++] = s;
+        for (int s : gp.slots) slots[ns++] = s;
         for (int b = FM - 1; ns < FSLOTS && b >= 0; --b) {
             bool used = false;
             for (int i = 0; i < ns; ++i) used |= slots[i] == b;
@@ -485,16 +547,18 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
         FGroup &G = P.groups[gi];
         for (int i = 0; i < FSLOTS; ++i) G.pos[i] = (int8_t)slots[i];
         thread_map(slots, G.tmap);
-        G.first = (int16_t)groups[gi].first;
-        G.count = (int16_t)(groups[gi].second - groups[gi].first);
+        G.first = (int16_t)k0;
+        G.count = (int16_t)gp.gates.size();
+        G.mb = (int16_t)gp.mb;
+        for (int j = 0; j < FM; ++j) G.mcol[j] = (int16_t)gp.mcol[j];
         auto slot_of = [&](int l) {
             for (int i = 0; i < FSLOTS; ++i)
                 if (slots[i] == l) return i;
             return -1;
         };
-        for (int k = groups[gi].first; k < groups[gi].second; ++k) {
-            const GateMeta &m = meta[order[k]];
-            FGate &fg = P.gates[k];
+        for (size_t gk = 0; gk < gp.gates.size(); ++gk) {
+            const GateMeta &m = meta[gp.gates[gk]];
+            FGate &fg = P.gates[k0 + gk];
             for (int i = 0; i < 4; ++i) fg.m[i] = m.g.m[i];
             fg.u = 0;
             fg.tl = -1;
@@ -508,12 +572,15 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
                 fg.tl = (int8_t)m.tl;
                 int var = FD_GENERAL;
                 if (m.g.d0_one) {
-                    switch (kPermOps ? unit_code(m.g.m[3]) : -1) {
-                        case 2: var = FD_Z; break;
-                        case 1: var = FD_S; break;
-                        case 3: var = FD_SDG; break;
-                        default: var = FD_D1; break;
-                    }
+                    const int uc = unit_code(m.g.m[3]);
+                    if (uc == 2)
+                        var = FD_Z;
+                    else if (kPermOps && uc == 1)
+                        var = FD_S;
+                    else if (kPermOps && uc == 3)
+                        var = FD_SDG;
+                    else
+                        var = FD_D1;
                 }
                 fg.op = (uint8_t)(FOP_DIAG + (var * (FSLOTS + 1) + tpos) * 2 + (cs >= 0 ? 1 : 0));
             } else {
@@ -541,7 +608,9 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
                 fg.op = (uint8_t)((kind * FSLOTS + ts) * 2 + (cs >= 0 ? 1 : 0));
             }
         }
+        k0 += (int)gp.gates.size();
     }
+    P.ngates = k0;
     return true;
 }
 
