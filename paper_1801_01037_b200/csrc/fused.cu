@@ -78,6 +78,7 @@ struct FGroup {
     // induce on local indices: applied for free by storing register l at P(l)
     int16_t mb;
     int16_t mcol[FM];    // column j of M = P(e_j) ^ mb
+    int16_t perm;        // P is not the identity
 };
 struct FPass {
     int ngates, ngroups, ncomp, flow;
@@ -261,6 +262,8 @@ __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__res
             // ends with X/CNOT gates).  P is linear, so P(l0 | dep(i)) =
             // P(l0) ^ M dep(i); recomputing (not keeping) the addresses saves
             // 16 live registers.
+            // a permuted store writes slots other threads load: wait for all loads
+            if (G.perm) __syncthreads();
             int ml0 = G.mb;
 #pragma unroll
             for (int j = 0; j < FTBITS; ++j)
@@ -550,7 +553,11 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
         G.first = (int16_t)k0;
         G.count = (int16_t)gp.gates.size();
         G.mb = (int16_t)gp.mb;
-        for (int j = 0; j < FM; ++j) G.mcol[j] = (int16_t)gp.mcol[j];
+        G.perm = (int16_t)(gp.mb != 0);
+        for (int j = 0; j < FM; ++j) {
+            G.mcol[j] = (int16_t)gp.mcol[j];
+            if (gp.mcol[j] != (1 << j)) G.perm = 1;
+        }
         auto slot_of = [&](int l) {
             for (int i = 0; i < FSLOTS; ++i)
                 if (slots[i] == l) return i;
