@@ -105,6 +105,11 @@ int svb_probs(const void *amps, int64_t n_amps, double *probs, void *stream);
 int svb_exchange_own_row(void *own, const void *other, int64_t count, const double q[8],
                          int own_is_low, int cbit, int64_t index_offset, void *stream);
 
+/* Qubit relabeling, out of place: dst[p] = src[s] where bit j of p is bit
+ * phys_to_logical[j] of s (svsim.layout.permute_state, layout.py:71-83). */
+int svb_permute_qubits(const void *src, void *dst, int64_t n_amps, const int *phys_to_logical, int n,
+                       void *stream);
+
 /* Control-masked exchange (regime ii, engine.py:444-447: only indices with
  * the local control bit set travel).  Packed index p stands for local index
  * insert_bit(offset + p, cbit, 1).  pack: dst[p] = src[that index], p in

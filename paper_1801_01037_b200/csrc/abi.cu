@@ -22,6 +22,7 @@ LaunchInfo launch_gate(double2 *a, int64_t n_amps, const Gate &g, int t, int c, 
 int launch_norm2(const double2 *a, int64_t n, double *scratch, cudaStream_t s);
 int norm_scratch_doubles();
 int launch_probs(const double2 *a, int64_t n, double *p, cudaStream_t s);
+int launch_permute(const double2 *src, double2 *dst, int64_t n, const int *p2l, int nbits, cudaStream_t s);
 LaunchInfo launch_exchange_own_row(double2 *own, const double2 *other, int64_t count, const Gate &g,
                                    int own_is_low, int cbit, int64_t offset, cudaStream_t s);
 LaunchInfo launch_pair_update(double2 *lo_slab, double2 *hi_slab, int64_t begin, int64_t end,
@@ -288,6 +289,30 @@ int svb_exchange_own_row(void *own, const void *other, int64_t count, const doub
     prof_end((cudaStream_t)stream, li);
     g_launches += li.kernels;
     SVB_CHECK_LAUNCH("svb_exchange_own_row");
+    return SVB_OK;
+}
+
+int svb_permute_qubits(const void *src, void *dst, int64_t n_amps, const int *phys_to_logical, int n,
+                       void *stream) {
+    int r = check_amps(src, n_amps);
+    if (r == SVB_OK) r = check_amps(dst, n_amps);
+    if (r != SVB_OK) return r;
+    if (!phys_to_logical || n != log2_exact(n_amps) || src == dst) {
+        set_error("bad arguments to svb_permute_qubits (needs n = log2(n_amps), out of place)");
+        return SVB_EINVAL;
+    }
+    uint64_t seen = 0;
+    for (int j = 0; j < n; ++j) {
+        int q = phys_to_logical[j];
+        if (q < 0 || q >= n || ((seen >> q) & 1)) {
+            set_error("phys_to_logical is not a permutation of 0..%d", n - 1);
+            return SVB_EINVAL;
+        }
+        seen |= uint64_t(1) << q;
+    }
+    g_launches += launch_permute((const double2 *)src, (double2 *)dst, n_amps, phys_to_logical, n,
+                                 (cudaStream_t)stream);
+    SVB_CHECK_LAUNCH("svb_permute_qubits");
     return SVB_OK;
 }
 

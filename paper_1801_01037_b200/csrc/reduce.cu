@@ -71,6 +71,31 @@ __global__ void __launch_bounds__(kRedThreads) k_probs(const double2 *__restrict
     }
 }
 
+// Qubit relabeling (layout.py:71-83): dst[p] = src[route(p)], route sending
+// bit j of p to bit p2l[j].  Writes are coalesced; reads gather (coalesced
+// whenever the low bits map to themselves).
+struct BitMap {
+    int8_t p2l[64];
+};
+
+__global__ void __launch_bounds__(kRedThreads) k_permute_bits(const double2 *__restrict__ src,
+                                                              double2 *__restrict__ dst, int64_t n,
+                                                              int nbits, BitMap m) {
+    const int64_t p = int64_t(blockIdx.x) * kRedThreads + threadIdx.x;
+    if (p >= n) return;
+    int64_t s = 0;
+    for (int j = 0; j < nbits; ++j) s |= ((p >> j) & 1) << m.p2l[j];
+    dst[p] = src[s];
+}
+
+int launch_permute(const double2 *src, double2 *dst, int64_t n, const int *p2l, int nbits, cudaStream_t s) {
+    BitMap m;
+    for (int j = 0; j < 64; ++j) m.p2l[j] = (int8_t)(j < nbits ? p2l[j] : 0);
+    int64_t blocks = (n + kRedThreads - 1) / kRedThreads;
+    k_permute_bits<<<(unsigned)blocks, kRedThreads, 0, s>>>(src, dst, n, nbits, m);
+    return 1;
+}
+
 // scratch: at least kRedBlocks + 1 doubles of device memory.
 int launch_norm2(const double2 *a, int64_t n, double *scratch, cudaStream_t s) {
     int blocks = (int)((n + kRedThreads - 1) / kRedThreads);
