@@ -50,6 +50,7 @@ typedef struct svb_op {
 /* svb_run_ops flags */
 #define SVB_RUN_FUSE 1u         /* plan multi-gate shared-memory passes        */
 #define SVB_RUN_STRICT_ORDER 2u /* fuse only contiguous runs (bit-exact order) */
+#define SVB_RUN_FMA 4u          /* fused passes may contract a*b+c (not with STRICT) */
 
 int svb_abi_version(void);
 const char *svb_last_error(void);

@@ -27,6 +27,12 @@ LIB_PATH = os.path.join(HERE, "libsvb.so")
 SVB_OK, SVB_EINVAL, SVB_ENOMEM, SVB_ECUDA, SVB_ENCCL, SVB_ESTATE = 0, -1, -2, -3, -4, -5
 RUN_FUSE = 1
 RUN_STRICT_ORDER = 2
+RUN_FMA = 4
+
+
+def run_flags(fuse: bool = True, strict_order: bool = False, fma: bool = False) -> int:
+    return ((RUN_FUSE if fuse else 0) | (RUN_STRICT_ORDER if strict_order else 0)
+            | (RUN_FMA if fma else 0))
 
 _dp = ctypes.POINTER(ctypes.c_double)
 _i64 = ctypes.c_int64

@@ -108,7 +108,7 @@ __device__ __forceinline__ double2 unit_mul(int code, double2 x) {
     return (code & 2) ? make_double2(-r.x, -r.y) : r;
 }
 
-template <int KIND, int S, int CTRL>
+template <int KIND, int S, int CTRL, bool FMA>
 __device__ __forceinline__ void nd_gate(double2 (&v)[FREGS], const FGate &fg) {
     const unsigned cm = fg.cmask;
     double2 q11 = make_double2(0, 0), q12 = q11, q21 = q11, q22 = q11;
@@ -135,18 +135,18 @@ __device__ __forceinline__ void nd_gate(double2 (&v)[FREGS], const FGate &fg) {
             lo = unit_mul(fg.u & 3, hi);
             hi = unit_mul((fg.u >> 2) & 3, t);
         } else if (KIND == FK_REAL) {
-            pair_both_c<K_REAL>(q11, q12, q21, q22, lo, hi);
+            if (FMA) pair_both_fma<K_REAL>(q11, q12, q21, q22, lo, hi); else pair_both_c<K_REAL>(q11, q12, q21, q22, lo, hi);
         } else if (KIND == FK_ANTI) {
-            pair_both_c<K_ANTI>(q11, q12, q21, q22, lo, hi);
+            if (FMA) pair_both_fma<K_ANTI>(q11, q12, q21, q22, lo, hi); else pair_both_c<K_ANTI>(q11, q12, q21, q22, lo, hi);
         } else if (KIND == FK_RX) {
-            pair_both_c<K_RX>(q11, q12, q21, q22, lo, hi);
+            if (FMA) pair_both_fma<K_RX>(q11, q12, q21, q22, lo, hi); else pair_both_c<K_RX>(q11, q12, q21, q22, lo, hi);
         } else {
-            pair_both_c<K_GENERAL>(q11, q12, q21, q22, lo, hi);
+            if (FMA) pair_both_fma<K_GENERAL>(q11, q12, q21, q22, lo, hi); else pair_both_c<K_GENERAL>(q11, q12, q21, q22, lo, hi);
         }
     }
 }
 
-template <int VAR, int TP, int CTRL>
+template <int VAR, int TP, int CTRL, bool FMA>
 __device__ __forceinline__ void diag_gate(double2 (&v)[FREGS], const FGate &fg, int l0) {
     const unsigned cm = fg.cmask;
     const double2 d0 = fg.m[0], d1 = fg.m[3];
@@ -162,8 +162,8 @@ __device__ __forceinline__ void diag_gate(double2 (&v)[FREGS], const FGate &fg, 
         const bool b = TP == FSLOTS ? true : ((i >> TP) & 1);
         if (VAR != FD_GENERAL && !b) continue;
         double2 &x = v[i];
-        if (VAR == FD_GENERAL) x = cmul(TP == FSLOTS ? f : (b ? d1 : d0), x);
-        if (VAR == FD_D1) x = cmul(f, x);
+        if (VAR == FD_GENERAL) x = FMA ? cmul_f(TP == FSLOTS ? f : (b ? d1 : d0), x) : cmul(TP == FSLOTS ? f : (b ? d1 : d0), x);
+        if (VAR == FD_D1) x = FMA ? cmul_f(f, x) : cmul(f, x);
         if (VAR == FD_Z) x = make_double2(-x.x, -x.y);
         if (VAR == FD_S) x = make_double2(-x.y, x.x);
         if (VAR == FD_SDG) x = make_double2(x.y, -x.x);
@@ -171,12 +171,12 @@ __device__ __forceinline__ void diag_gate(double2 (&v)[FREGS], const FGate &fg, 
 }
 
 #define SVB_ND2(K, S) \
-    case ((K)*FSLOTS + (S)) * 2 + 0: nd_gate<K, S, 0>(v, fg); break; \
-    case ((K)*FSLOTS + (S)) * 2 + 1: nd_gate<K, S, 1>(v, fg); break;
+    case ((K)*FSLOTS + (S)) * 2 + 0: nd_gate<K, S, 0, FMA>(v, fg); break; \
+    case ((K)*FSLOTS + (S)) * 2 + 1: nd_gate<K, S, 1, FMA>(v, fg); break;
 #define SVB_ND(K) SVB_ND2(K, 0) SVB_ND2(K, 1) SVB_ND2(K, 2) SVB_ND2(K, 3)
 #define SVB_DG2(V, T) \
-    case FOP_DIAG + ((V) * (FSLOTS + 1) + (T)) * 2 + 0: diag_gate<V, T, 0>(v, fg, l0); break; \
-    case FOP_DIAG + ((V) * (FSLOTS + 1) + (T)) * 2 + 1: diag_gate<V, T, 1>(v, fg, l0); break;
+    case FOP_DIAG + ((V) * (FSLOTS + 1) + (T)) * 2 + 0: diag_gate<V, T, 0, FMA>(v, fg, l0); break; \
+    case FOP_DIAG + ((V) * (FSLOTS + 1) + (T)) * 2 + 1: diag_gate<V, T, 1, FMA>(v, fg, l0); break;
 #define SVB_DG(V) SVB_DG2(V, 0) SVB_DG2(V, 1) SVB_DG2(V, 2) SVB_DG2(V, 3) SVB_DG2(V, 4)
 
 // Register-permuting ops (X, Y, unit phases) as their own cases make every
@@ -189,6 +189,7 @@ __device__ __forceinline__ void diag_gate(double2 (&v)[FREGS], const FGate &fg, 
 #endif
 constexpr bool kPermOps = SVB_FUSED_PERM_OPS != 0;
 
+template <bool FMA>
 __device__ __forceinline__ void run_gate(double2 (&v)[FREGS], const FGate &fg, int l0) {
     switch (fg.op) {
         SVB_ND(FK_GENERAL)
@@ -209,6 +210,7 @@ __device__ __forceinline__ void run_gate(double2 (&v)[FREGS], const FGate &fg, i
     }
 }
 
+template <bool FMA>
 __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__restrict__ a, int64_t ntiles,
                                                                   const __grid_constant__ FPass P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -256,7 +258,7 @@ __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__res
             for (int q = G.first; q < qend; ++q) {
                 const FGate &fg = P.gates[q];
                 if (fg.cl >= 0 && !((l0 >> fg.cl) & 1)) continue;  // thread-bit control clear
-                run_gate(v, fg, l0);
+                run_gate<FMA>(v, fg, l0);
             }
             // Store register l at P(l) = M l ^ mb (identity unless the group
             // ends with X/CNOT gates).  P is linear, so P(l0 | dep(i)) =
@@ -664,10 +666,12 @@ int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsi
     }
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem());
+        cudaFuncSetAttribute(k_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem());
+        cudaFuncSetAttribute(k_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem());
         attr_set = true;
     }
     const bool strict = flags & SVB_RUN_STRICT_ORDER;
+    const bool fma = (flags & SVB_RUN_FMA) && !strict;
     auto passes = plan(n, ops, nops, strict);
     const int64_t ntiles = n_amps >> FM;
     FPass P;  // ~17 KiB, passed by value as a __grid_constant__ kernel parameter
@@ -681,7 +685,10 @@ int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsi
             continue;
         }
         prof_begin(s);
-        k_fused<<<fused_grid(ntiles), FTHREADS, fused_smem(), s>>>(a, ntiles, P);
+        if (fma)
+            k_fused<true><<<fused_grid(ntiles), FTHREADS, fused_smem(), s>>>(a, ntiles, P);
+        else
+            k_fused<false><<<fused_grid(ntiles), FTHREADS, fused_smem(), s>>>(a, ntiles, P);
         prof_end(s, LaunchInfo{1, PROF_FUSED, n_amps * 32});
         *launches += 1;
         cudaError_t e = cudaGetLastError();

@@ -106,6 +106,37 @@ __device__ __forceinline__ void pair_both_c(double2 q11, double2 q12, double2 q2
     }
 }
 
+// FMA-contracted variants (SVB_RUN_FMA): fewer FP64 instructions and one
+// rounding per output component instead of up to three; NOT bit-identical to
+// the reference, agrees to ~1 ulp.
+__device__ __forceinline__ double2 cmul_f(double2 a, double2 b) {
+    return make_double2(__fma_rn(a.x, b.x, -__dmul_rn(a.y, b.y)), __fma_rn(a.x, b.y, __dmul_rn(a.y, b.x)));
+}
+
+template <int KIND>
+__device__ __forceinline__ void pair_both_fma(double2 q11, double2 q12, double2 q21, double2 q22,
+                                              double2 &lo, double2 &hi) {
+    const double2 a = lo, b = hi;
+    if (KIND == K_GENERAL) {
+        lo = make_double2(__fma_rn(q11.x, a.x, __fma_rn(-q11.y, a.y, __fma_rn(q12.x, b.x, -__dmul_rn(q12.y, b.y)))),
+                          __fma_rn(q11.x, a.y, __fma_rn(q11.y, a.x, __fma_rn(q12.x, b.y, __dmul_rn(q12.y, b.x)))));
+        hi = make_double2(__fma_rn(q21.x, a.x, __fma_rn(-q21.y, a.y, __fma_rn(q22.x, b.x, -__dmul_rn(q22.y, b.y)))),
+                          __fma_rn(q21.x, a.y, __fma_rn(q21.y, a.x, __fma_rn(q22.x, b.y, __dmul_rn(q22.y, b.x)))));
+    } else if (KIND == K_REAL) {
+        lo = make_double2(__fma_rn(q11.x, a.x, __dmul_rn(q12.x, b.x)), __fma_rn(q11.x, a.y, __dmul_rn(q12.x, b.y)));
+        hi = make_double2(__fma_rn(q21.x, a.x, __dmul_rn(q22.x, b.x)), __fma_rn(q21.x, a.y, __dmul_rn(q22.x, b.y)));
+    } else if (KIND == K_DIAG) {
+        lo = cmul_f(q11, a);
+        hi = cmul_f(q22, b);
+    } else if (KIND == K_ANTI) {
+        lo = cmul_f(q12, b);
+        hi = cmul_f(q21, a);
+    } else {  // K_RX: q11, q22 real; q12, q21 imaginary
+        lo = make_double2(__fma_rn(q11.x, a.x, -__dmul_rn(q12.y, b.y)), __fma_rn(q11.x, a.y, __dmul_rn(q12.y, b.x)));
+        hi = make_double2(__fma_rn(q22.x, b.x, -__dmul_rn(q21.y, a.y)), __fma_rn(q22.x, b.y, __dmul_rn(q21.y, a.x)));
+    }
+}
+
 template <int KIND>
 __device__ __forceinline__ void pair_both(const Gate &g, double2 &lo, double2 &hi) {
     double2 a = lo, b = hi;
