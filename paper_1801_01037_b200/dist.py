@@ -251,19 +251,28 @@ class DistEngine:
 
         self._flush()
         local = self.compute.norm2(self.slab)
-        dev = self.slab.device if self.slab.is_cuda else torch.device("cpu")
-        t = torch.tensor([local], dtype=torch.float64, device=dev)
+        t = torch.tensor([local], dtype=torch.float64, device=self._coll_device())
         self.dist.all_reduce(t, group=self.group)
         return float(t.item())
 
+    def _coll_device(self):
+        import torch
+
+        nccl = self.dist.get_backend(self.group) == "nccl"
+        return self.slab.device if (nccl and self.slab.is_cuda) else torch.device("cpu")
+
     def gather(self) -> np.ndarray | None:
         """Full state on rank 0 (engine.py:188-192); None elsewhere."""
+        import torch
+
         self._flush()
-        parts = [self.compute.zeros(self.L) for _ in range(self.world)]
-        self.dist.all_gather(parts, self.slab, group=self.group)
+        dev = self._coll_device()
+        mine = self.slab.to(dev)
+        parts = [torch.zeros(self.L, dtype=torch.complex128, device=dev) for _ in range(self.world)]
+        self.dist.all_gather(parts, mine, group=self.group)
         if self.rank != 0:
             return None
-        return np.concatenate([self.compute.to_numpy(p) for p in parts])
+        return np.concatenate([p.cpu().numpy() for p in parts])
 
 
 # ---------------------------------------------------------------------------
