@@ -174,6 +174,37 @@ def main():
     np.savez_compressed(os.path.join(HERE, "layers.npz"), out=out, sha=np.array(canon_sha(out)),
                         ops=op_rows(circ),
                         n=np.array(12), layers=np.array(20), seed=np.array(w.SEED_CFG2))
+    import json
+
+    texts = [
+        "qubits 3\nh 0\ncx 0 1\nz 2  # trailing\n\n# comment\nu 1 0 0 1 0 1 0 0 0\n",
+        "qubits 2\ncu 1 0 1 0 0 0 0 0 0 1\ncy 0 1\n",
+        "qubits 2\nq 0\n",
+        "h 0\n",
+        "qubits 2\nx 2\n",
+        "qubits 2\ncx 1 1\n",
+        "qubits 2\nu 0 1 0 1 0 0 0 1 0\n",
+        "qubits 2\nu 0 1 0 0 0 0 0 1\n",
+        "qubits 0\n",
+        "qubits 2\nx one\n",
+        "",
+    ]
+    cases = []
+    for txt in texts:
+        try:
+            c = svsim.parse_circuit(txt)
+            cases.append({"text": txt, "n": c.n, "ops": op_rows(c).tolist()})
+        except svsim.ParseError as exc:
+            cases.append({"text": txt, "error_line": exc.line})
+    fmt = []
+    rng = np.random.default_rng(11)
+    for circ in (w.qft_circuit(5), conftest.random_circuit(rng, 4, 12)):
+        rc = svsim.Circuit(circ.n, tuple(svsim.GateOp(op.kind, svsim.Gate2x2(op.gate.q11, op.gate.q12,
+                                                                             op.gate.q21, op.gate.q22),
+                                                      op.target, op.control) for op in circ.ops))
+        fmt.append({"ops": op_rows(rc).tolist(), "n": rc.n, "text": svsim.format_circuit(rc)})
+    with open(os.path.join(HERE, "circuit_io.json"), "w") as fh:
+        json.dump({"parse": cases, "format": fmt}, fh, indent=1)
     print("golden fixtures written to", HERE)
 
 
