@@ -79,6 +79,9 @@ struct FGroup {
     int16_t mb;
     int16_t mcol[FM];    // column j of M = P(e_j) ^ mb
     int16_t perm;        // P is not the identity
+    // byte offsets in the swizzled tile (host-precomputed, XOR-combined):
+    uint16_t ld_t[FTBITS], ld_s[FSLOTS];            // load: thread bits, slots
+    uint16_t st_b, st_t[FTBITS], st_s[FSLOTS];      // store through P
 };
 struct FPass {
     int ngates, ngroups, ncomp, flow;
@@ -241,41 +244,44 @@ __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__res
         cp_async_wait_all();
         __syncthreads();
 
+        unsigned char *sbytes = reinterpret_cast<unsigned char *>(buf);
         for (int gi = 0; gi < P.ngroups; ++gi) {
             const FGroup &G = P.groups[gi];
-            int l0 = 0;
+            // Shared-memory byte offset of register i: swizzle and the store map
+            // are XOR-linear, so it is the XOR of host-precomputed per-bit
+            // offsets: thread bits (ld_t) and slot bits (ld_s).
+            unsigned a0 = 0, tg = tid;
+            asm volatile("" : "+r"(tg));  // keep the per-bit masks out of the loop-invariant set
 #pragma unroll
-            for (int j = 0; j < FTBITS; ++j) l0 |= ((tid >> j) & 1) << G.tmap[j];
-            // register i lives at swz(l0 | dep(i)) = swz(l0) ^ XOR of swz(slot bits)
-            const int a0 = swz(l0);
-            const int s0 = swz(1 << G.pos[0]), s1 = swz(1 << G.pos[1]);
-            const int s2 = swz(1 << G.pos[2]), s3 = swz(1 << G.pos[3]);
+            for (int j = 0; j < FTBITS; ++j) a0 ^= (0u - ((tg >> j) & 1u)) & G.ld_t[j];
             double2 v[FREGS];
 #pragma unroll
-            for (int i = 0; i < FREGS; ++i)
-                v[i] = buf[a0 ^ ((i & 1) ? s0 : 0) ^ ((i & 2) ? s1 : 0) ^ ((i & 4) ? s2 : 0) ^ ((i & 8) ? s3 : 0)];
+            for (int i = 0; i < FREGS; ++i) {
+                unsigned off = a0 ^ ((i & 1) ? G.ld_s[0] : 0u) ^ ((i & 2) ? G.ld_s[1] : 0u) ^
+                               ((i & 4) ? G.ld_s[2] : 0u) ^ ((i & 8) ? G.ld_s[3] : 0u);
+                v[i] = *reinterpret_cast<const double2 *>(sbytes + off);
+            }
             const int qend = G.first + G.count;
             for (int q = G.first; q < qend; ++q) {
                 const FGate &fg = P.gates[q];
-                if (fg.cl >= 0 && !((l0 >> fg.cl) & 1)) continue;  // thread-bit control clear
-                run_gate<FMA>(v, fg, l0);
+                if (fg.cl >= 0 && !((tid >> fg.cl) & 1)) continue;  // thread-bit control clear
+                run_gate<FMA>(v, fg, tid);
             }
             // Store register l at P(l) = M l ^ mb (identity unless the group
-            // ends with X/CNOT gates).  P is linear, so P(l0 | dep(i)) =
-            // P(l0) ^ M dep(i); recomputing (not keeping) the addresses saves
-            // 16 live registers.
-            // a permuted store writes slots other threads load: wait for all loads
+            // ends with X/CNOT gates); P is affine, so again an XOR of
+            // per-bit offsets (st_b, st_t, st_s).  A permuted store writes
+            // slots other threads loaded: wait for all loads first.
             if (G.perm) __syncthreads();
-            int ml0 = G.mb;
+            unsigned b0 = G.st_b, ts = tid;
+            asm volatile("" : "+r"(ts));
 #pragma unroll
-            for (int j = 0; j < FTBITS; ++j)
-                if ((tid >> j) & 1) ml0 ^= G.mcol[G.tmap[j]];
-            const int b0 = swz(ml0);
-            const int t0 = swz(G.mcol[G.pos[0]]), t1 = swz(G.mcol[G.pos[1]]);
-            const int t2 = swz(G.mcol[G.pos[2]]), t3 = swz(G.mcol[G.pos[3]]);
+            for (int j = 0; j < FTBITS; ++j) b0 ^= (0u - ((ts >> j) & 1u)) & G.st_t[j];
 #pragma unroll
-            for (int i = 0; i < FREGS; ++i)
-                buf[b0 ^ ((i & 1) ? t0 : 0) ^ ((i & 2) ? t1 : 0) ^ ((i & 4) ? t2 : 0) ^ ((i & 8) ? t3 : 0)] = v[i];
+            for (int i = 0; i < FREGS; ++i) {
+                unsigned off = b0 ^ ((i & 1) ? G.st_s[0] : 0u) ^ ((i & 2) ? G.st_s[1] : 0u) ^
+                               ((i & 4) ? G.st_s[2] : 0u) ^ ((i & 8) ? G.st_s[3] : 0u);
+                *reinterpret_cast<double2 *>(sbytes + off) = v[i];
+            }
             __syncthreads();
         }
 
@@ -560,9 +566,23 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
             G.mcol[j] = (int16_t)gp.mcol[j];
             if (gp.mcol[j] != (1 << j)) G.perm = 1;
         }
+        for (int j = 0; j < FTBITS; ++j) {
+            G.ld_t[j] = (uint16_t)(16 * swz(1 << G.tmap[j]));
+            G.st_t[j] = (uint16_t)(16 * swz(gp.mcol[G.tmap[j]]));
+        }
+        for (int k = 0; k < FSLOTS; ++k) {
+            G.ld_s[k] = (uint16_t)(16 * swz(1 << slots[k]));
+            G.st_s[k] = (uint16_t)(16 * swz(gp.mcol[slots[k]]));
+        }
+        G.st_b = (uint16_t)(16 * swz(gp.mb));
         auto slot_of = [&](int l) {
             for (int i = 0; i < FSLOTS; ++i)
                 if (slots[i] == l) return i;
+            return -1;
+        };
+        auto tbit_of = [&](int l) {  // local bit -> thread-index bit
+            for (int j = 0; j < FTBITS; ++j)
+                if (G.tmap[j] == l) return j;
             return -1;
         };
         for (size_t gk = 0; gk < gp.gates.size(); ++gk) {
@@ -573,12 +593,12 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
             fg.tl = -1;
             fg.pad = 0;
             int cs = m.cl >= 0 ? slot_of(m.cl) : -1;
-            fg.cl = (int8_t)(m.cl >= 0 && cs < 0 ? m.cl : -1);
+            fg.cl = (int8_t)(m.cl >= 0 && cs < 0 ? tbit_of(m.cl) : -1);
             fg.cmask = (uint16_t)(cs >= 0 ? slot_pattern(cs) : 0xffffu);
             if (m.diag) {
                 int ts = slot_of(m.tl);
                 int tpos = ts >= 0 ? ts : FSLOTS;
-                fg.tl = (int8_t)m.tl;
+                fg.tl = (int8_t)(ts >= 0 ? -1 : tbit_of(m.tl));
                 int var = FD_GENERAL;
                 if (m.g.d0_one) {
                     const int uc = unit_code(m.g.m[3]);
