@@ -193,8 +193,8 @@ __device__ __forceinline__ void diag_gate(double2 (&v)[FREGS], const FGate &fg, 
 constexpr bool kPermOps = SVB_FUSED_PERM_OPS != 0;
 
 template <bool FMA>
-__device__ __forceinline__ void run_gate(double2 (&v)[FREGS], const FGate &fg, int l0) {
-    switch (fg.op) {
+__device__ __forceinline__ void run_gate(double2 (&v)[FREGS], const FGate &fg, int l0, unsigned op) {
+    switch (op) {
         SVB_ND(FK_GENERAL)
         SVB_ND(FK_REAL)
         SVB_ND(FK_ANTI)
@@ -261,11 +261,16 @@ __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__res
                                ((i & 4) ? G.ld_s[2] : 0u) ^ ((i & 8) ? G.ld_s[3] : 0u);
                 v[i] = *reinterpret_cast<const double2 *>(sbytes + off);
             }
+            // gate header word (op | tl << 8 | cl << 16 | u << 24) is fetched one
+            // gate ahead so the dispatch branch does not wait on the load
             const int qend = G.first + G.count;
+            unsigned hdr = G.count > 0 ? *reinterpret_cast<const unsigned *>(&P.gates[G.first].op) : 0u;
             for (int q = G.first; q < qend; ++q) {
-                const FGate &fg = P.gates[q];
-                if (fg.cl >= 0 && !((tid >> fg.cl) & 1)) continue;  // thread-bit control clear
-                run_gate<FMA>(v, fg, tid);
+                const unsigned cur = hdr;
+                if (q + 1 < qend) hdr = *reinterpret_cast<const unsigned *>(&P.gates[q + 1].op);
+                const int cl = (int8_t)(cur >> 16);
+                if (cl >= 0 && !((tid >> cl) & 1)) continue;  // thread-bit control clear
+                run_gate<FMA>(v, P.gates[q], tid, cur & 0xffu);
             }
             // Store register l at P(l) = M l ^ mb (identity unless the group
             // ends with X/CNOT gates); P is affine, so again an XOR of
