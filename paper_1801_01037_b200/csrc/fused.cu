@@ -85,6 +85,9 @@ struct FGroup {
 };
 struct FPass {
     int ngates, ngroups, ncomp, flow;
+    int direct_first, direct_last;  // first/last group move registers <-> HBM directly
+    int64_t gl_t[FTBITS], gl_s[FSLOTS];              // first group: amplitude offsets per bit
+    int64_t gs_b, gs_t[FTBITS], gs_s[FSLOTS];        // last group: offsets through its store map
     int8_t comp[64];      // tile-index bit j -> global qubit comp[j]
     int8_t rowbit[FM];    // local bit flow+j -> global qubit rowbit[j]
     FGroup groups[FMAXGRP];
@@ -231,35 +234,54 @@ __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__res
     }
     __syncthreads();
 
+    const int last = P.ngroups - 1;
     for (int64_t tix = blockIdx.x; tix < ntiles; tix += gridDim.x) {
         int64_t base = 0;
         for (int j = 0; j < P.ncomp; ++j)
             if ((tix >> j) & 1) base |= int64_t(1) << P.comp[j];
+        if (!P.direct_first) {
 #pragma unroll
-        for (int k = 0; k < FREGS; ++k) {
-            int e = tid + k * FTHREADS;
-            cp_async16(&buf[swz(e)], &a[base + rowoff[e >> flow] + (e & colmask)]);
+            for (int k = 0; k < FREGS; ++k) {
+                int e = tid + k * FTHREADS;
+                cp_async16(&buf[swz(e)], &a[base + rowoff[e >> flow] + (e & colmask)]);
+            }
+            cp_async_commit();
+            cp_async_wait_all();
+            __syncthreads();
         }
-        cp_async_commit();
-        cp_async_wait_all();
-        __syncthreads();
 
         unsigned char *sbytes = reinterpret_cast<unsigned char *>(buf);
         for (int gi = 0; gi < P.ngroups; ++gi) {
             const FGroup &G = P.groups[gi];
-            // Shared-memory byte offset of register i: swizzle and the store map
-            // are XOR-linear, so it is the XOR of host-precomputed per-bit
-            // offsets: thread bits (ld_t) and slot bits (ld_s).
-            unsigned a0 = 0, tg = tid;
-            asm volatile("" : "+r"(tg));  // keep the per-bit masks out of the loop-invariant set
-#pragma unroll
-            for (int j = 0; j < FTBITS; ++j) a0 ^= (0u - ((tg >> j) & 1u)) & G.ld_t[j];
             double2 v[FREGS];
+            if (gi == 0 && P.direct_first) {
+                // first group straight from HBM: lanes 0-7 hold 8 consecutive
+                // amplitudes (local bits 0-2), so each LDG.128 is 4 full 128 B lines
+                int64_t g0 = 0;
+                unsigned tg = tid;
+                asm volatile("" : "+r"(tg));
 #pragma unroll
-            for (int i = 0; i < FREGS; ++i) {
-                unsigned off = a0 ^ ((i & 1) ? G.ld_s[0] : 0u) ^ ((i & 2) ? G.ld_s[1] : 0u) ^
-                               ((i & 4) ? G.ld_s[2] : 0u) ^ ((i & 8) ? G.ld_s[3] : 0u);
-                v[i] = *reinterpret_cast<const double2 *>(sbytes + off);
+                for (int j = 0; j < FTBITS; ++j)
+                    if ((tg >> j) & 1) g0 ^= P.gl_t[j];
+                const double2 *src = a + (base | g0);
+#pragma unroll
+                for (int i = 0; i < FREGS; ++i)
+                    v[i] = __ldcs(src + (((i & 1) ? P.gl_s[0] : 0) ^ ((i & 2) ? P.gl_s[1] : 0) ^
+                                         ((i & 4) ? P.gl_s[2] : 0) ^ ((i & 8) ? P.gl_s[3] : 0)));
+            } else {
+                // Shared-memory byte offset of register i: swizzle and the store
+                // map are XOR-linear, so it is the XOR of host-precomputed per-bit
+                // offsets: thread bits (ld_t) and slot bits (ld_s).
+                unsigned a0 = 0, tg = tid;
+                asm volatile("" : "+r"(tg));  // keep the per-bit masks out of the loop-invariant set
+#pragma unroll
+                for (int j = 0; j < FTBITS; ++j) a0 ^= (0u - ((tg >> j) & 1u)) & G.ld_t[j];
+#pragma unroll
+                for (int i = 0; i < FREGS; ++i) {
+                    unsigned off = a0 ^ ((i & 1) ? G.ld_s[0] : 0u) ^ ((i & 2) ? G.ld_s[1] : 0u) ^
+                                   ((i & 4) ? G.ld_s[2] : 0u) ^ ((i & 8) ? G.ld_s[3] : 0u);
+                    v[i] = *reinterpret_cast<const double2 *>(sbytes + off);
+                }
             }
             // gate header word (op | tl << 8 | cl << 16 | u << 24) is fetched one
             // gate ahead so the dispatch branch does not wait on the load
@@ -271,6 +293,22 @@ __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__res
                 const int cl = (int8_t)(cur >> 16);
                 if (cl >= 0 && !((tid >> cl) & 1)) continue;  // thread-bit control clear
                 run_gate<FMA>(v, P.gates[q], tid, cur & 0xffu);
+            }
+            if (gi == last && P.direct_last) {
+                // last group straight to HBM through the store map P
+                int64_t g0 = P.gs_b;
+                unsigned tg = tid;
+                asm volatile("" : "+r"(tg));
+#pragma unroll
+                for (int j = 0; j < FTBITS; ++j)
+                    if ((tg >> j) & 1) g0 ^= P.gs_t[j];
+                double2 *dst = a + (base | g0);
+#pragma unroll
+                for (int i = 0; i < FREGS; ++i)
+                    __stcs(dst + (((i & 1) ? P.gs_s[0] : 0) ^ ((i & 2) ? P.gs_s[1] : 0) ^
+                                  ((i & 4) ? P.gs_s[2] : 0) ^ ((i & 8) ? P.gs_s[3] : 0)),
+                           v[i]);
+                continue;
             }
             // Store register l at P(l) = M l ^ mb (identity unless the group
             // ends with X/CNOT gates); P is affine, so again an XOR of
@@ -290,12 +328,14 @@ __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__res
             __syncthreads();
         }
 
-        int64_t base_s = base;  // recompute store addresses rather than keep 16 live
-        asm volatile("" : "+l"(base_s));
+        if (!P.direct_last) {
+            int64_t base_s = base;  // recompute store addresses rather than keep 16 live
+            asm volatile("" : "+l"(base_s));
 #pragma unroll
-        for (int k = 0; k < FREGS; ++k) {
-            int e = tid + k * FTHREADS;
-            a[base_s + rowoff[e >> flow] + (e & colmask)] = buf[swz(e)];
+            for (int k = 0; k < FREGS; ++k) {
+                int e = tid + k * FTHREADS;
+                a[base_s + rowoff[e >> flow] + (e & colmask)] = buf[swz(e)];
+            }
         }
         __syncthreads();  // buffer free for the next tile's loads
     }
@@ -326,6 +366,15 @@ static bool perm_fold() {
     static bool f = [] {
         const char *e = getenv("SVB_FUSE_PERM");
         return !(e && atoi(e) == 0);
+    }();
+    return f;
+}
+
+// SVB_FUSE_DIRECT=0 disables direct HBM first/last groups (for measurement)
+static bool no_direct() {
+    static bool f = [] {
+        const char *e = getenv("SVB_FUSE_DIRECT");
+        return e && atoi(e) == 0;
     }();
     return f;
 }
@@ -490,7 +539,11 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
         return (uint64_t(1) << m.tl) | (m.cl >= 0 ? uint64_t(1) << m.cl : 0);
     };
     auto fits = [&](const GroupPlan &g, const GateMeta &m) {
-        return m.diag || std::find(g.slots.begin(), g.slots.end(), m.tl) != g.slots.end() ||
+        if (m.diag) return true;
+        // the first group keeps local bits 0-2 out of its slots so it can load
+        // straight from HBM with coalesced 128 B lines (direct_first)
+        if (!strict && &g == &gps[0] && m.tl < 3) return false;
+        return std::find(g.slots.begin(), g.slots.end(), m.tl) != g.slots.end() ||
                (int)g.slots.size() < FSLOTS;
     };
     auto take = [&](GroupPlan &g, int q) {
@@ -645,6 +698,38 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
         k0 += (int)gp.gates.size();
     }
     P.ngates = k0;
+
+    // direct HBM access for the first / last group when the coalescing
+    // condition holds: no slot on local bits 0-2, thread bits 0-2 = local bits
+    // 0-2, and (last group) a store map that leaves bits 0-2 alone
+    int glob_of[FM];
+    for (int q = 0, b = 0; q < n; ++q)
+        if ((pp.S >> q) & 1) glob_of[b++] = q;
+    auto gidx = [&](int l) {
+        int64_t g = 0;
+        for (int b = 0; b < FM; ++b)
+            if ((l >> b) & 1) g |= int64_t(1) << glob_of[b];
+        return g;
+    };
+    auto coalesced = [&](const FGroup &G) {
+        for (int k = 0; k < FSLOTS; ++k)
+            if (G.pos[k] < 3) return false;
+        return G.tmap[0] == 0 && G.tmap[1] == 1 && G.tmap[2] == 2;
+    };
+    const FGroup &G0 = P.groups[0];
+    P.direct_first = coalesced(G0) && !no_direct();
+    for (int j = 0; j < FTBITS; ++j) P.gl_t[j] = gidx(1 << G0.tmap[j]);
+    for (int k = 0; k < FSLOTS; ++k) P.gl_s[k] = gidx(1 << G0.pos[k]);
+    const FGroup &GL = P.groups[P.ngroups - 1];
+    bool low_fixed = true;
+    for (int j = 0; j < FM; ++j) {
+        int c = GL.mcol[j];
+        if (j < 3 ? c != (1 << j) : (c & 7) != 0) low_fixed = false;
+    }
+    P.direct_last = coalesced(GL) && low_fixed && !no_direct();
+    P.gs_b = gidx(GL.mb);
+    for (int j = 0; j < FTBITS; ++j) P.gs_t[j] = gidx(GL.mcol[GL.tmap[j]]);
+    for (int k = 0; k < FSLOTS; ++k) P.gs_s[k] = gidx(GL.mcol[GL.pos[k]]);
     return true;
 }
 
