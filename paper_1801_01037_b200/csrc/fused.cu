@@ -302,11 +302,12 @@ __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__res
 #pragma unroll
                 for (int j = 0; j < FTBITS; ++j)
                     if ((tg >> j) & 1) g0 ^= P.gs_t[j];
-                double2 *dst = a + (base | g0);
+                // P mixes bits, so the per-register offset combines by XOR
+                // with g0 (not by addition); tile bits stay disjoint (OR base)
 #pragma unroll
                 for (int i = 0; i < FREGS; ++i)
-                    __stcs(dst + (((i & 1) ? P.gs_s[0] : 0) ^ ((i & 2) ? P.gs_s[1] : 0) ^
-                                  ((i & 4) ? P.gs_s[2] : 0) ^ ((i & 8) ? P.gs_s[3] : 0)),
+                    __stcs(a + (base | (g0 ^ ((i & 1) ? P.gs_s[0] : 0) ^ ((i & 2) ? P.gs_s[1] : 0) ^
+                                        ((i & 4) ? P.gs_s[2] : 0) ^ ((i & 8) ? P.gs_s[3] : 0))),
                            v[i]);
                 continue;
             }
