@@ -295,7 +295,11 @@ __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__res
                 run_gate<FMA>(v, P.gates[q], tid, cur & 0xffu);
             }
             if (gi == last && P.direct_last) {
-                // last group straight to HBM through the store map P
+                // last group straight to HBM through the store map P.  If this
+                // group also loaded from HBM, a permuted store may hit an
+                // address another thread has not read yet: barrier first
+                // (bar.sync orders the block's earlier loads before later stores).
+                if (G.perm && gi == 0 && P.direct_first) __syncthreads();
                 int64_t g0 = P.gs_b;
                 unsigned tg = tid;
                 asm volatile("" : "+r"(tg));
