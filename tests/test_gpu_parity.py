@@ -159,6 +159,29 @@ def test_fused_every_gate_class_strict_bit_exact(cuda_ok, n):
     assert device.plan_passes(n, circ, fuse=True) < len(ops)
 
 
+@pytest.mark.parametrize("n", [14, 15, 19])
+def test_fused_permutation_heavy(cuda_ok, n):
+    # X / CNOT fold into register-group store maps (incl. direct-to-HBM last
+    # groups): mix them densely with arithmetic gates on every qubit
+    rng = np.random.default_rng(500 + n)
+    x = standard_gate("x")
+    pool = [x, x, standard_gate("h"), standard_gate("t"), w.random_unitary2(rng), standard_gate("y")]
+    for trial in range(4):
+        ops = []
+        for _ in range(300):
+            g = pool[int(rng.integers(len(pool)))]
+            if rng.random() < 0.5:
+                c, t = rng.choice(n, size=2, replace=False)
+                ops.append(GateOp("controlled", g, int(t), int(c)))
+            else:
+                ops.append(GateOp("single", g, int(rng.integers(n))))
+        circ = Circuit(n, tuple(ops))
+        a = w.random_state_array(rng, n)
+        want = oracle.run_ops(a.copy(), w.oracle_ops(circ))
+        assert np.array_equal(device.simulate(circ, a.copy(), fuse=True, strict_order=True), want), trial
+        assert np.max(np.abs(device.simulate(circ, a.copy(), fuse=True) - want)) <= TOL, trial
+
+
 def test_random_reference_circuits_vs_oracle(cuda_ok):
     # conftest.random_circuit shape (p_controlled = 0.35, Haar gates), n up to 20
     rng = np.random.default_rng(77)
