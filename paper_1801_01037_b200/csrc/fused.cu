@@ -86,7 +86,6 @@ struct FGroup {
 struct FPass {
     int ngates, ngroups, ncomp, flow;
     int direct_first, direct_last;  // first/last group move registers <-> HBM directly
-    int prefetch;                   // direct_last and the last group reads smem: stream the next tile early
     int64_t gl_t[FTBITS], gl_s[FSLOTS];              // first group: amplitude offsets per bit
     int64_t gs_b, gs_t[FTBITS], gs_s[FSLOTS];        // last group: offsets through its store map
     int8_t comp[64];      // tile-index bit j -> global qubit comp[j]
@@ -236,30 +235,11 @@ __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__res
     __syncthreads();
 
     const int last = P.ngroups - 1;
-    auto tile_base = [&](int64_t t) {
-        int64_t b = 0;
-        for (int j = 0; j < P.ncomp; ++j)
-            if ((t >> j) & 1) b |= int64_t(1) << P.comp[j];
-        return b;
-    };
-    auto fill = [&](int64_t b) {
-#pragma unroll
-        for (int k = 0; k < FREGS; ++k) {
-            int e = tid + k * FTHREADS;
-            cp_async16(&buf[swz(e)], &a[b + rowoff[e >> flow] + (e & colmask)]);
-        }
-        cp_async_commit();
-    };
-    // prefetch mode (last group stores straight to HBM): the buffer is free
-    // once the last group has read it, so the next tile streams in under the
-    // last group's arithmetic and stores
-    if (P.prefetch && blockIdx.x < ntiles) fill(tile_base(blockIdx.x));
     for (int64_t tix = blockIdx.x; tix < ntiles; tix += gridDim.x) {
-        const int64_t base = tile_base(tix);
-        if (P.prefetch) {
-            cp_async_wait_all();
-            __syncthreads();
-        } else if (!P.direct_first) {
+        int64_t base = 0;
+        for (int j = 0; j < P.ncomp; ++j)
+            if ((tix >> j) & 1) base |= int64_t(1) << P.comp[j];
+        if (!P.direct_first) {
 #pragma unroll
             for (int k = 0; k < FREGS; ++k) {
                 int e = tid + k * FTHREADS;
@@ -301,11 +281,6 @@ __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__res
                     unsigned off = a0 ^ ((i & 1) ? G.ld_s[0] : 0u) ^ ((i & 2) ? G.ld_s[1] : 0u) ^
                                    ((i & 4) ? G.ld_s[2] : 0u) ^ ((i & 8) ? G.ld_s[3] : 0u);
                     v[i] = *reinterpret_cast<const double2 *>(sbytes + off);
-                }
-                if (gi == last && P.prefetch) {
-                    __syncthreads();  // every thread holds its registers: buffer free
-                    const int64_t next = tix + gridDim.x;
-                    if (next < ntiles) fill(tile_base(next));
                 }
             }
             // gate header word (op | tl << 8 | cl << 16 | u << 24) is fetched one
@@ -367,9 +342,8 @@ __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__res
                 a[base_s + rowoff[e >> flow] + (e & colmask)] = buf[swz(e)];
             }
         }
-        if (!P.prefetch) __syncthreads();  // buffer free for the next tile's loads
+        __syncthreads();  // buffer free for the next tile's loads
     }
-    cp_async_wait_all();
 }
 
 // ---------------------------------------------------------------------------
@@ -405,15 +379,6 @@ static bool perm_fold() {
 static bool no_direct() {
     static bool f = [] {
         const char *e = getenv("SVB_FUSE_DIRECT");
-        return e && atoi(e) == 0;
-    }();
-    return f;
-}
-
-// SVB_FUSE_PREFETCH=0 disables next-tile prefetch under the last group
-static bool no_prefetch() {
-    static bool f = [] {
-        const char *e = getenv("SVB_FUSE_PREFETCH");
         return e && atoi(e) == 0;
     }();
     return f;
@@ -767,11 +732,6 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
         if (j < 3 ? c != (1 << j) : (c & 7) != 0) low_fixed = false;
     }
     P.direct_last = coalesced(GL) && low_fixed && !no_direct();
-    // with a direct last group, prefer prefetching the next tile into shared
-    // memory under the last group over loading the first group from HBM
-    // (unless the pass is one group that can stream HBM -> registers -> HBM)
-    P.prefetch = P.direct_last && !(P.ngroups == 1 && P.direct_first) && !no_prefetch();
-    if (P.prefetch) P.direct_first = 0;
     P.gs_b = gidx(GL.mb);
     for (int j = 0; j < FTBITS; ++j) P.gs_t[j] = gidx(GL.mcol[GL.tmap[j]]);
     for (int k = 0; k < FSLOTS; ++k) P.gs_s[k] = gidx(GL.mcol[GL.pos[k]]);
