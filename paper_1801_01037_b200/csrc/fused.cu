@@ -20,13 +20,17 @@
 //  * The other 8 local bits index threads through a per-group map chosen so
 //    the 8 lanes of each LDS.128/STS.128 phase hit distinct 16 B bank groups
 //    under the swizzle phys(l) = l ^ fold3(l >> 3).
-//  * X / CNOT are register renames, Y / Z / S / S^dag are exact sign and
-//    re/im swaps; the rest use the exact single-gate arithmetic of
-//    svb_common.cuh.  A strict-order plan is therefore bit-identical to
-//    op-by-op application; the default plan may hoist a gate over earlier
-//    gates on disjoint qubits (they commute) and agrees to a few ulp.
-//  * Two persistent CTAs per SM (64 KiB tile each): one streams its next
-//    tile while the other computes.
+//  * X / CNOT are bit permutations: deferred to the end of their group and
+//    folded into the group's affine store map (exact, no arithmetic).  Z is
+//    an in-place negation; everything else uses the exact single-gate
+//    arithmetic of svb_common.cuh.  A strict-order plan is therefore
+//    bit-identical to op-by-op application; the default plan may hoist a gate
+//    over earlier gates on disjoint qubits (they commute) and agrees to a few
+//    ulp.
+//  * The first / last group of a pass moves its registers straight from / to
+//    HBM when its thread map keeps lanes 0-7 on 128 B lines (direct groups).
+//  * Two persistent CTAs per SM (64 KiB tile each): one streams its tile
+//    while the other computes.
 #include <cuda_runtime.h>
 
 #include <algorithm>
