@@ -22,7 +22,7 @@ from .errors import (
 )
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsvb.so")
+LIB_PATH = os.environ.get("SVB_LIB") or os.path.join(HERE, "libsvb.so")
 
 SVB_OK, SVB_EINVAL, SVB_ENOMEM, SVB_ECUDA, SVB_ENCCL, SVB_ESTATE = 0, -1, -2, -3, -4, -5
 RUN_FUSE = 1

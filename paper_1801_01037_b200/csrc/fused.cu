@@ -34,6 +34,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -47,14 +48,17 @@ LaunchInfo launch_gate(double2 *a, int64_t n_amps, const Gate &g, int t, int c, 
 
 constexpr int FM = 12;                 // qubits per tile
 constexpr int FTILE = 1 << FM;         // 4096 amplitudes = 64 KiB
-constexpr int FSLOTS = 4;              // register bits per thread
+#ifndef SVB_FSLOTS
+#define SVB_FSLOTS 4
+#endif
+constexpr int FSLOTS = SVB_FSLOTS;     // register bits per thread
 constexpr int FREGS = 1 << FSLOTS;     // 16 amplitudes per thread
 constexpr int FTHREADS = FTILE / FREGS;  // 256 threads
 constexpr int FTBITS = FM - FSLOTS;    // 8 thread bits
 constexpr int FMAXG = 192;             // gates per pass
 constexpr int FMAXGRP = 64;            // register groups per pass
 constexpr int FMAXROWS = FTILE / 8;    // rows when flow = 3
-constexpr int FCTAS_PER_SM = 2;
+constexpr int FCTAS_PER_SM = 2;  // 2 x 64 KiB tiles; 2 x 256 x 128 (or 2 x 512 x 64) registers
 
 // Opcodes.  Non-diagonal: op = (kind * FSLOTS + tslot) * 2 + ctrl.
 // Diagonal: FOP_DIAG + (var * (FSLOTS + 1) + tpos) * 2 + ctrl, tpos = FSLOTS
@@ -110,6 +114,16 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// XOR of the per-slot offsets selected by the bits of register index i
+template <class T, class S>
+__device__ __forceinline__ T xcombo(const S *s, int i) {
+    T r = 0;
+#pragma unroll
+    for (int k = 0; k < FSLOTS; ++k)
+        if ((i >> k) & 1) r ^= (T)s[k];
+    return r;
+}
 
 // x * u for u in {1, i, -1, -i} (code 0..3): exact, equal to the reference's
 // (ac - bd, ad + bc) up to the sign of zero
@@ -183,11 +197,19 @@ __device__ __forceinline__ void diag_gate(double2 (&v)[FREGS], const FGate &fg, 
 #define SVB_ND2(K, S) \
     case ((K)*FSLOTS + (S)) * 2 + 0: nd_gate<K, S, 0, FMA>(v, fg); break; \
     case ((K)*FSLOTS + (S)) * 2 + 1: nd_gate<K, S, 1, FMA>(v, fg); break;
+#if SVB_FSLOTS == 4
 #define SVB_ND(K) SVB_ND2(K, 0) SVB_ND2(K, 1) SVB_ND2(K, 2) SVB_ND2(K, 3)
+#else
+#define SVB_ND(K) SVB_ND2(K, 0) SVB_ND2(K, 1) SVB_ND2(K, 2)
+#endif
 #define SVB_DG2(V, T) \
     case FOP_DIAG + ((V) * (FSLOTS + 1) + (T)) * 2 + 0: diag_gate<V, T, 0, FMA>(v, fg, l0); break; \
     case FOP_DIAG + ((V) * (FSLOTS + 1) + (T)) * 2 + 1: diag_gate<V, T, 1, FMA>(v, fg, l0); break;
+#if SVB_FSLOTS == 4
 #define SVB_DG(V) SVB_DG2(V, 0) SVB_DG2(V, 1) SVB_DG2(V, 2) SVB_DG2(V, 3) SVB_DG2(V, 4)
+#else
+#define SVB_DG(V) SVB_DG2(V, 0) SVB_DG2(V, 1) SVB_DG2(V, 2) SVB_DG2(V, 3)
+#endif
 
 // Register-permuting ops (X, Y, unit phases) as their own cases make every
 // switch arm end with v[] in different physical registers, and ptxas then
@@ -270,8 +292,7 @@ __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__res
                 const double2 *src = a + (base | g0);
 #pragma unroll
                 for (int i = 0; i < FREGS; ++i)
-                    v[i] = __ldcs(src + (((i & 1) ? P.gl_s[0] : 0) ^ ((i & 2) ? P.gl_s[1] : 0) ^
-                                         ((i & 4) ? P.gl_s[2] : 0) ^ ((i & 8) ? P.gl_s[3] : 0)));
+                    v[i] = __ldcs(src + xcombo<int64_t>(P.gl_s, i));
             } else {
                 // Shared-memory byte offset of register i: swizzle and the store
                 // map are XOR-linear, so it is the XOR of host-precomputed per-bit
@@ -282,8 +303,7 @@ __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__res
                 for (int j = 0; j < FTBITS; ++j) a0 ^= (0u - ((tg >> j) & 1u)) & G.ld_t[j];
 #pragma unroll
                 for (int i = 0; i < FREGS; ++i) {
-                    unsigned off = a0 ^ ((i & 1) ? G.ld_s[0] : 0u) ^ ((i & 2) ? G.ld_s[1] : 0u) ^
-                                   ((i & 4) ? G.ld_s[2] : 0u) ^ ((i & 8) ? G.ld_s[3] : 0u);
+                    unsigned off = a0 ^ xcombo<unsigned>(G.ld_s, i);
                     v[i] = *reinterpret_cast<const double2 *>(sbytes + off);
                 }
             }
@@ -314,8 +334,7 @@ __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__res
                 // with g0 (not by addition); tile bits stay disjoint (OR base)
 #pragma unroll
                 for (int i = 0; i < FREGS; ++i)
-                    __stcs(a + (base | (g0 ^ ((i & 1) ? P.gs_s[0] : 0) ^ ((i & 2) ? P.gs_s[1] : 0) ^
-                                        ((i & 4) ? P.gs_s[2] : 0) ^ ((i & 8) ? P.gs_s[3] : 0))),
+                    __stcs(a + (base | (g0 ^ xcombo<int64_t>(P.gs_s, i))),
                            v[i]);
                 continue;
             }
@@ -330,8 +349,7 @@ __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__res
             for (int j = 0; j < FTBITS; ++j) b0 ^= (0u - ((ts >> j) & 1u)) & G.st_t[j];
 #pragma unroll
             for (int i = 0; i < FREGS; ++i) {
-                unsigned off = b0 ^ ((i & 1) ? G.st_s[0] : 0u) ^ ((i & 2) ? G.st_s[1] : 0u) ^
-                               ((i & 4) ? G.st_s[2] : 0u) ^ ((i & 8) ? G.st_s[3] : 0u);
+                unsigned off = b0 ^ xcombo<unsigned>(G.st_s, i);
                 *reinterpret_cast<double2 *>(sbytes + off) = v[i];
             }
             __syncthreads();
@@ -763,8 +781,17 @@ int plan_passes(int n, const svb_op *ops, int nops, unsigned flags, int *groups)
     auto passes = plan(n, ops, nops, strict);
     if (groups) {
         FPass P;
+        int df = 0, dl = 0, nf = 0;
         for (const PlanPass &pp : passes)
-            if (pp.ops.size() > 1 && build_pass(n, ops, pp, P, strict)) *groups += P.ngroups;
+            if (pp.ops.size() > 1 && build_pass(n, ops, pp, P, strict)) {
+                *groups += P.ngroups;
+                df += P.direct_first;
+                dl += P.direct_last;
+                ++nf;
+            }
+        if (getenv("SVB_PLAN_DEBUG"))
+            fprintf(stderr, "plan: %zu passes (%d fused), %d groups, direct first %d, direct last %d\n",
+                    passes.size(), nf, *groups, df, dl);
     }
     return (int)passes.size();
 }
