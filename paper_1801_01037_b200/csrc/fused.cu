@@ -58,7 +58,10 @@ constexpr int FTBITS = FM - FSLOTS;    // 8 thread bits
 constexpr int FMAXG = 192;             // gates per pass
 constexpr int FMAXGRP = 64;            // register groups per pass
 constexpr int FMAXROWS = FTILE / 8;    // rows when flow = 3
-constexpr int FCTAS_PER_SM = 2;  // 2 x 64 KiB tiles; 2 x 256 x 128 (or 2 x 512 x 64) registers
+#ifndef SVB_FCTAS
+#define SVB_FCTAS 2
+#endif
+constexpr int FCTAS_PER_SM = SVB_FCTAS;  // 2 x 64 KiB tiles; 2 x 256 x 128 registers
 
 // Opcodes.  Non-diagonal: op = (kind * FSLOTS + tslot) * 2 + ctrl.
 // Diagonal: FOP_DIAG + (var * (FSLOTS + 1) + tpos) * 2 + ctrl, tpos = FSLOTS
@@ -75,8 +78,7 @@ struct FGate {
     int8_t tl;       // diag with a thread-bit target: its local bit
     int8_t cl;       // control on a thread bit: its local bit, else -1
     uint8_t u;       // FK_UANTI unit codes: bits 0-1 q12, bits 2-3 q21
-    uint16_t cmask;  // ctrl = 1: registers (pairs: lo registers) the control allows
-    uint16_t pad;
+    uint32_t cmask;  // ctrl = 1: registers (pairs: lo registers) the control allows
 };
 struct FGroup {
     int8_t pos[FSLOTS];  // slot -> local bit
@@ -197,7 +199,9 @@ __device__ __forceinline__ void diag_gate(double2 (&v)[FREGS], const FGate &fg, 
 #define SVB_ND2(K, S) \
     case ((K)*FSLOTS + (S)) * 2 + 0: nd_gate<K, S, 0, FMA>(v, fg); break; \
     case ((K)*FSLOTS + (S)) * 2 + 1: nd_gate<K, S, 1, FMA>(v, fg); break;
-#if SVB_FSLOTS == 4
+#if SVB_FSLOTS == 5
+#define SVB_ND(K) SVB_ND2(K, 0) SVB_ND2(K, 1) SVB_ND2(K, 2) SVB_ND2(K, 3) SVB_ND2(K, 4)
+#elif SVB_FSLOTS == 4
 #define SVB_ND(K) SVB_ND2(K, 0) SVB_ND2(K, 1) SVB_ND2(K, 2) SVB_ND2(K, 3)
 #else
 #define SVB_ND(K) SVB_ND2(K, 0) SVB_ND2(K, 1) SVB_ND2(K, 2)
@@ -205,7 +209,9 @@ __device__ __forceinline__ void diag_gate(double2 (&v)[FREGS], const FGate &fg, 
 #define SVB_DG2(V, T) \
     case FOP_DIAG + ((V) * (FSLOTS + 1) + (T)) * 2 + 0: diag_gate<V, T, 0, FMA>(v, fg, l0); break; \
     case FOP_DIAG + ((V) * (FSLOTS + 1) + (T)) * 2 + 1: diag_gate<V, T, 1, FMA>(v, fg, l0); break;
-#if SVB_FSLOTS == 4
+#if SVB_FSLOTS == 5
+#define SVB_DG(V) SVB_DG2(V, 0) SVB_DG2(V, 1) SVB_DG2(V, 2) SVB_DG2(V, 3) SVB_DG2(V, 4) SVB_DG2(V, 5)
+#elif SVB_FSLOTS == 4
 #define SVB_DG(V) SVB_DG2(V, 0) SVB_DG2(V, 1) SVB_DG2(V, 2) SVB_DG2(V, 3) SVB_DG2(V, 4)
 #else
 #define SVB_DG(V) SVB_DG2(V, 0) SVB_DG2(V, 1) SVB_DG2(V, 2) SVB_DG2(V, 3)
@@ -676,10 +682,9 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
             for (int i = 0; i < 4; ++i) fg.m[i] = m.g.m[i];
             fg.u = 0;
             fg.tl = -1;
-            fg.pad = 0;
             int cs = m.cl >= 0 ? slot_of(m.cl) : -1;
             fg.cl = (int8_t)(m.cl >= 0 && cs < 0 ? tbit_of(m.cl) : -1);
-            fg.cmask = (uint16_t)(cs >= 0 ? slot_pattern(cs) : 0xffffu);
+            fg.cmask = cs >= 0 ? slot_pattern(cs) : 0xffffffffu;
             if (m.diag) {
                 int ts = slot_of(m.tl);
                 int tpos = ts >= 0 ? ts : FSLOTS;
@@ -718,7 +723,7 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
                     }
                 }
                 // pair loops visit lo registers (slot bit clear) whose control holds
-                fg.cmask = (uint16_t)(fg.cmask & ~slot_pattern(ts));
+                fg.cmask = fg.cmask & ~slot_pattern(ts);
                 fg.op = (uint8_t)((kind * FSLOTS + ts) * 2 + (cs >= 0 ? 1 : 0));
             }
         }
