@@ -46,7 +46,10 @@ namespace svb {
 
 LaunchInfo launch_gate(double2 *a, int64_t n_amps, const Gate &g, int t, int c, cudaStream_t s);
 
-constexpr int FM = 12;                 // qubits per tile
+#ifndef SVB_FM
+#define SVB_FM 12
+#endif
+constexpr int FM = SVB_FM;             // qubits per tile
 constexpr int FTILE = 1 << FM;         // 4096 amplitudes = 64 KiB
 #ifndef SVB_FSLOTS
 #define SVB_FSLOTS 4
