@@ -3,21 +3,21 @@
 // run_circuit applies one gate per sweep over the state (engine.py:483-494,
 // _stride_cy.pyx:24-90): 7,800 full read+write passes for the configs[1]
 // circuit.  Here a host-side planner packs gates whose qubits fit in a set S
-// of FM = 12 qubits into one pass; k_fused streams the state tile by tile --
-// a tile is the 2^12 amplitudes sharing every bit outside S -- through
+// of FM = 11 qubits into one pass; k_fused streams the state tile by tile --
+// a tile is the 2^11 amplitudes sharing every bit outside S -- through
 // shared memory and applies all gates of the pass before writing it back:
 // one HBM read + one HBM write per pass instead of per gate.
 //
 //  * S always holds qubits 0..flow-1 (flow = 4 by default), so a tile is
 //    2^(12-flow) runs of 2^flow contiguous amplitudes and every global access
 //    is a coalesced 16 B-per-lane cp.async (load) / store.
-//  * Gates run in "register groups": each of the 256 threads of a CTA holds
+//  * Gates run in "register groups": each of the 128 threads of a CTA holds
 //    16 amplitudes spanning 4 local bits (the group's slots).  Every
 //    non-diagonal gate of a group targets a slot, so its pair updates are
 //    register-to-register; a control bit needs no slot (it is a register mask
 //    or a per-thread predicate); diagonal gates (Z S T Rz CP) need no pairing
 //    at all.  Shared memory is read and written once per group.
-//  * The other 8 local bits index threads through a per-group map chosen so
+//  * The other 7 local bits index threads through a per-group map chosen so
 //    the 8 lanes of each LDS.128/STS.128 phase hit distinct 16 B bank groups
 //    under the swizzle phys(l) = l ^ fold3(l >> 3).
 //  * X / CNOT are bit permutations: deferred to the end of their group and
@@ -29,8 +29,10 @@
 //    ulp.
 //  * The first / last group of a pass moves its registers straight from / to
 //    HBM when its thread map keeps lanes 0-7 on 128 B lines (direct groups).
-//  * Two persistent CTAs per SM (64 KiB tile each): one streams its tile
-//    while the other computes.
+//  * Four persistent CTAs per SM (32 KiB tile each, 16 warps): while some
+//    stream their tile the others compute (measured best of FM 10-12 x
+//    2-8 CTAs: FM=12 x 2 CTAs 31.2k, FM=11 x 4 CTAs 31.8k, FM=10 x 8 28.7k
+//    gate applications/s on configs[1]).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -47,24 +49,24 @@ namespace svb {
 LaunchInfo launch_gate(double2 *a, int64_t n_amps, const Gate &g, int t, int c, cudaStream_t s);
 
 #ifndef SVB_FM
-#define SVB_FM 12
+#define SVB_FM 11
 #endif
 constexpr int FM = SVB_FM;             // qubits per tile
-constexpr int FTILE = 1 << FM;         // 4096 amplitudes = 64 KiB
+constexpr int FTILE = 1 << FM;         // 2048 amplitudes = 32 KiB
 #ifndef SVB_FSLOTS
 #define SVB_FSLOTS 4
 #endif
 constexpr int FSLOTS = SVB_FSLOTS;     // register bits per thread
 constexpr int FREGS = 1 << FSLOTS;     // 16 amplitudes per thread
-constexpr int FTHREADS = FTILE / FREGS;  // 256 threads
-constexpr int FTBITS = FM - FSLOTS;    // 8 thread bits
+constexpr int FTHREADS = FTILE / FREGS;  // 128 threads
+constexpr int FTBITS = FM - FSLOTS;    // 7 thread bits
 constexpr int FMAXG = 192;             // gates per pass
 constexpr int FMAXGRP = 64;            // register groups per pass
 constexpr int FMAXROWS = FTILE / 8;    // rows when flow = 3
 #ifndef SVB_FCTAS
-#define SVB_FCTAS 2
+#define SVB_FCTAS 4
 #endif
-constexpr int FCTAS_PER_SM = SVB_FCTAS;  // 2 x 64 KiB tiles; 2 x 256 x 128 registers
+constexpr int FCTAS_PER_SM = SVB_FCTAS;  // 4 x 32 KiB tiles; 4 x 128 threads x 128 registers
 
 // Opcodes.  Non-diagonal: op = (kind * FSLOTS + tslot) * 2 + ctrl.
 // Diagonal: FOP_DIAG + (var * (FSLOTS + 1) + tpos) * 2 + ctrl, tpos = FSLOTS
