@@ -231,10 +231,34 @@ __device__ __forceinline__ void diag_gate(double2 (&v)[FREGS], const FGate &fg, 
 #define SVB_FUSED_PERM_OPS 0
 #endif
 constexpr bool kPermOps = SVB_FUSED_PERM_OPS != 0;
+// Fewer switch arms = smaller hot code: ncu showed 23 % of warp stalls as
+// `no_instructions` (instruction fetch) with every (kind, slot, control) arm.
+#ifndef SVB_COMPACT_DISPATCH
+#define SVB_COMPACT_DISPATCH 1
+#endif
+constexpr bool kCompact = SVB_COMPACT_DISPATCH != 0;
 
 template <bool FMA>
 __device__ __forceinline__ void run_gate(double2 (&v)[FREGS], const FGate &fg, int l0, unsigned op) {
     switch (op) {
+#if SVB_COMPACT_DISPATCH
+        // controlled arithmetic gates all take the general arm (exact for every
+        // matrix class); uncontrolled ones get their specialised arm
+#define SVB_NDU(K, S) case ((K)*FSLOTS + (S)) * 2 + 0: nd_gate<K, S, 0, FMA>(v, fg); break;
+#define SVB_NDC(S) case ((FK_GENERAL)*FSLOTS + (S)) * 2 + 1: nd_gate<FK_GENERAL, S, 1, FMA>(v, fg); break;
+        SVB_NDU(FK_GENERAL, 0) SVB_NDU(FK_GENERAL, 1) SVB_NDU(FK_GENERAL, 2) SVB_NDU(FK_GENERAL, 3)
+        SVB_NDU(FK_REAL, 0) SVB_NDU(FK_REAL, 1) SVB_NDU(FK_REAL, 2) SVB_NDU(FK_REAL, 3)
+        SVB_NDU(FK_ANTI, 0) SVB_NDU(FK_ANTI, 1) SVB_NDU(FK_ANTI, 2) SVB_NDU(FK_ANTI, 3)
+        SVB_NDU(FK_RX, 0) SVB_NDU(FK_RX, 1) SVB_NDU(FK_RX, 2) SVB_NDU(FK_RX, 3)
+        SVB_NDC(0) SVB_NDC(1) SVB_NDC(2) SVB_NDC(3)
+#define SVB_DGU(V, T) case FOP_DIAG + ((V) * (FSLOTS + 1) + (T)) * 2 + 0: diag_gate<V, T, 0, FMA>(v, fg, l0); break;
+        SVB_DGU(FD_Z, 0) SVB_DGU(FD_Z, 1) SVB_DGU(FD_Z, 2) SVB_DGU(FD_Z, 3) SVB_DGU(FD_Z, 4)
+        SVB_DG(FD_GENERAL)
+        SVB_DG(FD_D1)
+        default: break;
+    }
+}
+#else
         SVB_ND(FK_GENERAL)
         SVB_ND(FK_REAL)
         SVB_ND(FK_ANTI)
@@ -252,6 +276,7 @@ __device__ __forceinline__ void run_gate(double2 (&v)[FREGS], const FGate &fg, i
         default: break;
     }
 }
+#endif
 
 template <bool FMA>
 __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__restrict__ a, int64_t ntiles,
@@ -706,6 +731,7 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
                     else
                         var = FD_D1;
                 }
+                if (kCompact && cs >= 0 && var == FD_Z) var = FD_D1;  // exact: cmul by (-1, 0)
                 fg.op = (uint8_t)(FOP_DIAG + (var * (FSLOTS + 1) + tpos) * 2 + (cs >= 0 ? 1 : 0));
             } else {
                 int ts = slot_of(m.tl);
@@ -729,6 +755,7 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
                 }
                 // pair loops visit lo registers (slot bit clear) whose control holds
                 fg.cmask = fg.cmask & ~slot_pattern(ts);
+                if (kCompact && cs >= 0) kind = FK_GENERAL;  // general formula = reference's, exact
                 fg.op = (uint8_t)((kind * FSLOTS + ts) * 2 + (cs >= 0 ? 1 : 0));
             }
         }
