@@ -8,8 +8,8 @@
 // shared memory and applies all gates of the pass before writing it back:
 // one HBM read + one HBM write per pass instead of per gate.
 //
-//  * S always holds qubits 0..flow-1 (flow = 4 by default), so a tile is
-//    2^(12-flow) runs of 2^flow contiguous amplitudes and every global access
+//  * S always holds qubits 0..flow-1 (flow = 3 by default), so a tile is
+//    2^(FM-flow) runs of 2^flow contiguous amplitudes and every global access
 //    is a coalesced 16 B-per-lane cp.async (load) / store.
 //  * Gates run in "register groups": each of the 128 threads of a CTA holds
 //    16 amplitudes spanning 4 local bits (the group's slots).  Every
@@ -417,7 +417,7 @@ static int popc(uint64_t x) { return __builtin_popcountll(x); }
 static int flow_bits() {
     static int f = [] {
         const char *e = getenv("SVB_FUSE_FLOW");
-        int v = e ? atoi(e) : 4;
+        int v = e ? atoi(e) : 3;  // 128 B runs; frees one more tile qubit than 4 (+1 %)
         return v < 3 ? 3 : (v > 5 ? 5 : v);
     }();
     return f;
