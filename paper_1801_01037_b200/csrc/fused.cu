@@ -95,13 +95,14 @@ struct FGroup {
     int16_t mcol[FM];    // column j of M = P(e_j) ^ mb
     int16_t perm;        // P is not the identity
     // byte offsets in the swizzled tile (host-precomputed, XOR-combined):
-    uint16_t ld_t[FTBITS], ld_s[FSLOTS];            // load: thread bits, slots
+    int16_t qb, qcol[FM];                           // load map Q (leading X / CNOT)
+    uint16_t ld_b, ld_t[FTBITS], ld_s[FSLOTS];      // load through Q: offset, thread bits, slots
     uint16_t st_b, st_t[FTBITS], st_s[FSLOTS];      // store through P
 };
 struct FPass {
     int ngates, ngroups, ncomp, flow;
     int direct_first, direct_last;  // first/last group move registers <-> HBM directly
-    int64_t gl_t[FTBITS], gl_s[FSLOTS];              // first group: amplitude offsets per bit
+    int64_t gl_b, gl_t[FTBITS], gl_s[FSLOTS];        // first group: offsets through its load map
     int64_t gs_b, gs_t[FTBITS], gs_s[FSLOTS];        // last group: offsets through its store map
     int8_t comp[64];      // tile-index bit j -> global qubit comp[j]
     int8_t rowbit[FM];    // local bit flow+j -> global qubit rowbit[j]
@@ -319,21 +320,21 @@ __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__res
             if (gi == 0 && P.direct_first) {
                 // first group straight from HBM: lanes 0-7 hold 8 consecutive
                 // amplitudes (local bits 0-2), so each LDG.128 is 4 full 128 B lines
-                int64_t g0 = 0;
+                // through the group's load map Q: offsets combine by XOR
+                int64_t g0 = P.gl_b;
                 unsigned tg = tid;
                 asm volatile("" : "+r"(tg));
 #pragma unroll
                 for (int j = 0; j < FTBITS; ++j)
                     if ((tg >> j) & 1) g0 ^= P.gl_t[j];
-                const double2 *src = a + (base | g0);
 #pragma unroll
                 for (int i = 0; i < FREGS; ++i)
-                    v[i] = __ldcs(src + xcombo<int64_t>(P.gl_s, i));
+                    v[i] = __ldcs(a + (base | (g0 ^ xcombo<int64_t>(P.gl_s, i))));
             } else {
                 // Shared-memory byte offset of register i: swizzle and the store
                 // map are XOR-linear, so it is the XOR of host-precomputed per-bit
                 // offsets: thread bits (ld_t) and slot bits (ld_s).
-                unsigned a0 = 0, tg = tid;
+                unsigned a0 = G.ld_b, tg = tid;
                 asm volatile("" : "+r"(tg));  // keep the per-bit masks out of the loop-invariant set
 #pragma unroll
                 for (int j = 0; j < FTBITS; ++j) a0 ^= (0u - ((tg >> j) & 1u)) & G.ld_t[j];
@@ -579,16 +580,25 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
     struct GroupPlan {
         std::vector<int> gates;  // indices into meta, execution order (no perms)
         std::vector<int> slots;
-        int mcol[FM];
+        int mcol[FM];            // post map P (store)
         int mb = 0;
         uint64_t permq = 0;
+        int qcol[FM];            // pre map Q (load): register l reads position Q(l)
+        int qb = 0;
     };
     std::vector<GroupPlan> gps;
     auto new_group = [&]() {
         GroupPlan g;
-        for (int j = 0; j < FM; ++j) g.mcol[j] = 1 << j;
+        for (int j = 0; j < FM; ++j) g.mcol[j] = g.qcol[j] = 1 << j;
         gps.push_back(g);
         return &gps.back();
+    };
+    // A permutation C met before any arithmetic gate of the group is folded
+    // into the load map instead: the state after C holds at l what was at
+    // C(l) (C is an involution), so Q <- Q o C; no qubit gets blocked.
+    auto pre_perm = [&](GroupPlan &g, const GateMeta &m) {
+        if (m.cl >= 0) g.qcol[m.cl] ^= g.qcol[m.tl];  // CNOT: column c of (M_Q L_C)
+        else g.qb ^= g.qcol[m.tl];                   // X: offset M_Q e_t
     };
     auto defer_perm = [&](GroupPlan &g, const GateMeta &m) {
         // compose C(x) = x ^ (x_c << t) (X: c = -1, always) after the current map
@@ -612,7 +622,10 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
     auto take = [&](GroupPlan &g, int q) {
         const GateMeta &m = meta[q];
         if (m.perm) {
-            defer_perm(g, m);
+            if (g.gates.empty() && g.permq == 0)
+                pre_perm(g, m);
+            else
+                defer_perm(g, m);
             return;
         }
         if (!m.diag && std::find(g.slots.begin(), g.slots.end(), m.tl) == g.slots.end()) g.slots.push_back(m.tl);
@@ -635,7 +648,9 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
             // permutation blocks its qubits like any unplaced gate); only when
             // that stalls, admit permutations -- each one closes its qubits
             // for the rest of the group, so they go last.
-            auto scan = [&](bool allow_perm) {
+            // mode 0: arithmetic only; 1: permutations too (post map);
+            // 2: permutations only -- run first, they fold into the load map
+            auto scan = [&](int mode) {
                 bool progress = false;
                 uint64_t blocked = 0;  // local bits touched by an unplaced earlier gate
                 for (int q = 0; q < ng; ++q) {
@@ -643,7 +658,8 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
                     const GateMeta &m = meta[q];
                     const uint64_t bits = gbits(m);
                     bool ok = (bits & blocked) == 0 &&
-                              (m.perm ? allow_perm : ((bits & g->permq) == 0 && fits(*g, m)));
+                              (m.perm ? mode != 0
+                                      : (mode != 2 && (bits & g->permq) == 0 && fits(*g, m)));
                     if (ok) {
                         take(*g, q);
                         placed[q] = 1;
@@ -655,14 +671,27 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
                 }
                 return progress;
             };
+            while (scan(2)) {
+            }
             for (;;) {
-                while (scan(false)) {
+                while (scan(0)) {
                 }
-                if (!scan(true)) break;
+                if (!scan(1)) break;
             }
         }
     }
     if ((int)gps.size() > FMAXGRP) return false;
+    if (getenv("SVB_PLAN_DEBUG") && atoi(getenv("SVB_PLAN_DEBUG")) >= 2) {
+        int nperm = 0;
+        for (const GateMeta &m : meta) nperm += m.perm;
+        fprintf(stderr, "pass: %d gates (%d X/CNOT), %zu groups:", ng, nperm, gps.size());
+        for (const GroupPlan &g : gps) {
+            fprintf(stderr, " [%zu gates, slots", g.gates.size());
+            for (int s : g.slots) fprintf(stderr, " %d", s);
+            fprintf(stderr, "%s]", g.permq ? ", perm" : "");
+        }
+        fprintf(stderr, "\n");
+    }
     P.ngroups = (int)gps.size();
     int k0 = 0;
     for (int gi = 0; gi < P.ngroups; ++gi) {
@@ -682,19 +711,22 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
         G.first = (int16_t)k0;
         G.count = (int16_t)gp.gates.size();
         G.mb = (int16_t)gp.mb;
-        G.perm = (int16_t)(gp.mb != 0);
+        G.perm = (int16_t)(gp.mb != 0 || gp.qb != 0);
         for (int j = 0; j < FM; ++j) {
             G.mcol[j] = (int16_t)gp.mcol[j];
-            if (gp.mcol[j] != (1 << j)) G.perm = 1;
+            G.qcol[j] = (int16_t)gp.qcol[j];
+            if (gp.mcol[j] != (1 << j) || gp.qcol[j] != (1 << j)) G.perm = 1;
         }
+        G.qb = (int16_t)gp.qb;
         for (int j = 0; j < FTBITS; ++j) {
-            G.ld_t[j] = (uint16_t)(16 * swz(1 << G.tmap[j]));
+            G.ld_t[j] = (uint16_t)(16 * swz(gp.qcol[G.tmap[j]]));
             G.st_t[j] = (uint16_t)(16 * swz(gp.mcol[G.tmap[j]]));
         }
         for (int k = 0; k < FSLOTS; ++k) {
-            G.ld_s[k] = (uint16_t)(16 * swz(1 << slots[k]));
+            G.ld_s[k] = (uint16_t)(16 * swz(gp.qcol[slots[k]]));
             G.st_s[k] = (uint16_t)(16 * swz(gp.mcol[slots[k]]));
         }
+        G.ld_b = (uint16_t)(16 * swz(gp.qb));
         G.st_b = (uint16_t)(16 * swz(gp.mb));
         auto slot_of = [&](int l) {
             for (int i = 0; i < FSLOTS; ++i)
@@ -780,17 +812,21 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
             if (G.pos[k] < 3) return false;
         return G.tmap[0] == 0 && G.tmap[1] == 1 && G.tmap[2] == 2;
     };
+    // the 8 lanes of a phase vary local bits 0-2; through an (invertible)
+    // affine map they still cover one 128 B line iff columns 0-2 stay inside
+    // bits 0-2 (other columns may add a per-line constant in bits 0-2)
+    auto low_fixed = [&](const int16_t *col) {
+        for (int j = 0; j < 3; ++j)
+            if (col[j] >> 3) return false;
+        return true;
+    };
     const FGroup &G0 = P.groups[0];
-    P.direct_first = coalesced(G0) && !no_direct();
-    for (int j = 0; j < FTBITS; ++j) P.gl_t[j] = gidx(1 << G0.tmap[j]);
-    for (int k = 0; k < FSLOTS; ++k) P.gl_s[k] = gidx(1 << G0.pos[k]);
+    P.direct_first = coalesced(G0) && low_fixed(G0.qcol) && !no_direct();
+    P.gl_b = gidx(G0.qb);
+    for (int j = 0; j < FTBITS; ++j) P.gl_t[j] = gidx(G0.qcol[G0.tmap[j]]);
+    for (int k = 0; k < FSLOTS; ++k) P.gl_s[k] = gidx(G0.qcol[G0.pos[k]]);
     const FGroup &GL = P.groups[P.ngroups - 1];
-    bool low_fixed = true;
-    for (int j = 0; j < FM; ++j) {
-        int c = GL.mcol[j];
-        if (j < 3 ? c != (1 << j) : (c & 7) != 0) low_fixed = false;
-    }
-    P.direct_last = coalesced(GL) && low_fixed && !no_direct();
+    P.direct_last = coalesced(GL) && low_fixed(GL.mcol) && !no_direct();
     P.gs_b = gidx(GL.mb);
     for (int j = 0; j < FTBITS; ++j) P.gs_t[j] = gidx(GL.mcol[GL.tmap[j]]);
     for (int k = 0; k < FSLOTS; ++k) P.gs_s[k] = gidx(GL.mcol[GL.pos[k]]);
