@@ -39,6 +39,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
+#include <mutex>
 #include <vector>
 
 #include "../../include/svb.h"
@@ -66,7 +68,13 @@ constexpr int FMAXROWS = FTILE / 8;    // rows when flow = 3
 #ifndef SVB_FCTAS
 #define SVB_FCTAS 4
 #endif
-constexpr int FCTAS_PER_SM = SVB_FCTAS;  // 4 x 32 KiB tiles; 4 x 128 threads x 128 registers
+constexpr int FCTAS_PER_SM = SVB_FCTAS;
+#ifndef SVB_FUSE_DB
+#define SVB_FUSE_DB 0
+#endif
+constexpr bool kDB = SVB_FUSE_DB != 0;  // double-buffered tiles (next tile prefetched)
+constexpr int kNBuf = kDB ? 2 : 1;
+// default: 4 CTAs x (32 KiB tile + 2 KiB row table), 4 x 128 threads x 128 registers
 
 // Opcodes.  Non-diagonal: op = (kind * FSLOTS + tslot) * 2 + ctrl.
 // Diagonal: FOP_DIAG + (var * (FSLOTS + 1) + tpos) * 2 + ctrl, tpos = FSLOTS
@@ -283,8 +291,8 @@ template <bool FMA>
 __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__restrict__ a, int64_t ntiles,
                                                                   const __grid_constant__ FPass P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double2 *buf = reinterpret_cast<double2 *>(smem_raw);
-    int64_t *rowoff = reinterpret_cast<int64_t *>(smem_raw + FTILE * sizeof(double2));
+    double2 *bufs = reinterpret_cast<double2 *>(smem_raw);
+    int64_t *rowoff = reinterpret_cast<int64_t *>(smem_raw + kNBuf * FTILE * sizeof(double2));
     const int tid = threadIdx.x;
     const int flow = P.flow;
     const int nrows = FTILE >> flow;
@@ -298,17 +306,35 @@ __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__res
     __syncthreads();
 
     const int last = P.ngroups - 1;
-    for (int64_t tix = blockIdx.x; tix < ntiles; tix += gridDim.x) {
-        int64_t base = 0;
+    auto tile_base = [&](int64_t t) {
+        int64_t b = 0;
         for (int j = 0; j < P.ncomp; ++j)
-            if ((tix >> j) & 1) base |= int64_t(1) << P.comp[j];
-        if (!P.direct_first) {
+            if ((t >> j) & 1) b |= int64_t(1) << P.comp[j];
+        return b;
+    };
+    auto fill = [&](double2 *dst, int64_t b) {
 #pragma unroll
-            for (int k = 0; k < FREGS; ++k) {
-                int e = tid + k * FTHREADS;
-                cp_async16(&buf[swz(e)], &a[base + rowoff[e >> flow] + (e & colmask)]);
-            }
-            cp_async_commit();
+        for (int k = 0; k < FREGS; ++k) {
+            int e = tid + k * FTHREADS;
+            cp_async16(&dst[swz(e)], &a[b + rowoff[e >> flow] + (e & colmask)]);
+        }
+        cp_async_commit();
+    };
+    // double-buffered mode: tile i+1 streams into the other buffer while the
+    // groups of tile i run (the first group then reads shared memory)
+    const bool direct_first = P.direct_first && !kDB;
+    if (kDB && blockIdx.x < ntiles) fill(bufs, tile_base(blockIdx.x));
+    int it = 0;
+    for (int64_t tix = blockIdx.x; tix < ntiles; tix += gridDim.x, ++it) {
+        double2 *buf = bufs + (kDB ? (it & 1) * FTILE : 0);
+        const int64_t base = tile_base(tix);
+        if (kDB) {
+            cp_async_wait_all();
+            __syncthreads();
+            const int64_t next = tix + gridDim.x;
+            if (next < ntiles) fill(bufs + ((it + 1) & 1) * FTILE, tile_base(next));
+        } else if (!direct_first) {
+            fill(buf, base);
             cp_async_wait_all();
             __syncthreads();
         }
@@ -317,7 +343,7 @@ __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__res
         for (int gi = 0; gi < P.ngroups; ++gi) {
             const FGroup &G = P.groups[gi];
             double2 v[FREGS];
-            if (gi == 0 && P.direct_first) {
+            if (gi == 0 && direct_first) {
                 // first group straight from HBM: lanes 0-7 hold 8 consecutive
                 // amplitudes (local bits 0-2), so each LDG.128 is 4 full 128 B lines
                 // through the group's load map Q: offsets combine by XOR
@@ -360,7 +386,7 @@ __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__res
                 // group also loaded from HBM, a permuted store may hit an
                 // address another thread has not read yet: barrier first
                 // (bar.sync orders the block's earlier loads before later stores).
-                if (G.perm && gi == 0 && P.direct_first) __syncthreads();
+                if (G.perm && gi == 0 && direct_first) __syncthreads();
                 int64_t g0 = P.gs_b;
                 unsigned tg = tid;
                 asm volatile("" : "+r"(tg));
@@ -401,8 +427,9 @@ __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__res
                 a[base_s + rowoff[e >> flow] + (e & colmask)] = buf[swz(e)];
             }
         }
-        __syncthreads();  // buffer free for the next tile's loads
+        if (!kDB) __syncthreads();  // buffer free for the next tile's loads
     }
+    if (kDB) cp_async_wait_all();
 }
 
 // ---------------------------------------------------------------------------
@@ -833,7 +860,7 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
     return true;
 }
 
-static size_t fused_smem() { return FTILE * sizeof(double2) + FMAXROWS * sizeof(int64_t); }
+static size_t fused_smem() { return kNBuf * FTILE * sizeof(double2) + FMAXROWS * sizeof(int64_t); }
 
 static int fused_grid(int64_t ntiles) {
     static int sms = [] {
@@ -869,6 +896,65 @@ int plan_passes(int n, const svb_op *ops, int nops, unsigned flags, int *groups)
     return (int)passes.size();
 }
 
+// ---------------------------------------------------------------------------
+// compiled plans, cached: a circuit run repeatedly (bench steps, parameter
+// sweeps) is planned and lowered to kernel descriptors once.
+
+struct PlanStep {
+    int op;  // >= 0: run ops[op] with the single-gate kernels; -1: next fused pass
+};
+struct CompiledPlan {
+    int n;
+    bool strict;
+    std::vector<svb_op> ops;  // exact key
+    std::vector<PlanStep> steps;
+    std::vector<FPass> passes;
+};
+
+static uint64_t fnv1a(const void *p, size_t len, uint64_t h) {
+    const unsigned char *b = static_cast<const unsigned char *>(p);
+    for (size_t i = 0; i < len; ++i) h = (h ^ b[i]) * 1099511628211ull;
+    return h;
+}
+
+static std::shared_ptr<const CompiledPlan> compiled_plan(int n, const svb_op *ops, int nops, bool strict) {
+    static std::mutex mu;
+    static std::vector<std::pair<uint64_t, std::shared_ptr<const CompiledPlan>>> cache;  // MRU first
+    uint64_t key = fnv1a(ops, sizeof(svb_op) * size_t(nops), 1469598103934665603ull);
+    key = fnv1a(&n, sizeof n, key);
+    key = fnv1a(&strict, sizeof strict, key);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (size_t i = 0; i < cache.size(); ++i) {
+            const auto &c = cache[i].second;
+            if (cache[i].first == key && c->n == n && c->strict == strict && (int)c->ops.size() == nops &&
+                std::memcmp(c->ops.data(), ops, sizeof(svb_op) * size_t(nops)) == 0) {
+                auto hit = cache[i];
+                cache.erase(cache.begin() + i);
+                cache.insert(cache.begin(), hit);
+                return hit.second;
+            }
+        }
+    }
+    auto cp = std::make_shared<CompiledPlan>();
+    cp->n = n;
+    cp->strict = strict;
+    cp->ops.assign(ops, ops + nops);
+    FPass P;
+    for (const PlanPass &pp : plan(n, ops, nops, strict)) {
+        if (pp.ops.size() > 1 && build_pass(n, ops, pp, P, strict)) {
+            cp->steps.push_back(PlanStep{-1});
+            cp->passes.push_back(P);
+        } else {
+            for (int oi : pp.ops) cp->steps.push_back(PlanStep{oi});
+        }
+    }
+    std::lock_guard<std::mutex> lk(mu);
+    cache.insert(cache.begin(), {key, cp});
+    if (cache.size() > 4) cache.pop_back();
+    return cp;
+}
+
 int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsigned flags,
                    cudaStream_t s, int64_t *launches) {
     int n = 0;
@@ -891,18 +977,15 @@ int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsi
     }
     const bool strict = flags & SVB_RUN_STRICT_ORDER;
     const bool fma = (flags & SVB_RUN_FMA) && !strict;
-    auto passes = plan(n, ops, nops, strict);
+    std::shared_ptr<const CompiledPlan> cp = compiled_plan(n, ops, nops, strict);
     const int64_t ntiles = n_amps >> FM;
-    FPass P;  // ~17 KiB, passed by value as a __grid_constant__ kernel parameter
-    for (const PlanPass &pp : passes) {
-        if (pp.ops.size() == 1) {
-            single(ops[pp.ops[0]]);
+    size_t next_pass = 0;
+    for (const PlanStep &st : cp->steps) {
+        if (st.op >= 0) {
+            single(ops[st.op]);
             continue;
         }
-        if (!build_pass(n, ops, pp, P, strict)) {
-            for (int oi : pp.ops) single(ops[oi]);
-            continue;
-        }
+        const FPass &P = cp->passes[next_pass++];  // ~17 KiB, a __grid_constant__ kernel parameter
         prof_begin(s);
         if (fma)
             k_fused<true><<<fused_grid(ntiles), FTHREADS, fused_smem(), s>>>(a, ntiles, P);
