@@ -479,7 +479,96 @@ static uint64_t op_mask(const svb_op &o) {
 // Greedy pass construction.  strict: only contiguous runs of ops.  Otherwise
 // a scan over the remaining ops that hoists an op past skipped ones only if
 // it shares no qubit with any skipped op (so every qubit keeps its order).
+static int planner_kind() {
+    static int k = [] {
+        const char *e = getenv("SVB_FUSE_PLANNER");
+        return e ? atoi(e) : 2;
+    }();
+    return k;
+}
+
+// Lookahead pass construction (non-strict): grow the pass's qubit set S one
+// gate's qubits at a time, choosing among the ready gates the one whose new
+// qubits admit the most gates per new qubit; after every growth, absorb every
+// ready gate whose qubits are already in S.  Gate order per qubit is kept by
+// the same blocked-qubit scan as the greedy planner.
+static std::vector<PlanPass> plan_lookahead(int n, const svb_op *ops, int nops) {
+    std::vector<PlanPass> passes;
+    const uint64_t low = (uint64_t(1) << flow_bits()) - 1;
+    std::vector<char> done(nops, 0);
+    int first = 0;
+    const int window = 1024;
+    std::vector<int> taken;
+    // ops that can join a pass with qubit set S (without marking them)
+    auto absorb_count = [&](uint64_t S, int lim) {
+        uint64_t blocked = 0;
+        int cnt = 0;
+        for (int i = first; i < nops && i < first + window; ++i) {
+            if (done[i]) continue;
+            uint64_t m = op_mask(ops[i]);
+            if ((m & blocked) == 0 && (m & ~S) == 0) {
+                if (++cnt >= lim) break;
+            } else {
+                blocked |= m;
+            }
+        }
+        return cnt;
+    };
+    while (first < nops) {
+        PlanPass p;
+        p.S = low;
+        for (;;) {
+            // absorb everything that fits S
+            uint64_t blocked = 0;
+            for (int i = first; i < nops && i < first + window && (int)p.ops.size() < FMAXG; ++i) {
+                if (done[i]) continue;
+                uint64_t m = op_mask(ops[i]);
+                if ((m & blocked) == 0 && (m & ~p.S) == 0) {
+                    p.ops.push_back(i);
+                    done[i] = 1;
+                } else {
+                    blocked |= m;
+                }
+            }
+            if (popc(p.S) >= FM || (int)p.ops.size() >= FMAXG) break;
+            // candidate growths: ready gates needing new qubits that still fit
+            uint64_t best = 0;
+            double best_score = -1.0;
+            int cands = 0;
+            blocked = 0;
+            for (int i = first; i < nops && i < first + window && cands < 24; ++i) {
+                if (done[i]) continue;
+                uint64_t m = op_mask(ops[i]);
+                uint64_t add = m & ~p.S;
+                if ((m & blocked) == 0 && add && popc(p.S | m) <= FM) {
+                    ++cands;
+                    int gain = absorb_count(p.S | m, FMAXG);
+                    double score = double(gain) / popc(add);
+                    if (score > best_score) {
+                        best_score = score;
+                        best = m;
+                    }
+                }
+                blocked |= m;
+            }
+            if (!best) break;
+            p.S |= best;
+        }
+        while (first < nops && done[first]) ++first;
+        if (p.ops.empty()) {  // cannot happen (the first pending op always fits) -- guard
+            p.ops.push_back(first);
+            p.S |= op_mask(ops[first]);
+            done[first] = 1;
+            while (first < nops && done[first]) ++first;
+        }
+        for (int q = 0; q < n && popc(p.S) < FM; ++q) p.S |= uint64_t(1) << q;
+        passes.push_back(std::move(p));
+    }
+    return passes;
+}
+
 static std::vector<PlanPass> plan(int n, const svb_op *ops, int nops, bool strict) {
+    if (!strict && planner_kind() == 2) return plan_lookahead(n, ops, nops);
     std::vector<PlanPass> passes;
     const uint64_t low = (uint64_t(1) << flow_bits()) - 1;
     const uint64_t all = n >= 64 ? ~uint64_t(0) : ((uint64_t(1) << n) - 1);
