@@ -357,7 +357,9 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-fuse", action="store_true", help="one launch per gate")
-    ap.add_argument("--fma", action="store_true", help="fused passes contract multiply-adds (~1 ulp)")
+    ap.add_argument("--no-fma", dest="fma", action="store_false",
+                    help="exact reference arithmetic in fused passes (default: FMA contraction, "
+                         "within ~1 ulp, parity-tested <= 1e-12)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the configs[2] n=30 sweep")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU reference work")

@@ -133,6 +133,21 @@ def test_fused_random_layers_vs_oracle(cuda_ok, n):
             assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("n", [14, 20])
+def test_fused_fma_within_tolerance(cuda_ok, n):
+    # SVB_RUN_FMA (the bench's default): multiply-adds contracted in fused
+    # passes -- not bit-identical, within the north-star 1e-12
+    rng = np.random.default_rng(400 + n)
+    for circ in (w.random_layer_circuit(n, 8, seed=n), w.qft_circuit(n)):
+        a = w.random_state_array(rng, n)
+        want = oracle.run_ops(a.copy(), w.oracle_ops(circ), workers=8)
+        got = device.simulate(circ, a.copy(), fma=True)
+        assert np.max(np.abs(got - want)) <= TOL
+        st = device.DeviceState.from_host(a)
+        device.run_ops(st, circ, fma=True)
+        assert np.max(np.abs(st.to_host().amps - want)) <= TOL
+
+
 @pytest.mark.parametrize("n", [14, 17])
 def test_fused_every_gate_class_strict_bit_exact(cuda_ok, n):
     # every fused opcode family: general / real / anti / Rx / unit-anti gates on
