@@ -256,7 +256,7 @@ def run_gpu_arm(args) -> None:
     circuit = workloads.random_layer_circuit(n, LAYERS)
     nops = len(circuit.ops)
     ops_arr, _ = _lib.ops_array(circuit.ops)
-    flags = _lib.run_flags(fuse=not args.no_fuse, fma=args.fma)
+    flags = _lib.run_flags(fuse=not args.no_fuse, fma=args.fma, jit=args.jit)
     passes = device.plan_passes(n, circuit, fuse=not args.no_fuse)
     st = device.DeviceState.zeros(n)
     stream = torch.cuda.current_stream()
@@ -311,10 +311,10 @@ def run_gpu_arm(args) -> None:
     pin_out = torch.empty(1 << n, dtype=torch.complex128).pin_memory()
     a_in, a_out = pin_in.numpy(), pin_out.numpy()
     e2e_steps = max(1, min(args.steps, 3))
-    device.simulate(circuit, a_in, fuse=not args.no_fuse, out=a_out, fma=args.fma)
+    device.simulate(circuit, a_in, fuse=not args.no_fuse, out=a_out, fma=args.fma, jit=args.jit)
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        device.simulate(circuit, a_in, fuse=not args.no_fuse, out=a_out, fma=args.fma)
+        device.simulate(circuit, a_in, fuse=not args.no_fuse, out=a_out, fma=args.fma, jit=args.jit)
     e2e_dt = time.perf_counter() - t0
     e2e_norm = float(np.vdot(a_out, a_out).real)
 
@@ -332,7 +332,7 @@ def run_gpu_arm(args) -> None:
         "data": "synthetic (seeded numpy PCG64 circuit, |0...0> start)",
         "config": {"workload": f"random layer circuit n={n}, {LAYERS} layers x ({n} 1q + {n // 2} CNOT) "
                                f"= {nops} ops (BASELINE configs[1])",
-                   "n_qubits": n, "layers": LAYERS, "ops_per_step": nops, "fused": not args.no_fuse, "fma": args.fma,
+                   "n_qubits": n, "layers": LAYERS, "ops_per_step": nops, "fused": not args.no_fuse, "fma": args.fma, "jit": args.jit,
                    "hbm_passes_per_step": passes, "state_bytes": 16 << n,
                    "l2": "state 1 GiB > 126 MB L2; no flush needed", "parallelism": "single GPU"},
         "roofline": roofline,
@@ -360,6 +360,7 @@ def main(argv=None):
     ap.add_argument("--no-fma", dest="fma", action="store_false",
                     help="exact reference arithmetic in fused passes (default: FMA contraction, "
                          "within ~1 ulp, parity-tested <= 1e-12)")
+    ap.add_argument("--jit", action="store_true", help="fused passes compiled to straight-line kernels (NVRTC)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the configs[2] n=30 sweep")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU reference work")

@@ -51,6 +51,8 @@ typedef struct svb_op {
 #define SVB_RUN_FUSE 1u         /* plan multi-gate shared-memory passes        */
 #define SVB_RUN_STRICT_ORDER 2u /* fuse only contiguous runs (bit-exact order) */
 #define SVB_RUN_FMA 4u          /* fused passes may contract a*b+c (not with STRICT) */
+#define SVB_RUN_JIT 8u          /* compile each fused pass to straight-line code (NVRTC,
+                                   cached per op list; falls back to the interpreter) */
 
 int svb_abi_version(void);
 const char *svb_last_error(void);
@@ -89,6 +91,12 @@ int svb_run_ops(void *amps, int64_t n_amps, const svb_op *ops, int nops, unsigne
  * Planner only, no device work. */
 int svb_plan_passes(int n_qubits, const svb_op *ops, int nops, unsigned flags, int *passes,
                     int *groups);
+
+/* Host-only: plan the op list, generate the SVB_RUN_JIT source of every fused
+ * pass and compile it with NVRTC (no device work).  *compiled = passes
+ * compiled; SVB_ESTATE (message in svb_last_error) when NVRTC is missing or a
+ * pass fails to compile. */
+int svb_jit_check(int n_qubits, const svb_op *ops, int nops, unsigned flags, int *compiled);
 
 /* sum |a_j|^2 -> *out (host).  Synchronises `stream`.  Replaces norm2
  * (core.py:171-174) / _dist_norm2 for one slab (engine.py:453-454). */

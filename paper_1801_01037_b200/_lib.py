@@ -28,11 +28,12 @@ SVB_OK, SVB_EINVAL, SVB_ENOMEM, SVB_ECUDA, SVB_ENCCL, SVB_ESTATE = 0, -1, -2, -3
 RUN_FUSE = 1
 RUN_STRICT_ORDER = 2
 RUN_FMA = 4
+RUN_JIT = 8
 
 
-def run_flags(fuse: bool = True, strict_order: bool = False, fma: bool = False) -> int:
+def run_flags(fuse: bool = True, strict_order: bool = False, fma: bool = False, jit: bool = False) -> int:
     return ((RUN_FUSE if fuse else 0) | (RUN_STRICT_ORDER if strict_order else 0)
-            | (RUN_FMA if fma else 0))
+            | (RUN_FMA if fma else 0) | (RUN_JIT if jit else 0))
 
 _dp = ctypes.POINTER(ctypes.c_double)
 _i64 = ctypes.c_int64
@@ -57,6 +58,7 @@ _SIGS = {
     "svb_run_ops": ([_vp, _i64, ctypes.POINTER(SvbOp), _int, ctypes.c_uint, _vp], _int),
     "svb_plan_passes": ([_int, ctypes.POINTER(SvbOp), _int, ctypes.c_uint, ctypes.POINTER(_int),
                          ctypes.POINTER(_int)], _int),
+    "svb_jit_check": ([_int, ctypes.POINTER(SvbOp), _int, ctypes.c_uint, ctypes.POINTER(_int)], _int),
     "svb_norm2": ([_vp, _i64, _dp, _vp], _int),
     "svb_probs": ([_vp, _i64, _vp, _vp], _int),
     "svb_exchange_own_row": ([_vp, _vp, _i64, _dp, _int, _int, _i64, _vp], _int),

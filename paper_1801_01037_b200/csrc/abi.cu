@@ -34,6 +34,7 @@ LaunchInfo launch_exchange_packed(double2 *own, const double2 *other, int64_t co
 int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsigned flags,
                    cudaStream_t s, int64_t *launches);
 int plan_passes(int n, const svb_op *ops, int nops, unsigned flags, int *groups);
+int jit_check(int n, const svb_op *ops, int nops, unsigned flags);
 
 static thread_local char g_err[512];
 std::atomic<int64_t> g_launches{0};
@@ -229,6 +230,19 @@ int svb_run_ops(void *amps, int64_t n_amps, const svb_op *ops, int nops, unsigne
     g_launches += launches;
     if (r != SVB_OK) return r;
     SVB_CHECK_LAUNCH("svb_run_ops");
+    return SVB_OK;
+}
+
+int svb_jit_check(int n_qubits, const svb_op *ops, int nops, unsigned flags, int *compiled) {
+    if (n_qubits < 1 || n_qubits > 62 || !compiled) {
+        set_error("bad arguments to svb_jit_check");
+        return SVB_EINVAL;
+    }
+    int r = check_ops(n_qubits, ops, nops);
+    if (r != SVB_OK) return r;
+    int c = jit_check(n_qubits, ops, nops, flags);
+    if (c < 0) return SVB_ESTATE;
+    *compiled = c;
     return SVB_OK;
 }
 

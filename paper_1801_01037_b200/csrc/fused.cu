@@ -41,6 +41,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "../../include/svb.h"
@@ -50,73 +51,9 @@ namespace svb {
 
 LaunchInfo launch_gate(double2 *a, int64_t n_amps, const Gate &g, int t, int c, cudaStream_t s);
 
-#ifndef SVB_FM
-#define SVB_FM 11
-#endif
-constexpr int FM = SVB_FM;             // qubits per tile
-constexpr int FTILE = 1 << FM;         // 2048 amplitudes = 32 KiB
-#ifndef SVB_FSLOTS
-#define SVB_FSLOTS 4
-#endif
-constexpr int FSLOTS = SVB_FSLOTS;     // register bits per thread
-constexpr int FREGS = 1 << FSLOTS;     // 16 amplitudes per thread
-constexpr int FTHREADS = FTILE / FREGS;  // 128 threads
-constexpr int FTBITS = FM - FSLOTS;    // 7 thread bits
-constexpr int FMAXG = 192;             // gates per pass
-constexpr int FMAXGRP = 64;            // register groups per pass
-constexpr int FMAXROWS = FTILE / 8;    // rows when flow = 3
-#ifndef SVB_FCTAS
-#define SVB_FCTAS 4
-#endif
-constexpr int FCTAS_PER_SM = SVB_FCTAS;
-#ifndef SVB_FUSE_DB
-#define SVB_FUSE_DB 0
-#endif
-constexpr bool kDB = SVB_FUSE_DB != 0;  // double-buffered tiles (next tile prefetched)
-constexpr int kNBuf = kDB ? 2 : 1;
-// default: 4 CTAs x (32 KiB tile + 2 KiB row table), 4 x 128 threads x 128 registers
-
-// Opcodes.  Non-diagonal: op = (kind * FSLOTS + tslot) * 2 + ctrl.
-// Diagonal: FOP_DIAG + (var * (FSLOTS + 1) + tpos) * 2 + ctrl, tpos = FSLOTS
-// meaning the target is a thread bit (one factor for all 16 registers).
-// ctrl = 1: a control on a slot, applied through the register mask cmask; a
-// control on a thread bit is the per-thread predicate `cl`.
-enum FKind { FK_GENERAL = 0, FK_REAL, FK_ANTI, FK_RX, FK_UANTI, FK_X, FK_Y, FK_NKIND };
-enum FDiag { FD_GENERAL = 0, FD_D1, FD_Z, FD_S, FD_SDG, FD_NVAR };
-constexpr int FOP_DIAG = FK_NKIND * FSLOTS * 2;
-
-struct FGate {
-    double2 m[4];
-    uint8_t op;
-    int8_t tl;       // diag with a thread-bit target: its local bit
-    int8_t cl;       // control on a thread bit: its local bit, else -1
-    uint8_t u;       // FK_UANTI unit codes: bits 0-1 q12, bits 2-3 q21
-    uint32_t cmask;  // ctrl = 1: registers (pairs: lo registers) the control allows
-};
-struct FGroup {
-    int8_t pos[FSLOTS];  // slot -> local bit
-    int8_t tmap[FTBITS]; // thread bit -> local bit
-    int16_t first, count;
-    // X / CNOT gates of the group, as the affine bit map P(l) = M l ^ mb they
-    // induce on local indices: applied for free by storing register l at P(l)
-    int16_t mb;
-    int16_t mcol[FM];    // column j of M = P(e_j) ^ mb
-    int16_t perm;        // P is not the identity
-    // byte offsets in the swizzled tile (host-precomputed, XOR-combined):
-    int16_t qb, qcol[FM];                           // load map Q (leading X / CNOT)
-    uint16_t ld_b, ld_t[FTBITS], ld_s[FSLOTS];      // load through Q: offset, thread bits, slots
-    uint16_t st_b, st_t[FTBITS], st_s[FSLOTS];      // store through P
-};
-struct FPass {
-    int ngates, ngroups, ncomp, flow;
-    int direct_first, direct_last;  // first/last group move registers <-> HBM directly
-    int64_t gl_b, gl_t[FTBITS], gl_s[FSLOTS];        // first group: offsets through its load map
-    int64_t gs_b, gs_t[FTBITS], gs_s[FSLOTS];        // last group: offsets through its store map
-    int8_t comp[64];      // tile-index bit j -> global qubit comp[j]
-    int8_t rowbit[FM];    // local bit flow+j -> global qubit rowbit[j]
-    FGroup groups[FMAXGRP];
-    FGate gates[FMAXG];
-};
+}  // namespace svb
+#include "fused_desc.h"
+namespace svb {
 
 // 16 B-granular XOR swizzle: bits 3-5, 6-8, 9-11 fold into bits 0-2, so local
 // bit j moves the 16 B chunk inside a 128 B line along axis (j mod 3).  It is
@@ -963,6 +900,21 @@ static int fused_grid(int64_t ntiles) {
 
 static bool fuse_enabled(int n, unsigned flags) { return (flags & SVB_RUN_FUSE) && n >= FM + 2; }
 
+int jit_compile_only(const std::vector<FPass> &passes, bool fma, std::string &err);
+
+// host-only: plan, lower and NVRTC-compile every fused pass (no device work)
+int jit_check(int n, const svb_op *ops, int nops, unsigned flags) {
+    const bool strict = flags & SVB_RUN_STRICT_ORDER;
+    std::vector<FPass> passes;
+    FPass P;
+    for (const PlanPass &pp : plan(n, ops, nops, strict))
+        if (pp.ops.size() > 1 && build_pass(n, ops, pp, P, strict)) passes.push_back(P);
+    std::string err;
+    int r = jit_compile_only(passes, (flags & SVB_RUN_FMA) && !strict, err);
+    if (r < 0) set_error("jit compile failed: %.400s", err.c_str());
+    return r;
+}
+
 int plan_passes(int n, const svb_op *ops, int nops, unsigned flags, int *groups) {
     if (groups) *groups = 0;
     if (!fuse_enabled(n, flags)) return nops;
@@ -998,7 +950,14 @@ struct CompiledPlan {
     std::vector<svb_op> ops;  // exact key
     std::vector<PlanStep> steps;
     std::vector<FPass> passes;
+    // runtime-specialised kernels per pass (jit.cu), built on first JIT use
+    mutable std::mutex jit_mu;
+    mutable int jit_state[2] = {0, 0};  // per FMA mode: 0 untried, 1 built, -1 failed
+    mutable std::vector<void *> jit_fns[2];
 };
+
+bool jit_build(const std::vector<FPass> &passes, bool fma, std::vector<void *> &fns);
+bool jit_launch(void *fn, double2 *a, int64_t ntiles, int grid, cudaStream_t s);
 
 static uint64_t fnv1a(const void *p, size_t len, uint64_t h) {
     const unsigned char *b = static_cast<const unsigned char *>(p);
@@ -1069,17 +1028,32 @@ int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsi
     std::shared_ptr<const CompiledPlan> cp = compiled_plan(n, ops, nops, strict);
     const int64_t ntiles = n_amps >> FM;
     size_t next_pass = 0;
+    const bool jit = (flags & SVB_RUN_JIT) && !cp->passes.empty();
+    const std::vector<void *> *jit_fns = nullptr;
+    if (jit) {
+        std::lock_guard<std::mutex> lk(cp->jit_mu);
+        int &state = cp->jit_state[fma];
+        if (state == 0) state = jit_build(cp->passes, fma, cp->jit_fns[fma]) ? 1 : -1;
+        if (state == 1) jit_fns = &cp->jit_fns[fma];
+    }
     for (const PlanStep &st : cp->steps) {
         if (st.op >= 0) {
             single(ops[st.op]);
             continue;
         }
-        const FPass &P = cp->passes[next_pass++];  // ~17 KiB, a __grid_constant__ kernel parameter
+        const size_t pi = next_pass++;
+        const FPass &P = cp->passes[pi];  // ~17 KiB, a __grid_constant__ kernel parameter
         prof_begin(s);
-        if (fma)
+        if (jit && jit_fns) {
+            if (!jit_launch((*jit_fns)[pi], a, ntiles, fused_grid(ntiles), s)) {
+                set_error("svb jit: cuLaunchKernel failed");
+                return SVB_ECUDA;
+            }
+        } else if (fma) {
             k_fused<true><<<fused_grid(ntiles), FTHREADS, fused_smem(), s>>>(a, ntiles, P);
-        else
+        } else {
             k_fused<false><<<fused_grid(ntiles), FTHREADS, fused_smem(), s>>>(a, ntiles, P);
+        }
         prof_end(s, LaunchInfo{1, PROF_FUSED, n_amps * 32});
         *launches += 1;
         cudaError_t e = cudaGetLastError();

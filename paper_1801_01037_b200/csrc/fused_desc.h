@@ -1,0 +1,78 @@
+// fused_desc.h -- fused-pass descriptor layout shared by the interpreter
+// kernel (fused.cu) and the runtime-specialised kernels (jit.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace svb {
+
+#ifndef SVB_FM
+#define SVB_FM 11
+#endif
+constexpr int FM = SVB_FM;             // qubits per tile
+constexpr int FTILE = 1 << FM;         // 2048 amplitudes = 32 KiB
+#ifndef SVB_FSLOTS
+#define SVB_FSLOTS 4
+#endif
+constexpr int FSLOTS = SVB_FSLOTS;     // register bits per thread
+constexpr int FREGS = 1 << FSLOTS;     // 16 amplitudes per thread
+constexpr int FTHREADS = FTILE / FREGS;  // 128 threads
+constexpr int FTBITS = FM - FSLOTS;    // 7 thread bits
+constexpr int FMAXG = 192;             // gates per pass
+constexpr int FMAXGRP = 64;            // register groups per pass
+constexpr int FMAXROWS = FTILE / 8;    // rows when flow = 3
+#ifndef SVB_FCTAS
+#define SVB_FCTAS 4
+#endif
+constexpr int FCTAS_PER_SM = SVB_FCTAS;
+#ifndef SVB_FUSE_DB
+#define SVB_FUSE_DB 0
+#endif
+constexpr bool kDB = SVB_FUSE_DB != 0;  // double-buffered tiles (next tile prefetched)
+constexpr int kNBuf = kDB ? 2 : 1;
+// default: 4 CTAs x (32 KiB tile + 2 KiB row table), 4 x 128 threads x 128 registers
+
+// Opcodes.  Non-diagonal: op = (kind * FSLOTS + tslot) * 2 + ctrl.
+// Diagonal: FOP_DIAG + (var * (FSLOTS + 1) + tpos) * 2 + ctrl, tpos = FSLOTS
+// meaning the target is a thread bit (one factor for all 16 registers).
+// ctrl = 1: a control on a slot, applied through the register mask cmask; a
+// control on a thread bit is the per-thread predicate `cl`.
+enum FKind { FK_GENERAL = 0, FK_REAL, FK_ANTI, FK_RX, FK_UANTI, FK_X, FK_Y, FK_NKIND };
+enum FDiag { FD_GENERAL = 0, FD_D1, FD_Z, FD_S, FD_SDG, FD_NVAR };
+constexpr int FOP_DIAG = FK_NKIND * FSLOTS * 2;
+
+struct FGate {
+    double2 m[4];
+    uint8_t op;
+    int8_t tl;       // diag with a thread-bit target: its local bit
+    int8_t cl;       // control on a thread bit: its local bit, else -1
+    uint8_t u;       // FK_UANTI unit codes: bits 0-1 q12, bits 2-3 q21
+    uint32_t cmask;  // ctrl = 1: registers (pairs: lo registers) the control allows
+};
+struct FGroup {
+    int8_t pos[FSLOTS];  // slot -> local bit
+    int8_t tmap[FTBITS]; // thread bit -> local bit
+    int16_t first, count;
+    // X / CNOT gates of the group, as the affine bit map P(l) = M l ^ mb they
+    // induce on local indices: applied for free by storing register l at P(l)
+    int16_t mb;
+    int16_t mcol[FM];    // column j of M = P(e_j) ^ mb
+    int16_t perm;        // P is not the identity
+    // byte offsets in the swizzled tile (host-precomputed, XOR-combined):
+    int16_t qb, qcol[FM];                           // load map Q (leading X / CNOT)
+    uint16_t ld_b, ld_t[FTBITS], ld_s[FSLOTS];      // load through Q: offset, thread bits, slots
+    uint16_t st_b, st_t[FTBITS], st_s[FSLOTS];      // store through P
+};
+struct FPass {
+    int ngates, ngroups, ncomp, flow;
+    int direct_first, direct_last;  // first/last group move registers <-> HBM directly
+    int64_t gl_b, gl_t[FTBITS], gl_s[FSLOTS];        // first group: offsets through its load map
+    int64_t gs_b, gs_t[FTBITS], gs_s[FSLOTS];        // last group: offsets through its store map
+    int8_t comp[64];      // tile-index bit j -> global qubit comp[j]
+    int8_t rowbit[FM];    // local bit flow+j -> global qubit rowbit[j]
+    FGroup groups[FMAXGRP];
+    FGate gates[FMAXG];
+};
+
+
+}  // namespace svb

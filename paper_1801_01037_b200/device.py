@@ -121,17 +121,18 @@ def apply_controlled(s, g: Gate2x2, c: int, t: int):
     return s
 
 
-def run_ops(s, ops, fuse: bool = True, strict_order: bool = False, fma: bool = False):
+def run_ops(s, ops, fuse: bool = True, strict_order: bool = False, fma: bool = False, jit: bool = False):
     """Apply ops in circuit order on the device (one rank of run_circuit,
     engine.py:483-494), optionally fused into shared-memory passes
     (strict_order: bit-identical to op-by-op; fma: fused passes contract
-    multiply-adds, ~1 ulp from the reference)."""
+    multiply-adds, ~1 ulp from the reference; jit: fused passes compiled to
+    straight-line kernels once per op list, same bits as the interpreter)."""
     lib = _lib.load()
     ptr, n_amps = _as_device(s)
     if isinstance(ops, Circuit):
         ops = ops.ops
     arr, nops = _lib.ops_array(ops)
-    flags = _lib.run_flags(fuse, strict_order, fma)
+    flags = _lib.run_flags(fuse, strict_order, fma, jit)
     _lib.check(lib.svb_run_ops(ptr, n_amps, arr, nops, flags, _stream_ptr()), "run_ops")
     return s
 
@@ -182,7 +183,7 @@ def _host_c128(a, writable: bool = False) -> np.ndarray:
 
 
 def simulate(circuit: Circuit, initial=None, fuse: bool = True, strict_order: bool = False,
-             out: np.ndarray | None = None, fma: bool = False) -> np.ndarray:
+             out: np.ndarray | None = None, fma: bool = False, jit: bool = False) -> np.ndarray:
     """End-to-end public call on HOST memory: copy the initial state (default
     |0...0>) to the device, run the whole circuit, copy the result back into
     `out` (default: `initial` itself when it is a writable complex128 array,
@@ -201,7 +202,7 @@ def simulate(circuit: Circuit, initial=None, fuse: bool = True, strict_order: bo
             and dst.flags.writeable and dst.shape == src.shape):
         raise ValidationError("out must be a writable contiguous complex128 array of the state's size")
     arr, nops = _lib.ops_array(circuit.ops)
-    flags = _lib.run_flags(fuse, strict_order, fma)
+    flags = _lib.run_flags(fuse, strict_order, fma, jit)
     _lib.check(lib.svb_host_run_ops(ctypes.c_void_p(src.ctypes.data), ctypes.c_void_p(dst.ctypes.data),
                                     src.shape[0], arr, nops, flags), "simulate")
     return dst

@@ -148,6 +148,32 @@ def test_fused_fma_within_tolerance(cuda_ok, n):
         assert np.max(np.abs(st.to_host().amps - want)) <= TOL
 
 
+@pytest.mark.parametrize("n", [14, 19])
+def test_jit_passes_bit_identical_to_interpreter(cuda_ok, n):
+    # SVB_RUN_JIT compiles each fused pass to straight-line code; it must give
+    # exactly the interpreter's bits (exact and FMA arithmetic, perms, controls)
+    rng = np.random.default_rng(600 + n)
+    x = standard_gate("x")
+    pool = all_gates(rng) + [x, x, Gate2x2(1, 0, 0, -1j)]
+    ops = []
+    for _ in range(250):
+        g = pool[int(rng.integers(len(pool)))]
+        if rng.random() < 0.4:
+            c, t = rng.choice(n, size=2, replace=False)
+            ops.append(GateOp("controlled", g, int(t), int(c)))
+        else:
+            ops.append(GateOp("single", g, int(rng.integers(n))))
+    circs = [Circuit(n, tuple(ops)), w.random_layer_circuit(n, 6, seed=n), w.qft_circuit(n)]
+    for circ in circs:
+        a = w.random_state_array(rng, n)
+        for fma in (False, True):
+            ref = device.simulate(circ, a.copy(), fma=fma)
+            got = device.simulate(circ, a.copy(), fma=fma, jit=True)
+            assert np.array_equal(got, ref), (fma, np.max(np.abs(got - ref)))
+        want = oracle.run_ops(a.copy(), w.oracle_ops(circ))
+        assert np.max(np.abs(got - want)) <= TOL
+
+
 @pytest.mark.parametrize("n", [14, 17])
 def test_fused_every_gate_class_strict_bit_exact(cuda_ok, n):
     # every fused opcode family: general / real / anti / Rx / unit-anti gates on

@@ -72,6 +72,20 @@ def test_plan_passes_host_only():
     assert 1 <= fused <= len(circ.ops)
 
 
+def test_jit_sources_compile_with_nvrtc():
+    # host-only: every fused pass of a circuit lowers to CUDA C that NVRTC
+    # compiles for sm_100a (no device needed)
+    lib = _lib.load(require_cuda=False)
+    circ = workloads.random_layer_circuit(15, 2, seed=4)
+    arr, nops = _lib.ops_array(circ.ops)
+    out = ctypes.c_int()
+    rc = lib.svb_jit_check(15, arr, nops, _lib.run_flags(fma=True), ctypes.byref(out))
+    if rc == _lib.SVB_ESTATE and b"NVRTC not available" in lib.svb_last_error():
+        pytest.skip("NVRTC not available")
+    assert rc == 0, lib.svb_last_error()
+    assert out.value >= 1
+
+
 def test_kernel_wrapper_validates_like_reference():
     # kernel/__init__.py:83-97, 124-128 -- raised before any device work
     with pytest.raises(ValidationError):
