@@ -267,7 +267,12 @@ def run_gpu_arm(args) -> None:
         st.amps[0] = 1.0
         _lib.check(lib.svb_run_ops(st.ptr, 1 << n, ops_arr, nops, flags, sp), "run_ops")
 
-    for _ in range(max(args.warmup, 0)):
+    # first warm-up step plans the circuit and (with JIT) compiles its passes
+    t_first = time.perf_counter()
+    step()
+    torch.cuda.synchronize()
+    first_step_s = time.perf_counter() - t_first
+    for _ in range(max(args.warmup - 1, 0)):
         step()
     torch.cuda.synchronize()
     _lib.profile_enable(True)
@@ -346,6 +351,8 @@ def run_gpu_arm(args) -> None:
         "local_gate_sweep": sweep,
         "clocks": clk.summary(),
         "check": {"norm_after_step": norm_after, "e2e_norm": e2e_norm},
+        "first_step_s": round(first_step_s, 3),
+        "jit_compile_s": round(max(0.0, first_step_s - ms / 1e3 / args.steps), 3) if args.jit else 0.0,
     }
     print(json.dumps(line), flush=True)
 
@@ -360,7 +367,9 @@ def main(argv=None):
     ap.add_argument("--no-fma", dest="fma", action="store_false",
                     help="exact reference arithmetic in fused passes (default: FMA contraction, "
                          "within ~1 ulp, parity-tested <= 1e-12)")
-    ap.add_argument("--jit", action="store_true", help="fused passes compiled to straight-line kernels (NVRTC)")
+    ap.add_argument("--no-jit", dest="jit", action="store_false",
+                    help="interpret fused passes (default: compile each pass once to a straight-line "
+                         "kernel with NVRTC; bit-identical results, compile time reported as jit_compile_s)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the configs[2] n=30 sweep")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU reference work")
