@@ -151,7 +151,8 @@ def ops_array(ops) -> tuple[ctypes.Array, int]:
     return arr, len(ops)
 
 
-PROFILE_CLASSES = ("k_pair_high", "k_pair_low", "k_diag", "k_tiny", "k_fused", "k_exchange")
+PROFILE_CLASSES = ("k_pair_high", "k_pair_low", "k_diag", "k_tiny", "k_fused", "k_exchange", "k_norm",
+                   "kpass_jit")
 
 
 def profile_enable(on: bool = True) -> None:

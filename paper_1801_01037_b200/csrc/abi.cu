@@ -471,7 +471,7 @@ int svb_profile_read(int cls, int64_t *launches, double *total_ms, int64_t *alg_
 
 const char *svb_profile_class_name(int cls) {
     static const char *names[PROF_NCLASSES] = {"k_pair_high", "k_pair_low", "k_diag", "k_tiny",
-                                               "k_fused", "k_exchange", "k_norm"};
+                                               "k_fused", "k_exchange", "k_norm", "kpass_jit"};
     return (cls >= 0 && cls < PROF_NCLASSES) ? names[cls] : "";
 }
 

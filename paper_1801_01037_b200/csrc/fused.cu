@@ -1054,7 +1054,7 @@ int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsi
         } else {
             k_fused<false><<<fused_grid(ntiles), FTHREADS, fused_smem(), s>>>(a, ntiles, P);
         }
-        prof_end(s, LaunchInfo{1, PROF_FUSED, n_amps * 32});
+        prof_end(s, LaunchInfo{1, (jit && jit_fns) ? PROF_FUSED_JIT : PROF_FUSED, n_amps * 32});
         *launches += 1;
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_status(e, "k_fused launch");

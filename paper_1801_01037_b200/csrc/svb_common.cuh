@@ -168,7 +168,8 @@ enum ProfClass : int {
     PROF_FUSED = 4,      // k_fused: multi-gate shared-memory pass
     PROF_EXCHANGE = 5,   // k_exchange_own_row / k_pair_update
     PROF_NORM = 6,       // norm / probs
-    PROF_NCLASSES = 7
+    PROF_FUSED_JIT = 7,  // kpass: NVRTC-specialised fused pass (jit.cu)
+    PROF_NCLASSES = 8
 };
 struct LaunchInfo {
     int kernels;
