@@ -397,9 +397,24 @@ bool jit_build(const std::vector<FPass> &passes, bool fma, std::vector<void *> &
 
 // Host-only check: generate and NVRTC-compile every pass (no device needed).
 int jit_compile_only(const std::vector<FPass> &passes, bool fma, std::string &err) {
+    const char *dump = getenv("SVB_JIT_DUMP");  // directory: write pass sources and cubins
+    int k = 0;
     for (const FPass &P : passes) {
         std::vector<char> cubin;
-        if (!nvrtc_compile(jit_source(P, fma), cubin, err)) return -1;
+        std::string src = jit_source(P, fma);
+        if (!nvrtc_compile(src, cubin, err)) return -1;
+        if (dump) {
+            std::string base = std::string(dump) + "/pass" + std::to_string(k);
+            if (FILE *f = fopen((base + ".cu").c_str(), "w")) {
+                fwrite(src.data(), 1, src.size(), f);
+                fclose(f);
+            }
+            if (FILE *f = fopen((base + ".cubin").c_str(), "wb")) {
+                fwrite(cubin.data(), 1, cubin.size(), f);
+                fclose(f);
+            }
+        }
+        ++k;
     }
     return (int)passes.size();
 }
