@@ -957,7 +957,7 @@ struct CompiledPlan {
 };
 
 bool jit_build(const std::vector<FPass> &passes, bool fma, std::vector<void *> &fns);
-bool jit_launch(void *fn, double2 *a, int64_t ntiles, int grid, cudaStream_t s);
+bool jit_launch(void *fn, const FPass &P, double2 *a, int64_t ntiles, cudaStream_t s);
 
 static uint64_t fnv1a(const void *p, size_t len, uint64_t h) {
     const unsigned char *b = static_cast<const unsigned char *>(p);
@@ -1045,7 +1045,7 @@ int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsi
         const FPass &P = cp->passes[pi];  // ~17 KiB, a __grid_constant__ kernel parameter
         prof_begin(s);
         if (jit && jit_fns) {
-            if (!jit_launch((*jit_fns)[pi], a, ntiles, fused_grid(ntiles), s)) {
+            if (!jit_launch((*jit_fns)[pi], cp->passes[pi], a, ntiles, s)) {
                 set_error("svb jit: cuLaunchKernel failed");
                 return SVB_ECUDA;
             }

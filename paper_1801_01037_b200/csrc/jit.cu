@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -97,6 +98,9 @@ __device__ __forceinline__ void stcs(d2 *p, d2 v) {
     asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" :: "l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
 __device__ __forceinline__ int swz(int l) { return l ^ ((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7; }
+__device__ __forceinline__ double ng(double x) {  // -x as a sign-bit flip (integer pipe)
+    return __longlong_as_double(__double_as_longlong(x) ^ (long long)0x8000000000000000ull);
+}
 )";
 
 int swz_h(int l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7); }
@@ -188,55 +192,330 @@ void emit_gate(Out &o, const FGate &g) {
     if (thread_ctl) o("}\n");
 }
 
+// ---------------------------------------------------------------------------
+// Unit-factor folding (FMA mode).  Gates whose entries are 0 / +-1 / +-i
+// (X, Y, Z, S, S^dag, CZ, ...) do not need arithmetic: the generator keeps,
+// per register, a pending factor u^c (u = i, c = 0..3) meaning "the
+// amplitude is i^c times what the register holds".  A unit gate only
+// renames registers and adds to c; the next arithmetic gate absorbs i^c into
+// its coefficients (exact: multiplying a constant by +-1 / +-i swaps and
+// negates its parts), with each product term in the same position of the
+// same FMA chain as the interpreter's, so results equal the interpreter's up
+// to the sign of zero.  Factors still pending when a group stores, or before
+// a branch on the thread index, are applied with sign-bit flips (integer
+// pipe, no DP instructions).
+
+int unit_code(const double2 &z) {  // z = i^c -> c, else -1
+    if (z.y == 0.0 && z.x == 1.0) return 0;
+    if (z.x == 0.0 && z.y == 1.0) return 1;
+    if (z.y == 0.0 && z.x == -1.0) return 2;
+    if (z.x == 0.0 && z.y == -1.0) return 3;
+    return -1;
+}
+
+// logical component `comp` (0 = re, 1 = im) of register `reg` named through
+// the pending factor: returns the physical member and multiplies k's sign
+const char *phys(int c, int comp, double &k) {
+    // i^c (x + i y): c=0 (x, y)  c=1 (-y, x)  c=2 (-x, -y)  c=3 (y, -x)
+    static const int member[4][2] = {{0, 1}, {1, 0}, {0, 1}, {1, 0}};
+    static const int neg[4][2] = {{0, 0}, {1, 0}, {1, 1}, {0, 1}};
+    if (neg[c][comp]) k = -k;
+    return member[c][comp] ? "y" : "x";
+}
+
+struct Term {
+    double k;
+    const char *var;  // "L" / "H" / "X"
+    int comp;         // logical component
+    int code;         // pending factor of that register
+};
+
+// k0*t0 + (k1*t1 + (... + kn*tn)) as the interpreter's FMA chain
+std::string chain(const std::vector<Term> &ts) {
+    std::string e;
+    for (int i = (int)ts.size() - 1; i >= 0; --i) {
+        double k = ts[i].k;
+        const char *m = phys(ts[i].code, ts[i].comp, k);
+        char b[160];
+        if (i == (int)ts.size() - 1)
+            snprintf(b, sizeof b, "__dmul_rn(%s, %s.%s)", lit(k).c_str(), ts[i].var, m);
+        else
+            snprintf(b, sizeof b, "__fma_rn(%s, %s.%s, ", lit(k).c_str(), ts[i].var, m);
+        e = (i == (int)ts.size() - 1) ? std::string(b) : std::string(b) + e + ")";
+    }
+    return e;
+}
+
+void materialize(Out &o, int *code, int i) {
+    switch (code[i]) {
+        case 1: o("v[%d] = mk(ng(v[%d].y), v[%d].x);\n", i, i, i); break;
+        case 2: o("v[%d] = mk(ng(v[%d].x), ng(v[%d].y));\n", i, i, i); break;
+        case 3: o("v[%d] = mk(v[%d].y, ng(v[%d].x));\n", i, i, i); break;
+        default: break;
+    }
+    code[i] = 0;
+}
+
+// a*X for complex constant a (cm form): re = a.x X.x - a.y X.y, im = a.x X.y + a.y X.x
+std::string cm_fold(const double2 &a, int cx) {
+    return "mk(" + chain({{a.x, "X", 0, cx}, {-a.y, "X", 1, cx}}) + ", " +
+           chain({{a.x, "X", 1, cx}, {a.y, "X", 0, cx}}) + ")";
+}
+
+void emit_gate_fold(Out &o, const FGate &g, int *code) {
+    const double2 *m = g.m;
+    const int op = g.op;
+    const bool thread_ctl = g.cl >= 0;
+    if (op < FOP_DIAG) {
+        const int kind = (op >> 1) / FSLOTS, s = (op >> 1) % FSLOTS, ctrl = op & 1;
+        const int u12 = unit_code(m[1]), u21 = unit_code(m[2]);
+        const bool unit_anti = m[0].x == 0.0 && m[0].y == 0.0 && m[3].x == 0.0 && m[3].y == 0.0 && u12 >= 0 &&
+                               u21 >= 0;
+        std::vector<int> lows;
+        for (int i = 0; i < FREGS; ++i) {
+            if (i & (1 << s)) continue;
+            if (ctrl && !((g.cmask >> i) & 1)) continue;
+            lows.push_back(i);
+        }
+        if (thread_ctl) {  // per-thread branch: pending factors must be uniform first
+            for (int i : lows) {
+                materialize(o, code, i);
+                materialize(o, code, i | (1 << s));
+            }
+            o("if ((tid >> %d) & 1) {\n", g.cl);
+        }
+        for (int i : lows) {
+            const int j = i | (1 << s);
+            const int cL = code[i], cH = code[j];
+            if (unit_anti && !thread_ctl) {  // lo' = i^u12 hi, hi' = i^u21 lo: rename
+                o("{ const d2 t = v[%d]; v[%d] = v[%d]; v[%d] = t; }\n", i, i, j, j);
+                code[i] = (u12 + cH) & 3;
+                code[j] = (u21 + cL) & 3;
+                continue;
+            }
+            std::string lo, hi;
+            switch (kind) {
+                case FK_REAL:
+                    lo = "mk(" + chain({{m[0].x, "L", 0, cL}, {m[1].x, "H", 0, cH}}) + ", " +
+                         chain({{m[0].x, "L", 1, cL}, {m[1].x, "H", 1, cH}}) + ")";
+                    hi = "mk(" + chain({{m[2].x, "L", 0, cL}, {m[3].x, "H", 0, cH}}) + ", " +
+                         chain({{m[2].x, "L", 1, cL}, {m[3].x, "H", 1, cH}}) + ")";
+                    break;
+                case FK_RX:  // rirow(a, r, s, im) = (a r.x - s im.y, a r.y + s im.x)
+                    lo = "mk(" + chain({{m[0].x, "L", 0, cL}, {-m[1].y, "H", 1, cH}}) + ", " +
+                         chain({{m[0].x, "L", 1, cL}, {m[1].y, "H", 0, cH}}) + ")";
+                    hi = "mk(" + chain({{m[3].x, "H", 0, cH}, {-m[2].y, "L", 1, cL}}) + ", " +
+                         chain({{m[3].x, "H", 1, cH}, {m[2].y, "L", 0, cL}}) + ")";
+                    break;
+                case FK_ANTI:  // cm(q12, H), cm(q21, L)
+                    lo = "mk(" + chain({{m[1].x, "H", 0, cH}, {-m[1].y, "H", 1, cH}}) + ", " +
+                         chain({{m[1].x, "H", 1, cH}, {m[1].y, "H", 0, cH}}) + ")";
+                    hi = "mk(" + chain({{m[2].x, "L", 0, cL}, {-m[2].y, "L", 1, cL}}) + ", " +
+                         chain({{m[2].x, "L", 1, cL}, {m[2].y, "L", 0, cL}}) + ")";
+                    break;
+                default:  // row(a, L, b, H)
+                    lo = "mk(" +
+                         chain({{m[0].x, "L", 0, cL}, {-m[0].y, "L", 1, cL}, {m[1].x, "H", 0, cH},
+                                {-m[1].y, "H", 1, cH}}) +
+                         ", " +
+                         chain({{m[0].x, "L", 1, cL}, {m[0].y, "L", 0, cL}, {m[1].x, "H", 1, cH},
+                                {m[1].y, "H", 0, cH}}) +
+                         ")";
+                    hi = "mk(" +
+                         chain({{m[2].x, "L", 0, cL}, {-m[2].y, "L", 1, cL}, {m[3].x, "H", 0, cH},
+                                {-m[3].y, "H", 1, cH}}) +
+                         ", " +
+                         chain({{m[2].x, "L", 1, cL}, {m[2].y, "L", 0, cL}, {m[3].x, "H", 1, cH},
+                                {m[3].y, "H", 0, cH}}) +
+                         ")";
+            }
+            o("{ const d2 L = v[%d], H = v[%d];\nv[%d] = %s;\nv[%d] = %s; }\n", i, j, i, lo.c_str(), j, hi.c_str());
+            code[i] = code[j] = 0;
+        }
+        if (thread_ctl) o("}\n");
+        return;
+    }
+    const int code_ = op - FOP_DIAG;
+    const int ctrl = code_ & 1, tpos = (code_ >> 1) % (FSLOTS + 1), var = (code_ >> 1) / (FSLOTS + 1);
+    const bool d0_one = var != FD_GENERAL;
+    const bool branch = thread_ctl || tpos == FSLOTS;
+    std::vector<int> regs;
+    for (int i = 0; i < FREGS; ++i)
+        if (!ctrl || ((g.cmask >> i) & 1)) regs.push_back(i);
+    auto mul = [&](int i, const double2 &d) {
+        const int u = unit_code(d);
+        if (u >= 0 && !branch) {
+            code[i] = (code[i] + u) & 3;
+            return;
+        }
+        if (u == 2) {  // -1 inside a branch: sign flips
+            o("v[%d] = mk(ng(v[%d].x), ng(v[%d].y));\n", i, i, i);
+            return;
+        }
+        o("{ const d2 X = v[%d]; v[%d] = %s; }\n", i, i, cm_fold(d, code[i]).c_str());
+        code[i] = 0;
+    };
+    if (branch)
+        for (int i : regs) materialize(o, code, i);
+    if (thread_ctl) o("if ((tid >> %d) & 1) {\n", g.cl);
+    if (tpos == FSLOTS) {
+        o("if ((tid >> %d) & 1) {\n", g.tl);
+        for (int i : regs) mul(i, m[3]);
+        o("}");
+        if (!d0_one) {
+            o(" else {\n");
+            for (int i : regs) mul(i, m[0]);
+            o("}");
+        }
+        o("\n");
+    } else {
+        for (int i : regs) {
+            if ((i >> tpos) & 1)
+                mul(i, m[3]);
+            else if (!d0_one)
+                mul(i, m[0]);
+        }
+    }
+    if (thread_ctl) o("}\n");
+}
+
 }  // namespace
 
+// Tile pipelining modes of the generated kernel:
+//   0  one shared buffer, 4 CTAs/SM; the first group reads HBM directly when
+//      its rows are coalesced, otherwise cp.async fills the buffer first
+//   1  two shared buffers, 3 CTAs/SM: tile i+1 streams in (cp.async) while
+//      the groups of tile i run; the first group reads shared memory
+//   2  one buffer, 4 CTAs/SM: once the last group has read its registers the
+//      buffer is free, so the next tile's cp.async fill is issued there and
+//      overlaps the last group's arithmetic and direct HBM stores (passes
+//      without a direct last group use mode 0)
+int jit_mode() {
+    static int m = [] {
+        const char *e = getenv("SVB_JIT_MODE");
+        int v = e ? atoi(e) : 0;
+        return (v >= 0 && v <= 2) ? v : 0;
+    }();
+    return m;
+}
+
+int jit_pass_mode(const FPass &P) {
+    int m = jit_mode();
+    if (m == 2 && !P.direct_last) m = 0;
+    return m;
+}
+
+// resident CTAs per SM the generated kernel is built for (__launch_bounds__)
+int jit_ctas_per_sm(const FPass &P) {
+    static int c = [] {
+        const char *e = getenv("SVB_JIT_CTAS");
+        int v = e ? atoi(e) : FCTAS_PER_SM;
+        return (v >= 1 && v <= 8) ? v : FCTAS_PER_SM;
+    }();
+    return jit_pass_mode(P) == 1 ? 3 : c;
+}
+// tile buffers live in dynamic shared memory when they exceed the 48 KiB
+// static limit (double buffering, or FM >= 12 builds)
+size_t jit_dyn_smem(const FPass &P) {
+    const size_t b = (jit_pass_mode(P) == 1 ? 2 : 1) * FTILE * sizeof(double2);
+    return b > 40 * 1024 ? b : 0;
+}
+
+// Thread-index copy the compiler cannot see through: per-thread address
+// terms are recomputed where they are used instead of being hoisted out of
+// the tile loop and kept live (or spilled) across the gate arithmetic.
+const char *kOpaqueTid = "unsigned tg = tid; asm volatile(\"\" : \"+r\"(tg));\n";
+
 std::string jit_source(const FPass &P, bool fma) {
+    const int mode = jit_pass_mode(P);
     Out o;
     o("#define SVB_FMA %d\n", fma ? 1 : 0);
     o.s += kPreamble;
     const int nrows = FTILE >> P.flow;
     const int colmask = (1 << P.flow) - 1;
     o("extern \"C\" __global__ void __launch_bounds__(%d, %d) kpass(d2 *__restrict__ a, i64 ntiles) {\n",
-      FTHREADS, FCTAS_PER_SM);
-    o("__shared__ alignas(16) d2 buf[%d];\n__shared__ i64 rowoff[%d];\n", FTILE, nrows);
-    o("const int tid = threadIdx.x;\nunsigned char *sb = reinterpret_cast<unsigned char *>(buf);\n");
+      FTHREADS, jit_ctas_per_sm(P));
+    if (jit_dyn_smem(P))
+        o("extern __shared__ d2 dsm[];\n");
+    else
+        o("__shared__ alignas(16) d2 dsm[%d];\n", FTILE);
+    o("__shared__ i64 rowoff[%d];\n", nrows);
+    o("const int tid = threadIdx.x;\n");
     o("for (int r = tid; r < %d; r += %d) { i64 off = 0;\n", nrows, FTHREADS);
     for (int j = 0; j < FM - P.flow; ++j) o("if ((r >> %d) & 1) off |= 1ll << %d;\n", j, P.rowbit[j]);
     o("rowoff[r] = off; }\n__syncthreads();\n");
-    o("for (i64 tix = blockIdx.x; tix < ntiles; tix += gridDim.x) {\ni64 base = 0;\n");
-    for (int j = 0; j < P.ncomp; ++j) o("base |= ((tix >> %d) & 1) << %d;\n", j, P.comp[j]);
-    if (!P.direct_first) {
-        o("#pragma unroll\nfor (int k = 0; k < %d; ++k) { int e = tid + k * %d;\n", FREGS, FTHREADS);
-        o("cpa(&buf[swz(e)], &a[base + rowoff[e >> %d] + (e & %d)]); }\n", P.flow, colmask);
-        o("asm volatile(\"cp.async.commit_group;\\ncp.async.wait_group 0;\\n\" ::: \"memory\");\n__syncthreads();\n");
+    o("auto tbase = [&](i64 t) { i64 b = 0;\n");
+    for (int j = 0; j < P.ncomp; ++j) o("b |= ((t >> %d) & 1) << %d;\n", j, P.comp[j]);
+    o("return b; };\n");
+    o("auto fill = [&](d2 *dst, i64 b) {\n%s#pragma unroll\nfor (int k = 0; k < %d; ++k) { int e = tg + k * %d;\n", kOpaqueTid,
+      FREGS, FTHREADS);
+    o("cpa(&dst[swz(e)], &a[b + rowoff[e >> %d] + (e & %d)]); }\n", P.flow, colmask);
+    o("asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\"); };\n(void)fill;\n");
+    const char *wait_all = "asm volatile(\"cp.async.wait_group 0;\\n\" ::: \"memory\");\n";
+    const bool direct_first = P.direct_first && mode == 0;
+    if (mode != 0) o("if (blockIdx.x < ntiles) fill(dsm, tbase(blockIdx.x));\n");
+    o("int it = 0;\nfor (i64 tix = blockIdx.x; tix < ntiles; tix += gridDim.x, ++it) {\n");
+    o("const i64 base = tbase(tix);\n");
+    if (mode == 1) {
+        o("d2 *buf = dsm + (it & 1) * %d;\n", FTILE);
+        o.s += wait_all;
+        o("__syncthreads();\n{ const i64 nx = tix + gridDim.x; if (nx < ntiles) fill(dsm + ((it + 1) & 1) * %d, tbase(nx)); }\n",
+          FTILE);
+    } else {
+        o("d2 *buf = dsm;\n");
+        if (mode == 2) {
+            o.s += wait_all;
+            o("__syncthreads();\n");
+        } else if (!direct_first) {
+            o("fill(buf, base);\n");
+            o.s += wait_all;
+            o("__syncthreads();\n");
+        }
     }
+    o("unsigned char *sb = reinterpret_cast<unsigned char *>(buf);\n");
     o("d2 v[%d];\n", FREGS);
     for (int gi = 0; gi < P.ngroups; ++gi) {
         const FGroup &G = P.groups[gi];
         const bool last = gi == P.ngroups - 1;
         o("{ // group %d\n", gi);
-        if (gi == 0 && P.direct_first) {
+        if (gi == 0 && direct_first) {
             o("i64 g0 = %lldll;\n", (long long)P.gl_b);
-            for (int j = 0; j < FTBITS; ++j) o("if ((tid >> %d) & 1) g0 ^= %lldll;\n", j, (long long)P.gl_t[j]);
+            o.s += kOpaqueTid;
+            for (int j = 0; j < FTBITS; ++j) o("if ((tg >> %d) & 1) g0 ^= %lldll;\n", j, (long long)P.gl_t[j]);
             for (int i = 0; i < FREGS; ++i)
                 o("v[%d] = ldcs(a + (base | (g0 ^ %lldll)));\n", i, (long long)xcombo_g(P.gl_s, i));
         } else {
             o("unsigned a0 = %uu;\n", (unsigned)G.ld_b);
-            for (int j = 0; j < FTBITS; ++j) o("if ((tid >> %d) & 1) a0 ^= %uu;\n", j, (unsigned)G.ld_t[j]);
+            o.s += kOpaqueTid;
+            for (int j = 0; j < FTBITS; ++j) o("if ((tg >> %d) & 1) a0 ^= %uu;\n", j, (unsigned)G.ld_t[j]);
             for (int i = 0; i < FREGS; ++i)
                 o("v[%d] = *reinterpret_cast<const d2 *>(sb + (a0 ^ %uu));\n", i, xcombo_h(G.ld_s, i));
         }
-        for (int q = G.first; q < G.first + G.count; ++q) emit_gate(o, P.gates[q]);
+        if (last && mode == 2) {
+            // every thread has its registers: refill the buffer with the next tile
+            o("__syncthreads();\n{ const i64 nx = tix + gridDim.x; if (nx < ntiles) fill(dsm, tbase(nx)); }\n");
+        }
+        if (fma) {
+            int code[FREGS] = {0};
+            for (int q = G.first; q < G.first + G.count; ++q) emit_gate_fold(o, P.gates[q], code);
+            for (int i = 0; i < FREGS; ++i) materialize(o, code, i);
+        } else {
+            for (int q = G.first; q < G.first + G.count; ++q) emit_gate(o, P.gates[q]);
+        }
         if (last && P.direct_last) {
-            if (G.perm && gi == 0 && P.direct_first) o("__syncthreads();\n");
+            if (G.perm && gi == 0 && direct_first) o("__syncthreads();\n");
             o("i64 s0 = %lldll;\n", (long long)P.gs_b);
-            for (int j = 0; j < FTBITS; ++j) o("if ((tid >> %d) & 1) s0 ^= %lldll;\n", j, (long long)P.gs_t[j]);
+            o("{\n%s", kOpaqueTid);
+            for (int j = 0; j < FTBITS; ++j) o("if ((tg >> %d) & 1) s0 ^= %lldll;\n", j, (long long)P.gs_t[j]);
+            o("}\n");
             for (int i = 0; i < FREGS; ++i)
                 o("stcs(a + (base | (s0 ^ %lldll)), v[%d]);\n", (long long)xcombo_g(P.gs_s, i), i);
         } else {
             if (G.perm) o("__syncthreads();\n");
             o("unsigned b0 = %uu;\n", (unsigned)G.st_b);
-            for (int j = 0; j < FTBITS; ++j) o("if ((tid >> %d) & 1) b0 ^= %uu;\n", j, (unsigned)G.st_t[j]);
+            o("{\n%s", kOpaqueTid);
+            for (int j = 0; j < FTBITS; ++j) o("if ((tg >> %d) & 1) b0 ^= %uu;\n", j, (unsigned)G.st_t[j]);
+            o("}\n");
             for (int i = 0; i < FREGS; ++i)
                 o("*reinterpret_cast<d2 *>(sb + (b0 ^ %uu)) = v[%d];\n", xcombo_h(G.st_s, i), i);
             o("__syncthreads();\n");
@@ -244,10 +523,15 @@ std::string jit_source(const FPass &P, bool fma) {
         o("}\n");
     }
     if (!P.direct_last) {
-        o("#pragma unroll\nfor (int k = 0; k < %d; ++k) { int e = tid + k * %d;\n", FREGS, FTHREADS);
-        o("a[base + rowoff[e >> %d] + (e & %d)] = buf[swz(e)]; }\n", P.flow, colmask);
+        o("{\n%s#pragma unroll\nfor (int k = 0; k < %d; ++k) { int e = tg + k * %d;\n", kOpaqueTid, FREGS, FTHREADS);
+        o("a[base + rowoff[e >> %d] + (e & %d)] = buf[swz(e)]; }\n}\n", P.flow, colmask);
     }
-    o("__syncthreads();\n}\n}\n");
+    // mode 0: the buffer must be free before the next tile's loads; modes 1/2
+    // order reuse with the barrier after the next wait
+    if (mode == 0) o("__syncthreads();\n");
+    o("}\n");
+    if (mode != 0) o.s += wait_all;
+    o("}\n");
     return o.s;
 }
 
@@ -318,8 +602,9 @@ static bool nvrtc_compile(const std::string &src, std::vector<char> &cubin, std:
         log = "nvrtcCreateProgram failed";
         return false;
     }
-    const char *opts[] = {"-arch=sm_100a", "-std=c++17", "-default-device", "-fmad=false"};
-    if (nv.compile(prog, 4, opts) != 0) {
+    const char *opts[] = {"-arch=sm_100a", "-std=c++17", "-default-device", "-fmad=false", "-lineinfo"};
+    static const int nopts = getenv("SVB_JIT_LINEINFO") ? 5 : 4;  // for ncu source pages
+    if (nv.compile(prog, nopts, opts) != 0) {
         size_t n = 0;
         nv.log_size(prog, &n);
         log.assign(n, '\0');
@@ -333,6 +618,13 @@ static bool nvrtc_compile(const std::string &src, std::vector<char> &cubin, std:
     nv.cubin(prog, cubin.data());
     nv.destroy(&prog);
     return true;
+}
+
+static bool set_dyn_smem(cudaKernel_t fn, size_t bytes) {
+    int d = 0;
+    cudaGetDevice(&d);
+    return cudaKernelSetAttributeForDevice(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes, d) ==
+           cudaSuccess;
 }
 
 // Compile (or fetch) one kernel per pass.  Returns false and leaves
@@ -383,7 +675,8 @@ bool jit_build(const std::vector<FPass> &passes, bool fma, std::vector<void *> &
             JitFn f;
             if (cudaLibraryLoadData(&f.lib, cubins[i].data(), nullptr, nullptr, 0, nullptr, nullptr, 0) !=
                     cudaSuccess ||
-                cudaLibraryGetKernel(&f.fn, f.lib, "kpass") != cudaSuccess) {
+                cudaLibraryGetKernel(&f.fn, f.lib, "kpass") != cudaSuccess ||
+                (jit_dyn_smem(passes[i]) && !set_dyn_smem(f.fn, jit_dyn_smem(passes[i])))) {
                 cudaGetLastError();
                 fns.clear();
                 return false;
@@ -419,10 +712,17 @@ int jit_compile_only(const std::vector<FPass> &passes, bool fma, std::string &er
     return (int)passes.size();
 }
 
-bool jit_launch(void *fn, double2 *a, int64_t ntiles, int grid, cudaStream_t s) {
+bool jit_launch(void *fn, const FPass &P, double2 *a, int64_t ntiles, cudaStream_t s) {
+    static int sms = [] {
+        int d = 0, v = 148;
+        cudaGetDevice(&d);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+        return v;
+    }();
+    const int grid = (int)std::min<int64_t>(ntiles, int64_t(sms) * jit_ctas_per_sm(P));
     long long nt = ntiles;
     void *args[] = {&a, &nt};
-    return cudaLaunchKernel((const void *)fn, dim3(grid), dim3(FTHREADS), args, 0, s) == cudaSuccess;
+    return cudaLaunchKernel((const void *)fn, dim3(grid), dim3(FTHREADS), args, jit_dyn_smem(P), s) == cudaSuccess;
 }
 
 }  // namespace svb
