@@ -567,7 +567,9 @@ struct GateMeta {
 // Thread-bit -> local-bit map for a group: the 3 lowest thread bits (which
 // vary across the 8 lanes of an LDS.128 phase) go to non-slot local bits
 // with distinct (bit mod 3) so the swizzle spreads them over 8 chunks.
-static void thread_map(const int *slots, int8_t *tmap) {
+static void thread_map(const int *slots, int8_t *tmap, const int16_t *qcol = nullptr,
+                       const int16_t *mcol = nullptr, bool need_ld = false, bool need_st = false,
+                       bool keep012 = false) {
     bool is_slot[FM] = {};
     for (int i = 0; i < FSLOTS; ++i) is_slot[slots[i]] = true;
     std::vector<int> free_bits;
@@ -585,13 +587,48 @@ static void thread_map(const int *slots, int8_t *tmap) {
         order = {pick[0], pick[1], pick[2]};
         std::sort(order.begin(), order.end());
     }
+    // With X/CNOT maps folded into the group's load (Q) or store (P) map, the
+    // lanes of a phase address Q(l) / P(l) instead of l: keep the 3 lanes'
+    // bank vectors independent for the accesses that go through shared
+    // memory, otherwise each STS.128 / LDS.128 takes 2-4x the wavefronts.
+    auto bank = [](int col) { return (col ^ (col >> 3) ^ (col >> 6) ^ (col >> 9)) & 7; };
+    auto rank3 = [&](const int16_t *cols, int a, int b, int c) {
+        const int x = bank(cols[a]), y = bank(cols[b]), z = bank(cols[c]);
+        if (!x || !y || !z || x == y || x == z || y == z) return false;
+        return (x ^ y ^ z) != 0;
+    };
+    auto ok = [&](int a, int b, int c) {
+        return (!need_ld || rank3(qcol, a, b, c)) && (!need_st || rank3(mcol, a, b, c));
+    };
+    // (a first / last group on local bits 0-2 keeps them: direct HBM access wins)
+    const bool direct_pick = order.size() == 3 && order[0] == 0 && order[1] == 1 && order[2] == 2;
+    if (qcol && !(keep012 && direct_pick) && (order.size() < 3 || !ok(order[0], order[1], order[2]))) {
+        const int nf = (int)free_bits.size();
+        bool found = false;
+        for (int i = 0; i < nf && !found; ++i)
+            for (int j = i + 1; j < nf && !found; ++j)
+                for (int k = j + 1; k < nf && !found; ++k)
+                    if (ok(free_bits[i], free_bits[j], free_bits[k])) {
+                        order = {free_bits[i], free_bits[j], free_bits[k]};
+                        found = true;
+                    }
+    }
     for (int b : free_bits)
         if (std::find(order.begin(), order.end(), b) == order.end()) order.push_back(b);
     for (int j = 0; j < FTBITS; ++j) tmap[j] = (int8_t)order[j];
 }
 
+// In-register X / CNOT (see the group scan) pays off when passes are JIT
+// compiled (a register rename); the interpreter would run them as arithmetic,
+// so it keeps deferring them.  SVB_FUSE_REGPERM=0/1 forces either.
+// (read per call: tests flip it to compare JIT and interpreter on one plan)
+static bool reg_perm(unsigned flags) {
+    const char *e = getenv("SVB_FUSE_REGPERM");
+    return e ? atoi(e) != 0 : (flags & SVB_RUN_JIT) != 0;
+}
+
 // Build the kernel descriptor for one pass; false if it does not fit.
-static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, bool strict) {
+static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, bool strict, bool regperm) {
     memset(&P, 0, sizeof(P));
     P.flow = flow_bits();
     int local_of[64];
@@ -672,9 +709,9 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
         return std::find(g.slots.begin(), g.slots.end(), m.tl) != g.slots.end() ||
                (int)g.slots.size() < FSLOTS;
     };
-    auto take = [&](GroupPlan &g, int q) {
+    auto take = [&](GroupPlan &g, int q, bool inreg = false) {
         const GateMeta &m = meta[q];
-        if (m.perm) {
+        if (m.perm && !inreg) {
             if (g.gates.empty() && g.permq == 0)
                 pre_perm(g, m);
             else
@@ -710,11 +747,16 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
                     if (placed[q]) continue;
                     const GateMeta &m = meta[q];
                     const uint64_t bits = gbits(m);
+                    // an X / CNOT whose target fits the group's slots runs in
+                    // registers (a masked register swap) instead of being
+                    // deferred to the store map, so it blocks nothing
+                    const bool inreg = m.perm && mode == 0 && regperm && (bits & blocked) == 0 &&
+                                       (bits & g->permq) == 0 && fits(*g, m);
                     bool ok = (bits & blocked) == 0 &&
-                              (m.perm ? mode != 0
+                              (m.perm ? (mode != 0 || inreg)
                                       : (mode != 2 && (bits & g->permq) == 0 && fits(*g, m)));
                     if (ok) {
-                        take(*g, q);
+                        take(*g, q, inreg);
                         placed[q] = 1;
                         --left;
                         progress = true;
@@ -760,7 +802,6 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
         std::sort(slots, slots + FSLOTS);
         FGroup &G = P.groups[gi];
         for (int i = 0; i < FSLOTS; ++i) G.pos[i] = (int8_t)slots[i];
-        thread_map(slots, G.tmap);
         G.first = (int16_t)k0;
         G.count = (int16_t)gp.gates.size();
         G.mb = (int16_t)gp.mb;
@@ -771,6 +812,7 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
             if (gp.mcol[j] != (1 << j) || gp.qcol[j] != (1 << j)) G.perm = 1;
         }
         G.qb = (int16_t)gp.qb;
+        thread_map(slots, G.tmap, G.qcol, G.mcol, gi > 0, gi < P.ngroups - 1, gi == 0 || gi == P.ngroups - 1);
         for (int j = 0; j < FTBITS; ++j) {
             G.ld_t[j] = (uint16_t)(16 * swz(gp.qcol[G.tmap[j]]));
             G.st_t[j] = (uint16_t)(16 * swz(gp.mcol[G.tmap[j]]));
@@ -908,7 +950,7 @@ int jit_check(int n, const svb_op *ops, int nops, unsigned flags) {
     std::vector<FPass> passes;
     FPass P;
     for (const PlanPass &pp : plan(n, ops, nops, strict))
-        if (pp.ops.size() > 1 && build_pass(n, ops, pp, P, strict)) passes.push_back(P);
+        if (pp.ops.size() > 1 && build_pass(n, ops, pp, P, strict, reg_perm(flags))) passes.push_back(P);
     std::string err;
     int r = jit_compile_only(passes, (flags & SVB_RUN_FMA) && !strict, err);
     if (r < 0) set_error("jit compile failed: %.400s", err.c_str());
@@ -924,7 +966,7 @@ int plan_passes(int n, const svb_op *ops, int nops, unsigned flags, int *groups)
         FPass P;
         int df = 0, dl = 0, nf = 0;
         for (const PlanPass &pp : passes)
-            if (pp.ops.size() > 1 && build_pass(n, ops, pp, P, strict)) {
+            if (pp.ops.size() > 1 && build_pass(n, ops, pp, P, strict, reg_perm(flags))) {
                 *groups += P.ngroups;
                 df += P.direct_first;
                 dl += P.direct_last;
@@ -946,7 +988,7 @@ struct PlanStep {
 };
 struct CompiledPlan {
     int n;
-    bool strict;
+    bool strict, regperm;
     std::vector<svb_op> ops;  // exact key
     std::vector<PlanStep> steps;
     std::vector<FPass> passes;
@@ -965,17 +1007,19 @@ static uint64_t fnv1a(const void *p, size_t len, uint64_t h) {
     return h;
 }
 
-static std::shared_ptr<const CompiledPlan> compiled_plan(int n, const svb_op *ops, int nops, bool strict) {
+static std::shared_ptr<const CompiledPlan> compiled_plan(int n, const svb_op *ops, int nops, bool strict,
+                                                         bool regperm) {
     static std::mutex mu;
     static std::vector<std::pair<uint64_t, std::shared_ptr<const CompiledPlan>>> cache;  // MRU first
     uint64_t key = fnv1a(ops, sizeof(svb_op) * size_t(nops), 1469598103934665603ull);
     key = fnv1a(&n, sizeof n, key);
     key = fnv1a(&strict, sizeof strict, key);
+    key = fnv1a(&regperm, sizeof regperm, key);
     {
         std::lock_guard<std::mutex> lk(mu);
         for (size_t i = 0; i < cache.size(); ++i) {
             const auto &c = cache[i].second;
-            if (cache[i].first == key && c->n == n && c->strict == strict && (int)c->ops.size() == nops &&
+            if (cache[i].first == key && c->n == n && c->strict == strict && c->regperm == regperm && (int)c->ops.size() == nops &&
                 std::memcmp(c->ops.data(), ops, sizeof(svb_op) * size_t(nops)) == 0) {
                 auto hit = cache[i];
                 cache.erase(cache.begin() + i);
@@ -987,10 +1031,11 @@ static std::shared_ptr<const CompiledPlan> compiled_plan(int n, const svb_op *op
     auto cp = std::make_shared<CompiledPlan>();
     cp->n = n;
     cp->strict = strict;
+    cp->regperm = regperm;
     cp->ops.assign(ops, ops + nops);
     FPass P;
     for (const PlanPass &pp : plan(n, ops, nops, strict)) {
-        if (pp.ops.size() > 1 && build_pass(n, ops, pp, P, strict)) {
+        if (pp.ops.size() > 1 && build_pass(n, ops, pp, P, strict, regperm)) {
             cp->steps.push_back(PlanStep{-1});
             cp->passes.push_back(P);
         } else {
@@ -1025,7 +1070,7 @@ int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsi
     }
     const bool strict = flags & SVB_RUN_STRICT_ORDER;
     const bool fma = (flags & SVB_RUN_FMA) && !strict;
-    std::shared_ptr<const CompiledPlan> cp = compiled_plan(n, ops, nops, strict);
+    std::shared_ptr<const CompiledPlan> cp = compiled_plan(n, ops, nops, strict, reg_perm(flags));
     const int64_t ntiles = n_amps >> FM;
     size_t next_pass = 0;
     const bool jit = (flags & SVB_RUN_JIT) && !cp->passes.empty();

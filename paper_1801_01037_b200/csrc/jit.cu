@@ -277,6 +277,30 @@ void emit_gate_fold(Out &o, const FGate &g, int *code) {
             if (ctrl && !((g.cmask >> i) & 1)) continue;
             lows.push_back(i);
         }
+        if (thread_ctl && unit_anti) {
+            // controlled X / Y on a thread-bit control: a conditional swap (plus
+            // sign flips for Y-like entries).  Equal pending factors on both
+            // registers of a pair survive an X swap unchanged.
+            for (int i : lows) {
+                const int j = i | (1 << s);
+                if (u12 != 0 || u21 != 0 || code[i] != code[j]) {
+                    materialize(o, code, i);
+                    materialize(o, code, j);
+                }
+            }
+            o("if ((tid >> %d) & 1) {\n", g.cl);
+            for (int i : lows) {
+                const int j = i | (1 << s);
+                o("{ const d2 t = v[%d]; v[%d] = v[%d]; v[%d] = t; }\n", i, i, j, j);
+                int tmp[FREGS] = {0};
+                tmp[i] = u12;
+                tmp[j] = u21;
+                materialize(o, tmp, i);
+                materialize(o, tmp, j);
+            }
+            o("}\n");
+            return;
+        }
         if (thread_ctl) {  // per-thread branch: pending factors must be uniform first
             for (int i : lows) {
                 materialize(o, code, i);

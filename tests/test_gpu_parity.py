@@ -149,9 +149,12 @@ def test_fused_fma_within_tolerance(cuda_ok, n):
 
 
 @pytest.mark.parametrize("n", [14, 19])
-def test_jit_passes_bit_identical_to_interpreter(cuda_ok, n):
-    # SVB_RUN_JIT compiles each fused pass to straight-line code; it must give
-    # exactly the interpreter's bits (exact and FMA arithmetic, perms, controls)
+def test_jit_passes_bit_identical_to_interpreter(cuda_ok, n, monkeypatch):
+    # SVB_RUN_JIT compiles each fused pass to straight-line code; on the same
+    # plan it must give exactly the interpreter's bits (exact and FMA
+    # arithmetic, perms, controls).  JIT plans run X / CNOT in registers by
+    # default; SVB_FUSE_REGPERM=1 gives the interpreter that same plan.
+    monkeypatch.setenv("SVB_FUSE_REGPERM", "1")
     rng = np.random.default_rng(600 + n)
     x = standard_gate("x")
     pool = all_gates(rng) + [x, x, Gate2x2(1, 0, 0, -1j)]
@@ -172,6 +175,15 @@ def test_jit_passes_bit_identical_to_interpreter(cuda_ok, n):
             assert np.array_equal(got, ref), (fma, np.max(np.abs(got - ref)))
         want = oracle.run_ops(a.copy(), w.oracle_ops(circ))
         assert np.max(np.abs(got - want)) <= TOL
+        # default plans (JIT: in-register perms; interpreter: deferred) agree
+        # to rounding, and strict order stays bit-exact through the JIT
+        monkeypatch.delenv("SVB_FUSE_REGPERM")
+        got = device.simulate(circ, a.copy(), fma=True, jit=True)
+        assert np.max(np.abs(got - want)) <= TOL
+        got = device.simulate(circ, a.copy(), strict_order=True, jit=True)
+        ref = device.simulate(circ, a.copy(), strict_order=True)
+        assert np.array_equal(got, ref)
+        monkeypatch.setenv("SVB_FUSE_REGPERM", "1")
 
 
 @pytest.mark.parametrize("n", [14, 17])
