@@ -413,13 +413,63 @@ static uint64_t op_mask(const svb_op &o) {
     return m;
 }
 
+// Commutation classes for hoisting (non-strict planners).  On each qubit an
+// op acts as Z-type (diagonal there: diagonal gates, and every control),
+// X-type (a I + b X: X, Rx -- and CNOT on its target) or general.  Two ops
+// whose factors on every shared qubit are both Z-type or both X-type commute
+// exactly, so a later op may be hoisted over an unplaced earlier one unless
+// some shared qubit mixes classes.  (Reordering changes rounding only: the
+// non-strict modes promise 1e-12, strict order is bit-exact.)
+struct Blocking {
+    uint64_t z = 0, x = 0, g = 0;
+    uint64_t all() const { return z | x | g; }
+};
+static bool commute_hoist() {
+    static int v = [] {
+        const char *e = getenv("SVB_FUSE_COMMUTE");
+        return e ? atoi(e) : 1;
+    }();
+    return v != 0;
+}
+static Blocking op_class(const svb_op &o) {
+    Blocking b;
+    const Gate g = make_gate(o.q);
+    const uint64_t t = uint64_t(1) << o.target;
+    const bool xtype = g.m[0].x == g.m[3].x && g.m[0].y == g.m[3].y && g.m[1].x == g.m[2].x &&
+                       g.m[1].y == g.m[2].y;
+    if (!commute_hoist())
+        b.g = t;
+    else if (g.kind == K_DIAG)
+        b.z = t;
+    else if (xtype)
+        b.x = t;
+    else
+        b.g = t;
+    if (o.kind == 1) {
+        if (commute_hoist())
+            b.z |= uint64_t(1) << o.control;
+        else
+            b.g |= uint64_t(1) << o.control;
+    }
+    return b;
+}
+// may op (class c) move ahead of the unplaced ops summarised in blk?
+static bool hoistable(const Blocking &c, const Blocking &blk) {
+    return (c.z & (blk.x | blk.g)) == 0 && (c.x & (blk.z | blk.g)) == 0 && (c.g & blk.all()) == 0;
+}
+static void block_add(Blocking &blk, const Blocking &c) {
+    blk.z |= c.z;
+    blk.x |= c.x;
+    blk.g |= c.g;
+}
+
 // Greedy pass construction.  strict: only contiguous runs of ops.  Otherwise
 // a scan over the remaining ops that hoists an op past skipped ones only if
 // it shares no qubit with any skipped op (so every qubit keeps its order).
-static int planner_kind() {
+static int planner_kind() {  // 1 greedy, 2 lookahead, 3 two-pass lookahead (default)
     static int k = [] {
         const char *e = getenv("SVB_FUSE_PLANNER");
-        return e ? atoi(e) : 2;
+        return e ? atoi(e) : 3;
     }();
     return k;
 }
@@ -433,20 +483,22 @@ static std::vector<PlanPass> plan_lookahead(int n, const svb_op *ops, int nops) 
     std::vector<PlanPass> passes;
     const uint64_t low = (uint64_t(1) << flow_bits()) - 1;
     std::vector<char> done(nops, 0);
+    std::vector<Blocking> cls(nops);
+    for (int i = 0; i < nops; ++i) cls[i] = op_class(ops[i]);
     int first = 0;
     const int window = 1024;
     std::vector<int> taken;
     // ops that can join a pass with qubit set S (without marking them)
     auto absorb_count = [&](uint64_t S, int lim) {
-        uint64_t blocked = 0;
+        Blocking blocked;
         int cnt = 0;
         for (int i = first; i < nops && i < first + window; ++i) {
             if (done[i]) continue;
             uint64_t m = op_mask(ops[i]);
-            if ((m & blocked) == 0 && (m & ~S) == 0) {
+            if (hoistable(cls[i], blocked) && (m & ~S) == 0) {
                 if (++cnt >= lim) break;
             } else {
-                blocked |= m;
+                block_add(blocked, cls[i]);
             }
         }
         return cnt;
@@ -456,15 +508,15 @@ static std::vector<PlanPass> plan_lookahead(int n, const svb_op *ops, int nops) 
         p.S = low;
         for (;;) {
             // absorb everything that fits S
-            uint64_t blocked = 0;
+            Blocking blocked;
             for (int i = first; i < nops && i < first + window && (int)p.ops.size() < FMAXG; ++i) {
                 if (done[i]) continue;
                 uint64_t m = op_mask(ops[i]);
-                if ((m & blocked) == 0 && (m & ~p.S) == 0) {
+                if (hoistable(cls[i], blocked) && (m & ~p.S) == 0) {
                     p.ops.push_back(i);
                     done[i] = 1;
                 } else {
-                    blocked |= m;
+                    block_add(blocked, cls[i]);
                 }
             }
             if (popc(p.S) >= FM || (int)p.ops.size() >= FMAXG) break;
@@ -472,12 +524,12 @@ static std::vector<PlanPass> plan_lookahead(int n, const svb_op *ops, int nops) 
             uint64_t best = 0;
             double best_score = -1.0;
             int cands = 0;
-            blocked = 0;
+            blocked = Blocking();
             for (int i = first; i < nops && i < first + window && cands < 24; ++i) {
                 if (done[i]) continue;
                 uint64_t m = op_mask(ops[i]);
                 uint64_t add = m & ~p.S;
-                if ((m & blocked) == 0 && add && popc(p.S | m) <= FM) {
+                if (hoistable(cls[i], blocked) && add && popc(p.S | m) <= FM) {
                     ++cands;
                     int gain = absorb_count(p.S | m, FMAXG);
                     double score = double(gain) / popc(add);
@@ -486,7 +538,7 @@ static std::vector<PlanPass> plan_lookahead(int n, const svb_op *ops, int nops) 
                         best = m;
                     }
                 }
-                blocked |= m;
+                block_add(blocked, cls[i]);
             }
             if (!best) break;
             p.S |= best;
@@ -504,7 +556,129 @@ static std::vector<PlanPass> plan_lookahead(int n, const svb_op *ops, int nops) 
     return passes;
 }
 
+// Two-pass lookahead over the lookahead planner: for each pass, try each
+// candidate first growth of S (the ready gates that bring new qubits), finish
+// that pass greedily, then plan the following pass greedily too, and keep the
+// first growth that retires the most ops over both passes.  Host-only and
+// run once per circuit (compiled plans are cached).
+static std::vector<PlanPass> plan_beam(int n, const svb_op *ops, int nops) {
+    std::vector<PlanPass> passes;
+    const uint64_t low = (uint64_t(1) << flow_bits()) - 1;
+    std::vector<Blocking> cls(nops);
+    for (int i = 0; i < nops; ++i) cls[i] = op_class(ops[i]);
+    const int window = 1024;
+    auto absorb = [&](std::vector<char> &done, int first, PlanPass &p, bool mark) {
+        Blocking blocked;
+        int cnt = 0;
+        for (int i = first; i < nops && i < first + window && (int)p.ops.size() + cnt < FMAXG; ++i) {
+            if (done[i]) continue;
+            uint64_t m = op_mask(ops[i]);
+            if (hoistable(cls[i], blocked) && (m & ~p.S) == 0) {
+                if (mark) {
+                    p.ops.push_back(i);
+                    done[i] = 1;
+                } else {
+                    ++cnt;
+                }
+            } else {
+                block_add(blocked, cls[i]);
+            }
+        }
+        return cnt;
+    };
+    // candidate growths of p.S (distinct op masks, ready, fitting)
+    auto candidates = [&](const std::vector<char> &done, int first, const PlanPass &p, int lim) {
+        std::vector<uint64_t> out;
+        Blocking blocked;
+        for (int i = first; i < nops && i < first + window && (int)out.size() < lim; ++i) {
+            if (done[i]) continue;
+            uint64_t m = op_mask(ops[i]);
+            uint64_t add = m & ~p.S;
+            if (hoistable(cls[i], blocked) && add && popc(p.S | m) <= FM &&
+                std::find(out.begin(), out.end(), m) == out.end())
+                out.push_back(m);
+            block_add(blocked, cls[i]);
+        }
+        return out;
+    };
+    // greedy pass (as plan_lookahead) from `first`, optionally forcing the first growth
+    auto greedy = [&](std::vector<char> &done, int first, uint64_t forced) {
+        PlanPass p;
+        p.S = low;
+        bool forced_used = forced == 0;
+        for (;;) {
+            absorb(done, first, p, true);
+            if (popc(p.S) >= FM || (int)p.ops.size() >= FMAXG) break;
+            uint64_t best = 0;
+            if (!forced_used) {
+                best = forced;
+                forced_used = true;
+            } else {
+                double best_score = -1.0;
+                for (uint64_t m : candidates(done, first, p, 24)) {
+                    PlanPass q;
+                    q.S = p.S | m;
+                    int gain = absorb(done, first, q, false);
+                    double score = double(gain) / popc(m & ~p.S);
+                    if (score > best_score) {
+                        best_score = score;
+                        best = m;
+                    }
+                }
+            }
+            if (!best) break;
+            p.S |= best;
+        }
+        return p;
+    };
+    std::vector<char> done(nops, 0);
+    int first = 0;
+    auto advance = [&](const std::vector<char> &d, int f) {
+        while (f < nops && d[f]) ++f;
+        return f;
+    };
+    while (first < nops) {
+        // candidate first growths after the free absorb at S = low
+        std::vector<char> d0 = done;
+        PlanPass p0;
+        p0.S = low;
+        absorb(d0, first, p0, true);
+        static const int ncand = getenv("SVB_BEAM_C") ? atoi(getenv("SVB_BEAM_C")) : 12;
+        static const int wa = getenv("SVB_BEAM_W") ? atoi(getenv("SVB_BEAM_W")) : 2;
+        static const int depth = getenv("SVB_BEAM_D") ? atoi(getenv("SVB_BEAM_D")) : 3;
+        std::vector<uint64_t> cands = candidates(d0, first, p0, ncand);
+        uint64_t best_m = 0;
+        long best_score = -1;
+        for (uint64_t m : cands) {
+            std::vector<char> d1 = done;
+            PlanPass a = greedy(d1, first, m);
+            long score = wa * (long)a.ops.size();
+            int f1 = first;
+            for (int k = 1; k < depth; ++k) {
+                f1 = advance(d1, f1);
+                if (f1 >= nops) break;
+                score += (long)greedy(d1, f1, 0).ops.size();
+            }
+            if (score > best_score) {
+                best_score = score;
+                best_m = m;
+            }
+        }
+        PlanPass p = greedy(done, first, best_m);
+        if (p.ops.empty()) {  // guard: the first pending op always fits
+            p.ops.push_back(first);
+            p.S |= op_mask(ops[first]);
+            done[first] = 1;
+        }
+        first = advance(done, first);
+        for (int q = 0; q < n && popc(p.S) < FM; ++q) p.S |= uint64_t(1) << q;
+        passes.push_back(std::move(p));
+    }
+    return passes;
+}
+
 static std::vector<PlanPass> plan(int n, const svb_op *ops, int nops, bool strict) {
+    if (!strict && planner_kind() == 3) return plan_beam(n, ops, nops);
     if (!strict && planner_kind() == 2) return plan_lookahead(n, ops, nops);
     std::vector<PlanPass> passes;
     const uint64_t low = (uint64_t(1) << flow_bits()) - 1;
