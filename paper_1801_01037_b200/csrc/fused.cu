@@ -1116,7 +1116,8 @@ static int fused_grid(int64_t ntiles) {
 
 static bool fuse_enabled(int n, unsigned flags) { return (flags & SVB_RUN_FUSE) && n >= FM + 2; }
 
-int jit_compile_only(const std::vector<FPass> &passes, bool fma, std::string &err);
+int jit_compile_only(const std::vector<FPass> &passes, int variant, std::string &err);
+int jit_variant(bool fma);
 
 // host-only: plan, lower and NVRTC-compile every fused pass (no device work)
 int jit_check(int n, const svb_op *ops, int nops, unsigned flags) {
@@ -1126,7 +1127,7 @@ int jit_check(int n, const svb_op *ops, int nops, unsigned flags) {
     for (const PlanPass &pp : plan(n, ops, nops, strict))
         if (pp.ops.size() > 1 && build_pass(n, ops, pp, P, strict, reg_perm(flags))) passes.push_back(P);
     std::string err;
-    int r = jit_compile_only(passes, (flags & SVB_RUN_FMA) && !strict, err);
+    int r = jit_compile_only(passes, jit_variant((flags & SVB_RUN_FMA) && !strict), err);
     if (r < 0) set_error("jit compile failed: %.400s", err.c_str());
     return r;
 }
@@ -1168,11 +1169,12 @@ struct CompiledPlan {
     std::vector<FPass> passes;
     // runtime-specialised kernels per pass (jit.cu), built on first JIT use
     mutable std::mutex jit_mu;
-    mutable int jit_state[2] = {0, 0};  // per FMA mode: 0 untried, 1 built, -1 failed
-    mutable std::vector<void *> jit_fns[2];
+    // per variant (exact / FMA / FMA + factors): 0 untried, 1 built, -1 failed
+    mutable int jit_state[3] = {0, 0, 0};
+    mutable std::vector<void *> jit_fns[3];
 };
 
-bool jit_build(const std::vector<FPass> &passes, bool fma, std::vector<void *> &fns);
+bool jit_build(const std::vector<FPass> &passes, int variant, std::vector<void *> &fns);
 bool jit_launch(void *fn, const FPass &P, double2 *a, int64_t ntiles, cudaStream_t s);
 
 static uint64_t fnv1a(const void *p, size_t len, uint64_t h) {
@@ -1251,9 +1253,10 @@ int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsi
     const std::vector<void *> *jit_fns = nullptr;
     if (jit) {
         std::lock_guard<std::mutex> lk(cp->jit_mu);
-        int &state = cp->jit_state[fma];
-        if (state == 0) state = jit_build(cp->passes, fma, cp->jit_fns[fma]) ? 1 : -1;
-        if (state == 1) jit_fns = &cp->jit_fns[fma];
+        const int variant = jit_variant(fma);
+        int &state = cp->jit_state[variant];
+        if (state == 0) state = jit_build(cp->passes, variant, cp->jit_fns[variant]) ? 1 : -1;
+        if (state == 1) jit_fns = &cp->jit_fns[variant];
     }
     for (const PlanStep &st : cp->steps) {
         if (st.op >= 0) {

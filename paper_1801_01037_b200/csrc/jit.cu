@@ -17,6 +17,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -403,6 +404,175 @@ void emit_gate_fold(Out &o, const FGate &g, int *code) {
     if (thread_ctl) o("}\n");
 }
 
+// ---------------------------------------------------------------------------
+// Factor extraction ("fast" FMA mode, SVB_JIT_FACTOR, default on).  An
+// uncontrolled one-qubit gate multiplies EVERY amplitude of the state, so a
+// scalar can be pulled out of it: U = a V with one entry of V equal to 1
+// (H = s [[1,1],[1,-1]], Ry = c [[1,-t],[t,1]], Rx = c [[1,-it],[-it,1]],
+// Rz = e^{-i th/2} diag(1, e^{i th})).  The pass applies V -- one FMA or add
+// per output part instead of a multiply and an FMA -- and the generator
+// multiplies a into a global factor F that the state carries: stored =
+// true / F.  F is applied (one complex multiply per amplitude) at the end of
+// the last fused pass of the circuit, or earlier when |F| leaves
+// [2^-200, 2^200].  Everything else the state meets in between (single-gate
+// kernels, controlled gates) is linear, so it commutes with the scalar.
+// Rounding differs from the reference at the 1e-16 level (within the FMA
+// mode's 1e-12 tolerance); exact and strict modes never extract.
+
+bool jit_factor_on() {
+    const char *e = getenv("SVB_JIT_FACTOR");
+    return e ? atoi(e) != 0 : true;
+}
+
+double2 cmulh(double2 a, double2 b) { return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+double2 cdivh(double2 a, double2 b) {
+    if (b.y == 0.0) return make_double2(a.x / b.x, a.y / b.x);
+    const double d = b.x * b.x + b.y * b.y;
+    return make_double2((a.x * b.x + a.y * b.y) / d, (a.y * b.x - a.x * b.y) / d);
+}
+double cabsh(double2 a) { return std::hypot(a.x, a.y); }
+
+struct FTerm {
+    double k;
+    const char *var;
+    int comp;  // logical component of var
+    int code;  // pending unit factor of var's register
+};
+
+// sum of k * var.comp with zero terms dropped and +-1 terms added plainly
+std::string fast_sum(const std::vector<FTerm> &ts) {
+    std::vector<std::pair<double, std::string>> unit, other;
+    for (const FTerm &t : ts) {
+        if (t.k == 0.0) continue;
+        double k = t.k;
+        const char *m = phys(t.code, t.comp, k);
+        std::string v = std::string(t.var) + "." + m;
+        if (k == 1.0 || k == -1.0)
+            unit.push_back({k, v});
+        else
+            other.push_back({k, v});
+    }
+    std::string e;
+    if (!unit.empty()) {
+        e = (unit[0].first < 0 ? "-" : "") + unit[0].second;
+        for (size_t i = 1; i < unit.size(); ++i)
+            e = "__dadd_rn(" + e + ", " + (unit[i].first < 0 ? "-" : "") + unit[i].second + ")";
+    }
+    for (size_t i = 0; i < other.size(); ++i) {
+        if (e.empty())
+            e = "__dmul_rn(" + lit(other[i].first) + ", " + other[i].second + ")";
+        else
+            e = "__fma_rn(" + lit(other[i].first) + ", " + other[i].second + ", " + e + ")";
+    }
+    return e.empty() ? std::string("0.0") : e;
+}
+
+// DP instructions fast_sum needs for one output part with the given weights
+int part_cost(std::initializer_list<double> ks) {
+    int n = 0, u = 0;
+    for (double k : ks)
+        if (k != 0.0) {
+            ++n;
+            u += (k == 1.0 || k == -1.0);
+        }
+    return n == 0 ? 0 : (u ? n - 1 : n);
+}
+
+// a L + b H, both parts
+std::string lin2(double2 a, int cL, double2 b, int cH) {
+    return "mk(" +
+           fast_sum({{a.x, "L", 0, cL}, {-a.y, "L", 1, cL}, {b.x, "H", 0, cH}, {-b.y, "H", 1, cH}}) + ", " +
+           fast_sum({{a.x, "L", 1, cL}, {a.y, "L", 0, cL}, {b.x, "H", 1, cH}, {b.y, "H", 0, cH}}) + ")";
+}
+int lin2_cost(double2 a, double2 b) {
+    return part_cost({a.x, -a.y, b.x, -b.y}) + part_cost({a.x, a.y, b.x, b.y});
+}
+
+// choose the scalar to pull out of a 2x2 (all four entries as candidates,
+// plus none); only well-conditioned ones (|a| >= 0.7 max |entry|)
+double2 pick_factor(const double2 *m, bool diag) {
+    double mx = 0;
+    for (int i = 0; i < 4; ++i) mx = std::max(mx, cabsh(m[i]));
+    double2 best = make_double2(1.0, 0.0);
+    auto cost_of = [&](double2 a) {
+        double2 v[4];
+        for (int i = 0; i < 4; ++i) v[i] = cdivh(m[i], a);
+        if (diag) return lin2_cost(v[0], make_double2(0, 0)) + lin2_cost(make_double2(0, 0), v[3]);
+        return lin2_cost(v[0], v[1]) + lin2_cost(v[2], v[3]);
+    };
+    int best_cost = cost_of(best);
+    for (int i = 0; i < 4; ++i) {
+        if (cabsh(m[i]) < 0.7 * mx || cabsh(m[i]) == 0.0) continue;
+        const int c = cost_of(m[i]);
+        if (c < best_cost) {
+            best_cost = c;
+            best = m[i];
+        }
+    }
+    return best;
+}
+
+void emit_gate_fast(Out &o, const FGate &g, int *code, double2 &F) {
+    const int op = g.op;
+    const bool uncontrolled = g.cl < 0 && !(op & 1);
+    if (!uncontrolled) {  // a controlled gate scales only part of the state
+        emit_gate_fold(o, g, code);
+        return;
+    }
+    if (op < FOP_DIAG) {
+        const int s = (op >> 1) % FSLOTS;
+        const int u12 = unit_code(g.m[1]), u21 = unit_code(g.m[2]);
+        if (g.m[0].x == 0.0 && g.m[0].y == 0.0 && g.m[3].x == 0.0 && g.m[3].y == 0.0 && u12 >= 0 && u21 >= 0) {
+            emit_gate_fold(o, g, code);  // a pure rename already
+            return;
+        }
+        const double2 a = pick_factor(g.m, false);
+        double2 v[4];
+        for (int i = 0; i < 4; ++i) v[i] = cdivh(g.m[i], a);
+        F = cmulh(F, a);
+        for (int i = 0; i < FREGS; ++i) {
+            if (i & (1 << s)) continue;
+            const int j = i | (1 << s);
+            o("{ const d2 L = v[%d], H = v[%d];\nv[%d] = %s;\nv[%d] = %s; }\n", i, j, i,
+              lin2(v[0], code[i], v[1], code[j]).c_str(), j, lin2(v[2], code[i], v[3], code[j]).c_str());
+            code[i] = code[j] = 0;
+        }
+        return;
+    }
+    const int c = op - FOP_DIAG;
+    const int tpos = (c >> 1) % (FSLOTS + 1);
+    const double2 a = pick_factor(g.m, true);
+    const double2 d0 = cdivh(g.m[0], a), d1 = cdivh(g.m[3], a);
+    F = cmulh(F, a);
+    auto mul = [&](int i, double2 d, bool branch) {
+        const int u = unit_code(d);
+        if (u >= 0 && !branch) {
+            code[i] = (code[i] + u) & 3;
+            return;
+        }
+        o("{ const d2 X = v[%d]; v[%d] = mk(%s, %s); }\n", i, i,
+          fast_sum({{d.x, "X", 0, code[i]}, {-d.y, "X", 1, code[i]}}).c_str(),
+          fast_sum({{d.x, "X", 1, code[i]}, {d.y, "X", 0, code[i]}}).c_str());
+        code[i] = 0;
+    };
+    if (tpos == FSLOTS) {  // target on a thread bit: the factor depends on the thread
+        const bool one0 = unit_code(d0) == 0, one1 = unit_code(d1) == 0;
+        for (int i = 0; i < FREGS; ++i) materialize(o, code, i);
+        if (!one1) {
+            o("if ((tid >> %d) & 1) {\n", g.tl);
+            for (int i = 0; i < FREGS; ++i) mul(i, d1, true);
+            o("}\n");
+        }
+        if (!one0) {
+            o("if (!((tid >> %d) & 1)) {\n", g.tl);
+            for (int i = 0; i < FREGS; ++i) mul(i, d0, true);
+            o("}\n");
+        }
+        return;
+    }
+    for (int i = 0; i < FREGS; ++i) mul(i, ((i >> tpos) & 1) ? d1 : d0, false);
+}
+
 }  // namespace
 
 // Tile pipelining modes of the generated kernel:
@@ -450,7 +620,10 @@ size_t jit_dyn_smem(const FPass &P) {
 // the tile loop and kept live (or spilled) across the gate arithmetic.
 const char *kOpaqueTid = "unsigned tg = tid; asm volatile(\"\" : \"+r\"(tg));\n";
 
-std::string jit_source(const FPass &P, bool fma) {
+// variant: 0 exact, 1 FMA, 2 FMA + factor extraction (F: the global factor
+// carried in and out; last: the circuit's last fused pass, which applies F)
+std::string jit_source(const FPass &P, int variant, double2 &F, bool last) {
+    const bool fma = variant >= 1, fast = variant == 2;
     const int mode = jit_pass_mode(P);
     Out o;
     o("#define SVB_FMA %d\n", fma ? 1 : 0);
@@ -519,7 +692,20 @@ std::string jit_source(const FPass &P, bool fma) {
             // every thread has its registers: refill the buffer with the next tile
             o("__syncthreads();\n{ const i64 nx = tix + gridDim.x; if (nx < ntiles) fill(dsm, tbase(nx)); }\n");
         }
-        if (fma) {
+        if (fast) {
+            int code[FREGS] = {0};
+            for (int q = G.first; q < G.first + G.count; ++q) emit_gate_fast(o, P.gates[q], code, F);
+            const double mag = cabsh(F);
+            if (gi == P.ngroups - 1 && (last || mag < 0x1p-200 || mag > 0x1p200) &&
+                !(F.x == 1.0 && F.y == 0.0)) {
+                for (int i = 0; i < FREGS; ++i) {  // stored * F = true amplitude
+                    o("{ const d2 X = v[%d]; v[%d] = %s; }\n", i, i, cm_fold(F, code[i]).c_str());
+                    code[i] = 0;
+                }
+                F = make_double2(1.0, 0.0);
+            }
+            for (int i = 0; i < FREGS; ++i) materialize(o, code, i);
+        } else if (fma) {
             int code[FREGS] = {0};
             for (int q = G.first; q < G.first + G.count; ++q) emit_gate_fold(o, P.gates[q], code);
             for (int i = 0; i < FREGS; ++i) materialize(o, code, i);
@@ -653,15 +839,18 @@ static bool set_dyn_smem(cudaKernel_t fn, size_t bytes) {
 
 // Compile (or fetch) one kernel per pass.  Returns false and leaves
 // `fns` empty on any failure (the caller falls back to k_fused).
-bool jit_build(const std::vector<FPass> &passes, bool fma, std::vector<void *> &fns) {
+int jit_variant(bool fma) { return fma ? (jit_factor_on() ? 2 : 1) : 0; }
+
+bool jit_build(const std::vector<FPass> &passes, int variant, std::vector<void *> &fns) {
     fns.assign(passes.size(), nullptr);
     std::vector<std::string> srcs(passes.size());
     std::vector<uint64_t> keys(passes.size());
     std::vector<size_t> todo;
+    double2 F = make_double2(1.0, 0.0);
     {
         std::lock_guard<std::mutex> lk(g_jit_mu);
         for (size_t i = 0; i < passes.size(); ++i) {
-            srcs[i] = jit_source(passes[i], fma);
+            srcs[i] = jit_source(passes[i], variant, F, i + 1 == passes.size());
             keys[i] = hash_str(srcs[i]);
             auto it = g_jit_cache.find(keys[i]);
             if (it != g_jit_cache.end())
@@ -713,12 +902,13 @@ bool jit_build(const std::vector<FPass> &passes, bool fma, std::vector<void *> &
 }
 
 // Host-only check: generate and NVRTC-compile every pass (no device needed).
-int jit_compile_only(const std::vector<FPass> &passes, bool fma, std::string &err) {
+int jit_compile_only(const std::vector<FPass> &passes, int variant, std::string &err) {
     const char *dump = getenv("SVB_JIT_DUMP");  // directory: write pass sources and cubins
     int k = 0;
+    double2 F = make_double2(1.0, 0.0);
     for (const FPass &P : passes) {
         std::vector<char> cubin;
-        std::string src = jit_source(P, fma);
+        std::string src = jit_source(P, variant, F, k + 1 == (int)passes.size());
         if (!nvrtc_compile(src, cubin, err)) return -1;
         if (dump) {
             std::string base = std::string(dump) + "/pass" + std::to_string(k);

@@ -148,13 +148,37 @@ def test_fused_fma_within_tolerance(cuda_ok, n):
         assert np.max(np.abs(st.to_host().amps - want)) <= TOL
 
 
+def test_bench_path_deep_circuit_vs_oracle(cuda_ok):
+    # the bench's default path (fused + FMA + JIT: in-register perms, unit
+    # folding, scalar extraction with the global factor applied at the end)
+    # on the full configs[1] depth -- 200 layers, 7800 ops -- at n = 20, where
+    # the oracle finishes in seconds; also the same circuit in two halves
+    # (each run_ops applies its own factor)
+    n = 20
+    circ = w.random_layer_circuit(n, 200)
+    rng = np.random.default_rng(77)
+    a = w.random_state_array(rng, n)
+    want = oracle.run_ops(a.copy(), w.oracle_ops(circ), workers=16)
+    got = device.simulate(circ, a.copy(), fma=True, jit=True)
+    err = np.max(np.abs(got - want))
+    assert err <= TOL, err
+    st = device.DeviceState.from_host(a)
+    half = len(circ.ops) // 2
+    device.run_ops(st, circ.ops[:half], fma=True, jit=True)
+    device.run_ops(st, circ.ops[half:], fma=True, jit=True)
+    assert np.max(np.abs(st.to_host().amps - want)) <= TOL
+    assert abs(device.norm2(st) - 1.0) < 1e-12
+
+
 @pytest.mark.parametrize("n", [14, 19])
 def test_jit_passes_bit_identical_to_interpreter(cuda_ok, n, monkeypatch):
     # SVB_RUN_JIT compiles each fused pass to straight-line code; on the same
     # plan it must give exactly the interpreter's bits (exact and FMA
     # arithmetic, perms, controls).  JIT plans run X / CNOT in registers by
-    # default; SVB_FUSE_REGPERM=1 gives the interpreter that same plan.
+    # default; SVB_FUSE_REGPERM=1 gives the interpreter that same plan, and
+    # SVB_JIT_FACTOR=0 turns off the (rounding-level) scalar extraction.
     monkeypatch.setenv("SVB_FUSE_REGPERM", "1")
+    monkeypatch.setenv("SVB_JIT_FACTOR", "0")
     rng = np.random.default_rng(600 + n)
     x = standard_gate("x")
     pool = all_gates(rng) + [x, x, Gate2x2(1, 0, 0, -1j)]
@@ -178,12 +202,14 @@ def test_jit_passes_bit_identical_to_interpreter(cuda_ok, n, monkeypatch):
         # default plans (JIT: in-register perms; interpreter: deferred) agree
         # to rounding, and strict order stays bit-exact through the JIT
         monkeypatch.delenv("SVB_FUSE_REGPERM")
+        monkeypatch.delenv("SVB_JIT_FACTOR")
         got = device.simulate(circ, a.copy(), fma=True, jit=True)
         assert np.max(np.abs(got - want)) <= TOL
         got = device.simulate(circ, a.copy(), strict_order=True, jit=True)
         ref = device.simulate(circ, a.copy(), strict_order=True)
         assert np.array_equal(got, ref)
         monkeypatch.setenv("SVB_FUSE_REGPERM", "1")
+        monkeypatch.setenv("SVB_JIT_FACTOR", "0")
 
 
 @pytest.mark.parametrize("n", [14, 17])
