@@ -766,26 +766,32 @@ static void thread_map(const int *slots, int8_t *tmap, const int16_t *qcol = nul
     // bank vectors independent for the accesses that go through shared
     // memory, otherwise each STS.128 / LDS.128 takes 2-4x the wavefronts.
     auto bank = [](int col) { return (col ^ (col >> 3) ^ (col >> 6) ^ (col >> 9)) & 7; };
-    auto rank3 = [&](const int16_t *cols, int a, int b, int c) {
-        const int x = bank(cols[a]), y = bank(cols[b]), z = bank(cols[c]);
-        if (!x || !y || !z || x == y || x == z || y == z) return false;
-        return (x ^ y ^ z) != 0;
+    // wavefronts of one 8-lane phase whose lanes vary bits a, b, c through cols
+    auto ways = [&](const int16_t *cols, int a, int b, int c) {
+        int seen[8] = {0}, w = 0;
+        for (int l = 0; l < 8; ++l) {
+            int x = ((l & 1) ? bank(cols[a]) : 0) ^ ((l & 2) ? bank(cols[b]) : 0) ^ ((l & 4) ? bank(cols[c]) : 0);
+            w = std::max(w, ++seen[x]);
+        }
+        return w;
     };
-    auto ok = [&](int a, int b, int c) {
-        return (!need_ld || rank3(qcol, a, b, c)) && (!need_st || rank3(mcol, a, b, c));
+    auto cost = [&](int a, int b, int c) {
+        return (need_ld ? ways(qcol, a, b, c) : 1) + (need_st ? ways(mcol, a, b, c) : 1);
     };
     // (a first / last group on local bits 0-2 keeps them: direct HBM access wins)
     const bool direct_pick = order.size() == 3 && order[0] == 0 && order[1] == 1 && order[2] == 2;
-    if (qcol && !(keep012 && direct_pick) && (order.size() < 3 || !ok(order[0], order[1], order[2]))) {
+    if (qcol && !(keep012 && direct_pick) && (order.size() < 3 || cost(order[0], order[1], order[2]) > 2)) {
         const int nf = (int)free_bits.size();
-        bool found = false;
-        for (int i = 0; i < nf && !found; ++i)
-            for (int j = i + 1; j < nf && !found; ++j)
-                for (int k = j + 1; k < nf && !found; ++k)
-                    if (ok(free_bits[i], free_bits[j], free_bits[k])) {
+        int best = order.size() == 3 ? cost(order[0], order[1], order[2]) : 1 << 20;
+        for (int i = 0; i < nf && best > 2; ++i)
+            for (int j = i + 1; j < nf && best > 2; ++j)
+                for (int k = j + 1; k < nf && best > 2; ++k) {
+                    const int c = cost(free_bits[i], free_bits[j], free_bits[k]);
+                    if (c < best) {
+                        best = c;
                         order = {free_bits[i], free_bits[j], free_bits[k]};
-                        found = true;
                     }
+                }
     }
     for (int b : free_bits)
         if (std::find(order.begin(), order.end(), b) == order.end()) order.push_back(b);
@@ -986,7 +992,15 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
             if (gp.mcol[j] != (1 << j) || gp.qcol[j] != (1 << j)) G.perm = 1;
         }
         G.qb = (int16_t)gp.qb;
-        thread_map(slots, G.tmap, G.qcol, G.mcol, gi > 0, gi < P.ngroups - 1, gi == 0 || gi == P.ngroups - 1);
+        // can this group reach HBM directly (see direct_first / direct_last
+        // below)?  Then its HBM side needs no bank-friendly lanes, and its
+        // lanes 0-2 must stay on local bits 0-2.
+        bool slots_high = !no_direct();
+        for (int k = 0; k < FSLOTS; ++k) slots_high &= slots[k] >= 3;
+        auto low3 = [](const int16_t *col) { return (col[0] >> 3) == 0 && (col[1] >> 3) == 0 && (col[2] >> 3) == 0; };
+        const bool can_df = gi == 0 && slots_high && low3(G.qcol);
+        const bool can_dl = gi == P.ngroups - 1 && slots_high && low3(G.mcol);
+        thread_map(slots, G.tmap, G.qcol, G.mcol, !can_df, !can_dl, can_df || can_dl);
         for (int j = 0; j < FTBITS; ++j) {
             G.ld_t[j] = (uint16_t)(16 * swz(gp.qcol[G.tmap[j]]));
             G.st_t[j] = (uint16_t)(16 * swz(gp.mcol[G.tmap[j]]));
@@ -1099,6 +1113,26 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
     P.gs_b = gidx(GL.mb);
     for (int j = 0; j < FTBITS; ++j) P.gs_t[j] = gidx(GL.mcol[GL.tmap[j]]);
     for (int k = 0; k < FSLOTS; ++k) P.gs_s[k] = gidx(GL.mcol[GL.pos[k]]);
+    if (getenv("SVB_PLAN_DEBUG") && atoi(getenv("SVB_PLAN_DEBUG")) >= 3) {
+        // shared-memory wavefronts per LDS/STS.128 phase of 8 lanes (1 = conflict-free)
+        auto ways = [](const uint16_t *t) {
+            int seen[8] = {0}, w = 0;
+            for (int l = 0; l < 8; ++l) {
+                unsigned a = 0;
+                for (int j = 0; j < 3; ++j)
+                    if ((l >> j) & 1) a ^= t[j];
+                w = std::max(w, ++seen[(a >> 4) & 7]);
+            }
+            return w;
+        };
+        fprintf(stderr, "  banks: df %d dl %d |", P.direct_first, P.direct_last);
+        for (int gi = 0; gi < P.ngroups; ++gi) {
+            const FGroup &G = P.groups[gi];
+            const bool ld_smem = !(gi == 0 && P.direct_first), st_smem = !(gi == P.ngroups - 1 && P.direct_last);
+            fprintf(stderr, " g%d ld %d st %d", gi, ld_smem ? ways(G.ld_t) : 0, st_smem ? ways(G.st_t) : 0);
+        }
+        fprintf(stderr, "\n");
+    }
     return true;
 }
 
