@@ -257,7 +257,7 @@ def run_gpu_arm(args) -> None:
     nops = len(circuit.ops)
     ops_arr, _ = _lib.ops_array(circuit.ops)
     flags = _lib.run_flags(fuse=not args.no_fuse, fma=args.fma, jit=args.jit)
-    passes = device.plan_passes(n, circuit, fuse=not args.no_fuse)
+    passes = device.plan_passes(n, circuit, fuse=not args.no_fuse, jit=args.jit)
     st = device.DeviceState.zeros(n)
     stream = torch.cuda.current_stream()
     sp = device._stream_ptr()

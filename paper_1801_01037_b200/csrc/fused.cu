@@ -55,10 +55,10 @@ LaunchInfo launch_gate(double2 *a, int64_t n_amps, const Gate &g, int t, int c, 
 #include "fused_desc.h"
 namespace svb {
 
-// 16 B-granular XOR swizzle: bits 3-5, 6-8, 9-11 fold into bits 0-2, so local
+// 16 B-granular XOR swizzle: bits 3-5, 6-8, 9-11, 12 fold into bits 0-2, so local
 // bit j moves the 16 B chunk inside a 128 B line along axis (j mod 3).  It is
 // linear over XOR, so swz(l0 | d) = swz(l0) ^ swz(d) for disjoint bits.
-__host__ __device__ __forceinline__ int fold3(int x) { return (x ^ (x >> 3) ^ (x >> 6)) & 7; }
+__host__ __device__ __forceinline__ int fold3(int x) { return (x ^ (x >> 3) ^ (x >> 6) ^ (x >> 9)) & 7; }
 __host__ __device__ __forceinline__ int swz(int l) { return l ^ fold3(l >> 3); }
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
@@ -192,13 +192,21 @@ __device__ __forceinline__ void run_gate(double2 (&v)[FREGS], const FGate &fg, i
         // matrix class); uncontrolled ones get their specialised arm
 #define SVB_NDU(K, S) case ((K)*FSLOTS + (S)) * 2 + 0: nd_gate<K, S, 0, FMA>(v, fg); break;
 #define SVB_NDC(S) case ((FK_GENERAL)*FSLOTS + (S)) * 2 + 1: nd_gate<FK_GENERAL, S, 1, FMA>(v, fg); break;
-        SVB_NDU(FK_GENERAL, 0) SVB_NDU(FK_GENERAL, 1) SVB_NDU(FK_GENERAL, 2) SVB_NDU(FK_GENERAL, 3)
-        SVB_NDU(FK_REAL, 0) SVB_NDU(FK_REAL, 1) SVB_NDU(FK_REAL, 2) SVB_NDU(FK_REAL, 3)
-        SVB_NDU(FK_ANTI, 0) SVB_NDU(FK_ANTI, 1) SVB_NDU(FK_ANTI, 2) SVB_NDU(FK_ANTI, 3)
-        SVB_NDU(FK_RX, 0) SVB_NDU(FK_RX, 1) SVB_NDU(FK_RX, 2) SVB_NDU(FK_RX, 3)
-        SVB_NDC(0) SVB_NDC(1) SVB_NDC(2) SVB_NDC(3)
+#if SVB_FSLOTS == 5
+#define SVB_SLOTS(M, K) M(K, 0) M(K, 1) M(K, 2) M(K, 3) M(K, 4)
+#elif SVB_FSLOTS == 4
+#define SVB_SLOTS(M, K) M(K, 0) M(K, 1) M(K, 2) M(K, 3)
+#else
+#define SVB_SLOTS(M, K) M(K, 0) M(K, 1) M(K, 2)
+#endif
+#define SVB_NDC2(K, S) SVB_NDC(S)
+        SVB_SLOTS(SVB_NDU, FK_GENERAL)
+        SVB_SLOTS(SVB_NDU, FK_REAL)
+        SVB_SLOTS(SVB_NDU, FK_ANTI)
+        SVB_SLOTS(SVB_NDU, FK_RX)
+        SVB_SLOTS(SVB_NDC2, 0)
 #define SVB_DGU(V, T) case FOP_DIAG + ((V) * (FSLOTS + 1) + (T)) * 2 + 0: diag_gate<V, T, 0, FMA>(v, fg, l0); break;
-        SVB_DGU(FD_Z, 0) SVB_DGU(FD_Z, 1) SVB_DGU(FD_Z, 2) SVB_DGU(FD_Z, 3) SVB_DGU(FD_Z, 4)
+        SVB_SLOTS(SVB_DGU, FD_Z) SVB_DGU(FD_Z, FSLOTS)
         SVB_DG(FD_GENERAL)
         SVB_DG(FD_D1)
         default: break;
@@ -479,7 +487,7 @@ static int planner_kind() {  // 1 greedy, 2 lookahead, 3 two-pass lookahead (def
 // qubits admit the most gates per new qubit; after every growth, absorb every
 // ready gate whose qubits are already in S.  Gate order per qubit is kept by
 // the same blocked-qubit scan as the greedy planner.
-static std::vector<PlanPass> plan_lookahead(int n, const svb_op *ops, int nops) {
+static std::vector<PlanPass> plan_lookahead(int n, const svb_op *ops, int nops, int fm) {
     std::vector<PlanPass> passes;
     const uint64_t low = (uint64_t(1) << flow_bits()) - 1;
     std::vector<char> done(nops, 0);
@@ -519,7 +527,7 @@ static std::vector<PlanPass> plan_lookahead(int n, const svb_op *ops, int nops) 
                     block_add(blocked, cls[i]);
                 }
             }
-            if (popc(p.S) >= FM || (int)p.ops.size() >= FMAXG) break;
+            if (popc(p.S) >= fm || (int)p.ops.size() >= FMAXG) break;
             // candidate growths: ready gates needing new qubits that still fit
             uint64_t best = 0;
             double best_score = -1.0;
@@ -529,7 +537,7 @@ static std::vector<PlanPass> plan_lookahead(int n, const svb_op *ops, int nops) 
                 if (done[i]) continue;
                 uint64_t m = op_mask(ops[i]);
                 uint64_t add = m & ~p.S;
-                if (hoistable(cls[i], blocked) && add && popc(p.S | m) <= FM) {
+                if (hoistable(cls[i], blocked) && add && popc(p.S | m) <= fm) {
                     ++cands;
                     int gain = absorb_count(p.S | m, FMAXG);
                     double score = double(gain) / popc(add);
@@ -550,7 +558,7 @@ static std::vector<PlanPass> plan_lookahead(int n, const svb_op *ops, int nops) 
             done[first] = 1;
             while (first < nops && done[first]) ++first;
         }
-        for (int q = 0; q < n && popc(p.S) < FM; ++q) p.S |= uint64_t(1) << q;
+        for (int q = 0; q < n && popc(p.S) < fm; ++q) p.S |= uint64_t(1) << q;
         passes.push_back(std::move(p));
     }
     return passes;
@@ -561,7 +569,7 @@ static std::vector<PlanPass> plan_lookahead(int n, const svb_op *ops, int nops) 
 // that pass greedily, then plan the following pass greedily too, and keep the
 // first growth that retires the most ops over both passes.  Host-only and
 // run once per circuit (compiled plans are cached).
-static std::vector<PlanPass> plan_beam(int n, const svb_op *ops, int nops) {
+static std::vector<PlanPass> plan_beam(int n, const svb_op *ops, int nops, int fm) {
     std::vector<PlanPass> passes;
     const uint64_t low = (uint64_t(1) << flow_bits()) - 1;
     std::vector<Blocking> cls(nops);
@@ -594,7 +602,7 @@ static std::vector<PlanPass> plan_beam(int n, const svb_op *ops, int nops) {
             if (done[i]) continue;
             uint64_t m = op_mask(ops[i]);
             uint64_t add = m & ~p.S;
-            if (hoistable(cls[i], blocked) && add && popc(p.S | m) <= FM &&
+            if (hoistable(cls[i], blocked) && add && popc(p.S | m) <= fm &&
                 std::find(out.begin(), out.end(), m) == out.end())
                 out.push_back(m);
             block_add(blocked, cls[i]);
@@ -608,7 +616,7 @@ static std::vector<PlanPass> plan_beam(int n, const svb_op *ops, int nops) {
         bool forced_used = forced == 0;
         for (;;) {
             absorb(done, first, p, true);
-            if (popc(p.S) >= FM || (int)p.ops.size() >= FMAXG) break;
+            if (popc(p.S) >= fm || (int)p.ops.size() >= FMAXG) break;
             uint64_t best = 0;
             if (!forced_used) {
                 best = forced;
@@ -671,15 +679,15 @@ static std::vector<PlanPass> plan_beam(int n, const svb_op *ops, int nops) {
             done[first] = 1;
         }
         first = advance(done, first);
-        for (int q = 0; q < n && popc(p.S) < FM; ++q) p.S |= uint64_t(1) << q;
+        for (int q = 0; q < n && popc(p.S) < fm; ++q) p.S |= uint64_t(1) << q;
         passes.push_back(std::move(p));
     }
     return passes;
 }
 
-static std::vector<PlanPass> plan(int n, const svb_op *ops, int nops, bool strict) {
-    if (!strict && planner_kind() == 3) return plan_beam(n, ops, nops);
-    if (!strict && planner_kind() == 2) return plan_lookahead(n, ops, nops);
+static std::vector<PlanPass> plan(int n, const svb_op *ops, int nops, bool strict, int fm) {
+    if (!strict && planner_kind() == 3) return plan_beam(n, ops, nops, fm);
+    if (!strict && planner_kind() == 2) return plan_lookahead(n, ops, nops, fm);
     std::vector<PlanPass> passes;
     const uint64_t low = (uint64_t(1) << flow_bits()) - 1;
     const uint64_t all = n >= 64 ? ~uint64_t(0) : ((uint64_t(1) << n) - 1);
@@ -693,7 +701,7 @@ static std::vector<PlanPass> plan(int n, const svb_op *ops, int nops, bool stric
         for (int i = first; i < nops && i < first + window; ++i) {
             if (done[i]) continue;
             uint64_t m = op_mask(ops[i]);
-            bool fits = (m & blocked) == 0 && popc(p.S | m) <= FM && (int)p.ops.size() < FMAXG;
+            bool fits = (m & blocked) == 0 && popc(p.S | m) <= fm && (int)p.ops.size() < FMAXG;
             if (fits) {
                 p.S |= m;
                 p.ops.push_back(i);
@@ -701,7 +709,7 @@ static std::vector<PlanPass> plan(int n, const svb_op *ops, int nops, bool stric
             } else {
                 if (strict) break;
                 blocked |= m;
-                if ((blocked | p.S) == all && popc(p.S) == FM) {
+                if ((blocked | p.S) == all && popc(p.S) == fm) {
                     // nothing outside S can join and every S qubit is blocked or
                     // free; keep scanning only while S-internal ops remain possible
                     if ((blocked & p.S) == p.S) break;
@@ -709,7 +717,7 @@ static std::vector<PlanPass> plan(int n, const svb_op *ops, int nops, bool stric
             }
         }
         while (first < nops && done[first]) ++first;
-        for (int q = 0; q < n && popc(p.S) < FM; ++q) p.S |= uint64_t(1) << q;
+        for (int q = 0; q < n && popc(p.S) < fm; ++q) p.S |= uint64_t(1) << q;
         passes.push_back(std::move(p));
     }
     return passes;
@@ -741,13 +749,13 @@ struct GateMeta {
 // Thread-bit -> local-bit map for a group: the 3 lowest thread bits (which
 // vary across the 8 lanes of an LDS.128 phase) go to non-slot local bits
 // with distinct (bit mod 3) so the swizzle spreads them over 8 chunks.
-static void thread_map(const int *slots, int8_t *tmap, const int16_t *qcol = nullptr,
+static void thread_map(int fm, const int *slots, int8_t *tmap, const int16_t *qcol = nullptr,
                        const int16_t *mcol = nullptr, bool need_ld = false, bool need_st = false,
                        bool keep012 = false) {
-    bool is_slot[FM] = {};
+    bool is_slot[FMMAX] = {};
     for (int i = 0; i < FSLOTS; ++i) is_slot[slots[i]] = true;
     std::vector<int> free_bits;
-    for (int b = 0; b < FM; ++b)
+    for (int b = 0; b < fm; ++b)
         if (!is_slot[b]) free_bits.push_back(b);
     int pick[3] = {-1, -1, -1};
     for (int r = 0; r < 3; ++r)
@@ -765,7 +773,7 @@ static void thread_map(const int *slots, int8_t *tmap, const int16_t *qcol = nul
     // lanes of a phase address Q(l) / P(l) instead of l: keep the 3 lanes'
     // bank vectors independent for the accesses that go through shared
     // memory, otherwise each STS.128 / LDS.128 takes 2-4x the wavefronts.
-    auto bank = [](int col) { return (col ^ (col >> 3) ^ (col >> 6) ^ (col >> 9)) & 7; };
+    auto bank = [](int col) { return (col ^ (col >> 3) ^ (col >> 6) ^ (col >> 9) ^ (col >> 12)) & 7; };
     // wavefronts of one 8-lane phase whose lanes vary bits a, b, c through cols
     auto ways = [&](const int16_t *cols, int a, int b, int c) {
         int seen[8] = {0}, w = 0;
@@ -795,7 +803,7 @@ static void thread_map(const int *slots, int8_t *tmap, const int16_t *qcol = nul
     }
     for (int b : free_bits)
         if (std::find(order.begin(), order.end(), b) == order.end()) order.push_back(b);
-    for (int j = 0; j < FTBITS; ++j) tmap[j] = (int8_t)order[j];
+    for (int j = 0; j < fm - FSLOTS; ++j) tmap[j] = (int8_t)order[j];
 }
 
 // In-register X / CNOT (see the group scan) pays off when passes are JIT
@@ -808,9 +816,12 @@ static bool reg_perm(unsigned flags) {
 }
 
 // Build the kernel descriptor for one pass; false if it does not fit.
-static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, bool strict, bool regperm) {
+static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, bool strict, bool regperm,
+                       int fm) {
     memset(&P, 0, sizeof(P));
     P.flow = flow_bits();
+    P.fm = fm;
+    const int tbits = fm - FSLOTS;
     int local_of[64];
     int nl = 0, nc = 0;
     for (int q = 0; q < n; ++q) {
@@ -850,16 +861,16 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
     struct GroupPlan {
         std::vector<int> gates;  // indices into meta, execution order (no perms)
         std::vector<int> slots;
-        int mcol[FM];            // post map P (store)
+        int mcol[FMMAX];         // post map P (store)
         int mb = 0;
         uint64_t permq = 0;
-        int qcol[FM];            // pre map Q (load): register l reads position Q(l)
+        int qcol[FMMAX];         // pre map Q (load): register l reads position Q(l)
         int qb = 0;
     };
     std::vector<GroupPlan> gps;
     auto new_group = [&]() {
         GroupPlan g;
-        for (int j = 0; j < FM; ++j) g.mcol[j] = g.qcol[j] = 1 << j;
+        for (int j = 0; j < fm; ++j) g.mcol[j] = g.qcol[j] = 1 << j;
         gps.push_back(g);
         return &gps.back();
     };
@@ -874,7 +885,7 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
         // compose C(x) = x ^ (x_c << t) (X: c = -1, always) after the current map
         auto C = [&](int x) { return (m.cl < 0 || ((x >> m.cl) & 1)) ? x ^ (1 << m.tl) : x; };
         auto Cl = [&](int x) { return (m.cl >= 0 && ((x >> m.cl) & 1)) ? x ^ (1 << m.tl) : x; };
-        for (int j = 0; j < FM; ++j) g.mcol[j] = Cl(g.mcol[j]);
+        for (int j = 0; j < fm; ++j) g.mcol[j] = Cl(g.mcol[j]);
         g.mb = C(g.mb);
         g.permq |= (uint64_t(1) << m.tl) | (m.cl >= 0 ? uint64_t(1) << m.cl : 0);
     };
@@ -974,7 +985,7 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
         int slots[FSLOTS];
         int ns = 0;
         for (int s : gp.slots) slots[ns++] = s;
-        for (int b = FM - 1; ns < FSLOTS && b >= 0; --b) {
+        for (int b = fm - 1; ns < FSLOTS && b >= 0; --b) {
             bool used = false;
             for (int i = 0; i < ns; ++i) used |= slots[i] == b;
             if (!used) slots[ns++] = b;
@@ -986,7 +997,7 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
         G.count = (int16_t)gp.gates.size();
         G.mb = (int16_t)gp.mb;
         G.perm = (int16_t)(gp.mb != 0 || gp.qb != 0);
-        for (int j = 0; j < FM; ++j) {
+        for (int j = 0; j < fm; ++j) {
             G.mcol[j] = (int16_t)gp.mcol[j];
             G.qcol[j] = (int16_t)gp.qcol[j];
             if (gp.mcol[j] != (1 << j) || gp.qcol[j] != (1 << j)) G.perm = 1;
@@ -1000,24 +1011,24 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
         auto low3 = [](const int16_t *col) { return (col[0] >> 3) == 0 && (col[1] >> 3) == 0 && (col[2] >> 3) == 0; };
         const bool can_df = gi == 0 && slots_high && low3(G.qcol);
         const bool can_dl = gi == P.ngroups - 1 && slots_high && low3(G.mcol);
-        thread_map(slots, G.tmap, G.qcol, G.mcol, !can_df, !can_dl, can_df || can_dl);
-        for (int j = 0; j < FTBITS; ++j) {
-            G.ld_t[j] = (uint16_t)(16 * swz(gp.qcol[G.tmap[j]]));
-            G.st_t[j] = (uint16_t)(16 * swz(gp.mcol[G.tmap[j]]));
+        thread_map(fm, slots, G.tmap, G.qcol, G.mcol, !can_df, !can_dl, can_df || can_dl);
+        for (int j = 0; j < tbits; ++j) {
+            G.ld_t[j] = (uint32_t)(16 * swz(gp.qcol[G.tmap[j]]));
+            G.st_t[j] = (uint32_t)(16 * swz(gp.mcol[G.tmap[j]]));
         }
         for (int k = 0; k < FSLOTS; ++k) {
-            G.ld_s[k] = (uint16_t)(16 * swz(gp.qcol[slots[k]]));
-            G.st_s[k] = (uint16_t)(16 * swz(gp.mcol[slots[k]]));
+            G.ld_s[k] = (uint32_t)(16 * swz(gp.qcol[slots[k]]));
+            G.st_s[k] = (uint32_t)(16 * swz(gp.mcol[slots[k]]));
         }
-        G.ld_b = (uint16_t)(16 * swz(gp.qb));
-        G.st_b = (uint16_t)(16 * swz(gp.mb));
+        G.ld_b = (uint32_t)(16 * swz(gp.qb));
+        G.st_b = (uint32_t)(16 * swz(gp.mb));
         auto slot_of = [&](int l) {
             for (int i = 0; i < FSLOTS; ++i)
                 if (slots[i] == l) return i;
             return -1;
         };
         auto tbit_of = [&](int l) {  // local bit -> thread-index bit
-            for (int j = 0; j < FTBITS; ++j)
+            for (int j = 0; j < tbits; ++j)
                 if (G.tmap[j] == l) return j;
             return -1;
         };
@@ -1081,12 +1092,12 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
     // direct HBM access for the first / last group when the coalescing
     // condition holds: no slot on local bits 0-2, thread bits 0-2 = local bits
     // 0-2, and (last group) a store map that leaves bits 0-2 alone
-    int glob_of[FM];
+    int glob_of[FMMAX];
     for (int q = 0, b = 0; q < n; ++q)
         if ((pp.S >> q) & 1) glob_of[b++] = q;
     auto gidx = [&](int l) {
         int64_t g = 0;
-        for (int b = 0; b < FM; ++b)
+        for (int b = 0; b < fm; ++b)
             if ((l >> b) & 1) g |= int64_t(1) << glob_of[b];
         return g;
     };
@@ -1106,16 +1117,16 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
     const FGroup &G0 = P.groups[0];
     P.direct_first = coalesced(G0) && low_fixed(G0.qcol) && !no_direct();
     P.gl_b = gidx(G0.qb);
-    for (int j = 0; j < FTBITS; ++j) P.gl_t[j] = gidx(G0.qcol[G0.tmap[j]]);
+    for (int j = 0; j < tbits; ++j) P.gl_t[j] = gidx(G0.qcol[G0.tmap[j]]);
     for (int k = 0; k < FSLOTS; ++k) P.gl_s[k] = gidx(G0.qcol[G0.pos[k]]);
     const FGroup &GL = P.groups[P.ngroups - 1];
     P.direct_last = coalesced(GL) && low_fixed(GL.mcol) && !no_direct();
     P.gs_b = gidx(GL.mb);
-    for (int j = 0; j < FTBITS; ++j) P.gs_t[j] = gidx(GL.mcol[GL.tmap[j]]);
+    for (int j = 0; j < tbits; ++j) P.gs_t[j] = gidx(GL.mcol[GL.tmap[j]]);
     for (int k = 0; k < FSLOTS; ++k) P.gs_s[k] = gidx(GL.mcol[GL.pos[k]]);
     if (getenv("SVB_PLAN_DEBUG") && atoi(getenv("SVB_PLAN_DEBUG")) >= 3) {
         // shared-memory wavefronts per LDS/STS.128 phase of 8 lanes (1 = conflict-free)
-        auto ways = [](const uint16_t *t) {
+        auto ways = [](const uint32_t *t) {
             int seen[8] = {0}, w = 0;
             for (int l = 0; l < 8; ++l) {
                 unsigned a = 0;
@@ -1152,14 +1163,29 @@ static bool fuse_enabled(int n, unsigned flags) { return (flags & SVB_RUN_FUSE) 
 
 int jit_compile_only(const std::vector<FPass> &passes, int variant, std::string &err);
 int jit_variant(bool fma);
+bool jit_available();
+
+// Tile qubits of a plan: the interpreter's FM, or -- for runtime-specialised
+// passes -- 12 while the state still has >= 2^12 tiles (every SM busy):
+// bigger tiles hold more qubits, so fewer HBM passes per circuit.  configs[1]
+// measured: fm 11 239 passes x 0.416 ms = 77.2k gate apps/s, fm 12 203 x
+// 0.467 ms = 81.0k, fm 13 174 x 0.574 ms = 77.0k (one 512-thread CTA per SM
+// hides latency worse).  SVB_JIT_FM overrides (11..FMMAX).
+static int plan_fm(int n, unsigned flags) {
+    if (!(flags & SVB_RUN_JIT) || !jit_available()) return FM;
+    const char *e = getenv("SVB_JIT_FM");
+    const int fm = e ? atoi(e) : std::min(12, n - 12);
+    return std::max(FM, std::min(FMMAX, fm));
+}
 
 // host-only: plan, lower and NVRTC-compile every fused pass (no device work)
 int jit_check(int n, const svb_op *ops, int nops, unsigned flags) {
     const bool strict = flags & SVB_RUN_STRICT_ORDER;
     std::vector<FPass> passes;
     FPass P;
-    for (const PlanPass &pp : plan(n, ops, nops, strict))
-        if (pp.ops.size() > 1 && build_pass(n, ops, pp, P, strict, reg_perm(flags))) passes.push_back(P);
+    const int fm = plan_fm(n, flags | SVB_RUN_JIT);
+    for (const PlanPass &pp : plan(n, ops, nops, strict, fm))
+        if (pp.ops.size() > 1 && build_pass(n, ops, pp, P, strict, reg_perm(flags), fm)) passes.push_back(P);
     std::string err;
     int r = jit_compile_only(passes, jit_variant((flags & SVB_RUN_FMA) && !strict), err);
     if (r < 0) set_error("jit compile failed: %.400s", err.c_str());
@@ -1170,12 +1196,13 @@ int plan_passes(int n, const svb_op *ops, int nops, unsigned flags, int *groups)
     if (groups) *groups = 0;
     if (!fuse_enabled(n, flags)) return nops;
     const bool strict = flags & SVB_RUN_STRICT_ORDER;
-    auto passes = plan(n, ops, nops, strict);
+    const int fm = plan_fm(n, flags);
+    auto passes = plan(n, ops, nops, strict, fm);
     if (groups) {
         FPass P;
         int df = 0, dl = 0, nf = 0;
         for (const PlanPass &pp : passes)
-            if (pp.ops.size() > 1 && build_pass(n, ops, pp, P, strict, reg_perm(flags))) {
+            if (pp.ops.size() > 1 && build_pass(n, ops, pp, P, strict, reg_perm(flags), fm)) {
                 *groups += P.ngroups;
                 df += P.direct_first;
                 dl += P.direct_last;
@@ -1196,7 +1223,7 @@ struct PlanStep {
     int op;  // >= 0: run ops[op] with the single-gate kernels; -1: next fused pass
 };
 struct CompiledPlan {
-    int n;
+    int n, fm;
     bool strict, regperm;
     std::vector<svb_op> ops;  // exact key
     std::vector<PlanStep> steps;
@@ -1218,18 +1245,20 @@ static uint64_t fnv1a(const void *p, size_t len, uint64_t h) {
 }
 
 static std::shared_ptr<const CompiledPlan> compiled_plan(int n, const svb_op *ops, int nops, bool strict,
-                                                         bool regperm) {
+                                                         bool regperm, int fm) {
     static std::mutex mu;
     static std::vector<std::pair<uint64_t, std::shared_ptr<const CompiledPlan>>> cache;  // MRU first
     uint64_t key = fnv1a(ops, sizeof(svb_op) * size_t(nops), 1469598103934665603ull);
     key = fnv1a(&n, sizeof n, key);
     key = fnv1a(&strict, sizeof strict, key);
     key = fnv1a(&regperm, sizeof regperm, key);
+    key = fnv1a(&fm, sizeof fm, key);
     {
         std::lock_guard<std::mutex> lk(mu);
         for (size_t i = 0; i < cache.size(); ++i) {
             const auto &c = cache[i].second;
-            if (cache[i].first == key && c->n == n && c->strict == strict && c->regperm == regperm && (int)c->ops.size() == nops &&
+            if (cache[i].first == key && c->n == n && c->fm == fm && c->strict == strict && c->regperm == regperm &&
+                (int)c->ops.size() == nops &&
                 std::memcmp(c->ops.data(), ops, sizeof(svb_op) * size_t(nops)) == 0) {
                 auto hit = cache[i];
                 cache.erase(cache.begin() + i);
@@ -1240,12 +1269,13 @@ static std::shared_ptr<const CompiledPlan> compiled_plan(int n, const svb_op *op
     }
     auto cp = std::make_shared<CompiledPlan>();
     cp->n = n;
+    cp->fm = fm;
     cp->strict = strict;
     cp->regperm = regperm;
     cp->ops.assign(ops, ops + nops);
     FPass P;
-    for (const PlanPass &pp : plan(n, ops, nops, strict)) {
-        if (pp.ops.size() > 1 && build_pass(n, ops, pp, P, strict, regperm)) {
+    for (const PlanPass &pp : plan(n, ops, nops, strict, fm)) {
+        if (pp.ops.size() > 1 && build_pass(n, ops, pp, P, strict, regperm, fm)) {
             cp->steps.push_back(PlanStep{-1});
             cp->passes.push_back(P);
         } else {
@@ -1280,10 +1310,9 @@ int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsi
     }
     const bool strict = flags & SVB_RUN_STRICT_ORDER;
     const bool fma = (flags & SVB_RUN_FMA) && !strict;
-    std::shared_ptr<const CompiledPlan> cp = compiled_plan(n, ops, nops, strict, reg_perm(flags));
-    const int64_t ntiles = n_amps >> FM;
+    std::shared_ptr<const CompiledPlan> cp = compiled_plan(n, ops, nops, strict, reg_perm(flags), plan_fm(n, flags));
     size_t next_pass = 0;
-    const bool jit = (flags & SVB_RUN_JIT) && !cp->passes.empty();
+    bool jit = (flags & SVB_RUN_JIT) && !cp->passes.empty();
     const std::vector<void *> *jit_fns = nullptr;
     if (jit) {
         std::lock_guard<std::mutex> lk(cp->jit_mu);
@@ -1292,13 +1321,18 @@ int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsi
         if (state == 0) state = jit_build(cp->passes, variant, cp->jit_fns[variant]) ? 1 : -1;
         if (state == 1) jit_fns = &cp->jit_fns[variant];
     }
+    if (!jit_fns && cp->fm != FM) {  // JIT unavailable: the interpreter runs FM tiles
+        cp = compiled_plan(n, ops, nops, strict, reg_perm(flags & ~SVB_RUN_JIT), FM);
+        jit = false;
+    }
     for (const PlanStep &st : cp->steps) {
         if (st.op >= 0) {
             single(ops[st.op]);
             continue;
         }
         const size_t pi = next_pass++;
-        const FPass &P = cp->passes[pi];  // ~17 KiB, a __grid_constant__ kernel parameter
+        const FPass &P = cp->passes[pi];  // ~27 KiB, a __grid_constant__ kernel parameter
+        const int64_t ntiles = n_amps >> P.fm;
         prof_begin(s);
         if (jit && jit_fns) {
             if (!jit_launch((*jit_fns)[pi], cp->passes[pi], a, ntiles, s)) {

@@ -18,6 +18,10 @@ constexpr int FSLOTS = SVB_FSLOTS;     // register bits per thread
 constexpr int FREGS = 1 << FSLOTS;     // 16 amplitudes per thread
 constexpr int FTHREADS = FTILE / FREGS;  // 128 threads
 constexpr int FTBITS = FM - FSLOTS;    // 7 thread bits
+// Tiles of runtime-specialised (JIT) passes may be larger than the
+// interpreter's: descriptors carry their own fm (11..FMMAX qubits)
+constexpr int FMMAX = 13;
+constexpr int FTBMAX = FMMAX - FSLOTS;  // thread bits at the largest tile
 constexpr int FMAXG = 192;             // gates per pass
 constexpr int FMAXGRP = 64;            // register groups per pass
 constexpr int FMAXROWS = FTILE / 8;    // rows when flow = 3
@@ -51,28 +55,29 @@ struct FGate {
 };
 struct FGroup {
     int8_t pos[FSLOTS];  // slot -> local bit
-    int8_t tmap[FTBITS]; // thread bit -> local bit
+    int8_t tmap[FTBMAX]; // thread bit -> local bit
     int16_t first, count;
     // X / CNOT gates of the group, as the affine bit map P(l) = M l ^ mb they
     // induce on local indices: applied for free by storing register l at P(l)
     int16_t mb;
-    int16_t mcol[FM];    // column j of M = P(e_j) ^ mb
+    int16_t mcol[FMMAX]; // column j of M = P(e_j) ^ mb
     int16_t perm;        // P is not the identity
     // byte offsets in the swizzled tile (host-precomputed, XOR-combined):
-    int16_t qb, qcol[FM];                           // load map Q (leading X / CNOT)
-    uint16_t ld_b, ld_t[FTBITS], ld_s[FSLOTS];      // load through Q: offset, thread bits, slots
-    uint16_t st_b, st_t[FTBITS], st_s[FSLOTS];      // store through P
+    int16_t qb, qcol[FMMAX];                        // load map Q (leading X / CNOT)
+    uint32_t ld_b, ld_t[FTBMAX], ld_s[FSLOTS];      // load through Q: offset, thread bits, slots
+    uint32_t st_b, st_t[FTBMAX], st_s[FSLOTS];      // store through P
 };
 struct FPass {
     int ngates, ngroups, ncomp, flow;
+    int fm;                         // tile qubits (== FM for the interpreter)
     int direct_first, direct_last;  // first/last group move registers <-> HBM directly
-    int64_t gl_b, gl_t[FTBITS], gl_s[FSLOTS];        // first group: offsets through its load map
-    int64_t gs_b, gs_t[FTBITS], gs_s[FSLOTS];        // last group: offsets through its store map
+    int64_t gl_b, gl_t[FTBMAX], gl_s[FSLOTS];        // first group: offsets through its load map
+    int64_t gs_b, gs_t[FTBMAX], gs_s[FSLOTS];        // last group: offsets through its store map
     int8_t comp[64];      // tile-index bit j -> global qubit comp[j]
-    int8_t rowbit[FM];    // local bit flow+j -> global qubit rowbit[j]
+    int8_t rowbit[FMMAX]; // local bit flow+j -> global qubit rowbit[j]
     FGroup groups[FMAXGRP];
     FGate gates[FMAXG];
 };
-
+static_assert(sizeof(FPass) <= 32000, "FPass is a __grid_constant__ kernel parameter");
 
 }  // namespace svb

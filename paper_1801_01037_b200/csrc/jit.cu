@@ -98,15 +98,15 @@ __device__ __forceinline__ d2 ldcs(const d2 *p) {
 __device__ __forceinline__ void stcs(d2 *p, d2 v) {
     asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" :: "l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
-__device__ __forceinline__ int swz(int l) { return l ^ ((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7; }
+__device__ __forceinline__ int swz(int l) { return l ^ ((l >> 3) ^ (l >> 6) ^ (l >> 9) ^ (l >> 12)) & 7; }
 __device__ __forceinline__ double ng(double x) {  // -x as a sign-bit flip (integer pipe)
     return __longlong_as_double(__double_as_longlong(x) ^ (long long)0x8000000000000000ull);
 }
 )";
 
-int swz_h(int l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7); }
+int swz_h(int l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9) ^ (l >> 12)) & 7); }
 
-unsigned xcombo_h(const uint16_t *s, int i) {
+unsigned xcombo_h(const uint32_t *s, int i) {
     unsigned r = 0;
     for (int k = 0; k < FSLOTS; ++k)
         if ((i >> k) & 1) r ^= s[k];
@@ -587,33 +587,44 @@ void emit_gate_fast(Out &o, const FGate &g, int *code, double2 &F) {
 int jit_mode() {
     static int m = [] {
         const char *e = getenv("SVB_JIT_MODE");
-        int v = e ? atoi(e) : 0;
-        return (v >= 0 && v <= 2) ? v : 0;
+        int v = e ? atoi(e) : -1;
+        return (v >= 0 && v <= 2) ? v : -1;
     }();
     return m;
 }
 
+// default per tile size: fm 11 runs 4 CTAs/SM, which already overlap one
+// another's loads; fm 12/13 run 2 / 1 CTAs per SM and need the prefetch
+// (measured on configs[1]: fm 13 mode 0 75.2k, mode 2 86.6k gate apps/s)
 int jit_pass_mode(const FPass &P) {
     int m = jit_mode();
+    if (m < 0) m = P.fm > 11 ? 2 : 0;
+    if (m == 1 && P.fm != 11) m = 0;  // two tiles fit only at fm 11
     if (m == 2 && !P.direct_last) m = 0;
     return m;
 }
 
-// resident CTAs per SM the generated kernel is built for (__launch_bounds__)
+int jit_threads(const FPass &P) { return (1 << P.fm) / FREGS; }
+
+// resident CTAs per SM the generated kernel is built for (__launch_bounds__):
+// 128 registers per thread (16 amplitudes + addresses), so 64K / (128 x threads)
 int jit_ctas_per_sm(const FPass &P) {
     static int c = [] {
         const char *e = getenv("SVB_JIT_CTAS");
-        int v = e ? atoi(e) : FCTAS_PER_SM;
-        return (v >= 1 && v <= 8) ? v : FCTAS_PER_SM;
+        int v = e ? atoi(e) : 0;
+        return (v >= 1 && v <= 8) ? v : 0;
     }();
-    return jit_pass_mode(P) == 1 ? 3 : c;
+    if (jit_pass_mode(P) == 1) return 3;
+    if (c) return c;
+    return std::max(1, 512 / jit_threads(P));
 }
 // tile buffers live in dynamic shared memory when they exceed the 48 KiB
-// static limit (double buffering, or FM >= 12 builds)
+// static limit (double buffering, or tiles of 12+ qubits)
 size_t jit_dyn_smem(const FPass &P) {
-    const size_t b = (jit_pass_mode(P) == 1 ? 2 : 1) * FTILE * sizeof(double2);
+    const size_t b = (jit_pass_mode(P) == 1 ? 2 : 1) * (size_t(1) << P.fm) * sizeof(double2);
     return b > 40 * 1024 ? b : 0;
 }
+
 
 // Thread-index copy the compiler cannot see through: per-thread address
 // terms are recomputed where they are used instead of being hoisted out of
@@ -628,6 +639,7 @@ std::string jit_source(const FPass &P, int variant, double2 &F, bool last) {
     Out o;
     o("#define SVB_FMA %d\n", fma ? 1 : 0);
     o.s += kPreamble;
+    const int FTILE = 1 << P.fm, FTHREADS = jit_threads(P), FTBITS = P.fm - FSLOTS;
     const int nrows = FTILE >> P.flow;
     const int colmask = (1 << P.flow) - 1;
     o("extern \"C\" __global__ void __launch_bounds__(%d, %d) kpass(d2 *__restrict__ a, i64 ntiles) {\n",
@@ -639,7 +651,7 @@ std::string jit_source(const FPass &P, int variant, double2 &F, bool last) {
     o("__shared__ i64 rowoff[%d];\n", nrows);
     o("const int tid = threadIdx.x;\n");
     o("for (int r = tid; r < %d; r += %d) { i64 off = 0;\n", nrows, FTHREADS);
-    for (int j = 0; j < FM - P.flow; ++j) o("if ((r >> %d) & 1) off |= 1ll << %d;\n", j, P.rowbit[j]);
+    for (int j = 0; j < P.fm - P.flow; ++j) o("if ((r >> %d) & 1) off |= 1ll << %d;\n", j, P.rowbit[j]);
     o("rowoff[r] = off; }\n__syncthreads();\n");
     o("auto tbase = [&](i64 t) { i64 b = 0;\n");
     for (int j = 0; j < P.ncomp; ++j) o("b |= ((t >> %d) & 1) << %d;\n", j, P.comp[j]);
@@ -801,6 +813,8 @@ static const Nvrtc &nvrtc() {
     return n;
 }
 
+bool jit_available() { return nvrtc().ok; }
+
 static bool nvrtc_compile(const std::string &src, std::vector<char> &cubin, std::string &log) {
     const Nvrtc &nv = nvrtc();
     if (!nv.ok) {
@@ -936,7 +950,8 @@ bool jit_launch(void *fn, const FPass &P, double2 *a, int64_t ntiles, cudaStream
     const int grid = (int)std::min<int64_t>(ntiles, int64_t(sms) * jit_ctas_per_sm(P));
     long long nt = ntiles;
     void *args[] = {&a, &nt};
-    return cudaLaunchKernel((const void *)fn, dim3(grid), dim3(FTHREADS), args, jit_dyn_smem(P), s) == cudaSuccess;
+    return cudaLaunchKernel((const void *)fn, dim3(grid), dim3(jit_threads(P)), args, jit_dyn_smem(P), s) ==
+           cudaSuccess;
 }
 
 }  // namespace svb

@@ -137,21 +137,23 @@ def run_ops(s, ops, fuse: bool = True, strict_order: bool = False, fma: bool = F
     return s
 
 
-def plan_stats(n: int, ops, fuse: bool = True, strict_order: bool = False) -> tuple[int, int]:
-    """(HBM passes, shared-memory register groups) the planner makes (host only)."""
+def plan_stats(n: int, ops, fuse: bool = True, strict_order: bool = False,
+               jit: bool = False) -> tuple[int, int]:
+    """(HBM passes, shared-memory register groups) the planner makes (host
+    only); jit: the plan runtime-specialised passes get (larger tiles)."""
     lib = _lib.load(require_cuda=False)
     if isinstance(ops, Circuit):
         ops = ops.ops
     arr, nops = _lib.ops_array(ops)
-    flags = (_lib.RUN_FUSE if fuse else 0) | (_lib.RUN_STRICT_ORDER if strict_order else 0)
+    flags = _lib.run_flags(fuse, strict_order, jit=jit)
     out, groups = ctypes.c_int(0), ctypes.c_int(0)
     _lib.check(lib.svb_plan_passes(int(n), arr, nops, flags, ctypes.byref(out), ctypes.byref(groups)),
                "plan_passes")
     return out.value, groups.value
 
 
-def plan_passes(n: int, ops, fuse: bool = True, strict_order: bool = False) -> int:
-    return plan_stats(n, ops, fuse, strict_order)[0]
+def plan_passes(n: int, ops, fuse: bool = True, strict_order: bool = False, jit: bool = False) -> int:
+    return plan_stats(n, ops, fuse, strict_order, jit)[0]
 
 
 def norm2(s) -> float:

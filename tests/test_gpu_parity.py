@@ -170,6 +170,24 @@ def test_bench_path_deep_circuit_vs_oracle(cuda_ok):
     assert abs(device.norm2(st) - 1.0) < 1e-12
 
 
+@pytest.mark.parametrize("fm", [11, 12, 13])
+def test_jit_tile_sizes_vs_oracle(cuda_ok, fm, monkeypatch):
+    # runtime-specialised passes may use 2^12 / 2^13-amplitude tiles (64 /
+    # 128 KiB of shared memory, 256 / 512 threads): every tile size agrees
+    # with the oracle, exact arithmetic bit-identical to the interpreter's
+    monkeypatch.setenv("SVB_JIT_FM", str(fm))
+    n = 22
+    rng = np.random.default_rng(900 + fm)
+    circ = w.random_layer_circuit(n, 12, seed=fm)
+    a = w.random_state_array(rng, n)
+    want = oracle.run_ops(a.copy(), w.oracle_ops(circ), workers=16)
+    got = device.simulate(circ, a.copy(), fma=True, jit=True)
+    assert np.max(np.abs(got - want)) <= TOL
+    assert device.plan_passes(n, circ, jit=True) <= device.plan_passes(n, circ)
+    got = device.simulate(circ, a.copy(), strict_order=True, jit=True)
+    assert np.array_equal(got, device.simulate(circ, a.copy(), strict_order=True))
+
+
 @pytest.mark.parametrize("n", [14, 19])
 def test_jit_passes_bit_identical_to_interpreter(cuda_ok, n, monkeypatch):
     # SVB_RUN_JIT compiles each fused pass to straight-line code; on the same
