@@ -46,10 +46,36 @@ struct Out {
     }
 };
 
-std::string lit(double x) {
+std::string hexf(double x) {
     char b[64];
     snprintf(b, sizeof b, "%a", x);
     return b;
+}
+
+// Gate coefficients live in a __constant__ table of the generated module:
+// FP64 instructions take constant-bank operands directly, while literals
+// would be materialised with two UMOVs each.  While a source is generated,
+// lit() interns its value (by bit pattern) and names the table slot.
+struct ConstPool {
+    std::vector<double> vals;
+    std::unordered_map<uint64_t, int> index;
+};
+thread_local ConstPool *t_pool = nullptr;
+
+std::string lit(double x) {
+    if (!t_pool) return hexf(x);
+    uint64_t bits;
+    memcpy(&bits, &x, 8);
+    auto it = t_pool->index.find(bits);
+    int i;
+    if (it != t_pool->index.end()) {
+        i = it->second;
+    } else {
+        i = (int)t_pool->vals.size();
+        t_pool->vals.push_back(x);
+        t_pool->index[bits] = i;
+    }
+    return "kc[" + std::to_string(i) + "]";
 }
 
 const char *kPreamble = R"(
@@ -633,42 +659,92 @@ const char *kOpaqueTid = "unsigned tg = tid; asm volatile(\"\" : \"+r\"(tg));\n"
 
 // variant: 0 exact, 1 FMA, 2 FMA + factor extraction (F: the global factor
 // carried in and out; last: the circuit's last fused pass, which applies F)
+std::string jit_body(const FPass &P, int variant, double2 &F, bool last);
+
 std::string jit_source(const FPass &P, int variant, double2 &F, bool last) {
+    ConstPool pool;
+    t_pool = &pool;
+    std::string body = jit_body(P, variant, F, last);
+    t_pool = nullptr;
+    Out o;
+    o("#define SVB_FMA %d\n", variant >= 1 ? 1 : 0);
+    o.s += kPreamble;
+    o("__constant__ double kc[%d] = {", std::max<int>(1, (int)pool.vals.size()));
+    for (size_t i = 0; i < pool.vals.size(); ++i) o("%s%s", i ? ", " : "", hexf(pool.vals[i]).c_str());
+    if (pool.vals.empty()) o("0.0");
+    o("};\n");
+    return o.s + body;
+}
+
+std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
     const bool fma = variant >= 1, fast = variant == 2;
     const int mode = jit_pass_mode(P);
     Out o;
-    o("#define SVB_FMA %d\n", fma ? 1 : 0);
-    o.s += kPreamble;
     const int FTILE = 1 << P.fm, FTHREADS = jit_threads(P), FTBITS = P.fm - FSLOTS;
-    const int nrows = FTILE >> P.flow;
     const int colmask = (1 << P.flow) - 1;
+    // Tile-local global offsets are XOR-linear in the thread index and the
+    // register number: thread parts are computed per use from the opaque
+    // index, register parts are constants.  They fit 32 bits while every
+    // tile qubit is < 32 (always, for one GPU's <= 2^31-amplitude slab), so
+    // an address is one XOR plus one IMAD.WIDE off the tile pointer pa.
+    int maxbit = P.flow - 1;
+    for (int j = 0; j < P.fm - P.flow; ++j) maxbit = std::max(maxbit, (int)P.rowbit[j]);
+    const bool narrow = maxbit < 32;
+    const char *OFF = narrow ? "unsigned" : "i64";
+    auto offl = [&](int64_t v) {
+        char b[40];
+        if (narrow)
+            snprintf(b, sizeof b, "%uu", (unsigned)v);
+        else
+            snprintf(b, sizeof b, "%lldll", (long long)v);
+        return std::string(b);
+    };
+    int lt = 0;  // log2(threads)
+    while ((1 << lt) < FTHREADS) ++lt;
+    // element e = tid + k * threads: column = tid's low flow bits, row bits =
+    // tid's remaining bits then k's bits
+    auto row_off = [&](int rbit) { return int64_t(1) << P.rowbit[rbit]; };
     o("extern \"C\" __global__ void __launch_bounds__(%d, %d) kpass(d2 *__restrict__ a, i64 ntiles) {\n",
       FTHREADS, jit_ctas_per_sm(P));
     if (jit_dyn_smem(P))
         o("extern __shared__ d2 dsm[];\n");
     else
         o("__shared__ alignas(16) d2 dsm[%d];\n", FTILE);
-    o("__shared__ i64 rowoff[%d];\n", nrows);
     o("const int tid = threadIdx.x;\n");
-    o("for (int r = tid; r < %d; r += %d) { i64 off = 0;\n", nrows, FTHREADS);
-    for (int j = 0; j < P.fm - P.flow; ++j) o("if ((r >> %d) & 1) off |= 1ll << %d;\n", j, P.rowbit[j]);
-    o("rowoff[r] = off; }\n__syncthreads();\n");
     o("auto tbase = [&](i64 t) { i64 b = 0;\n");
     for (int j = 0; j < P.ncomp; ++j) o("b |= ((t >> %d) & 1) << %d;\n", j, P.comp[j]);
     o("return b; };\n");
-    o("auto fill = [&](d2 *dst, i64 b) {\n%s#pragma unroll\nfor (int k = 0; k < %d; ++k) { int e = tg + k * %d;\n", kOpaqueTid,
-      FREGS, FTHREADS);
-    o("cpa(&dst[swz(e)], &a[b + rowoff[e >> %d] + (e & %d)]); }\n", P.flow, colmask);
+    // per-thread (global row/column offset, swizzled smem byte offset) of element tid
+    auto thread_parts = [&]() {
+        o("%s r = tg & %d; unsigned s = 0;\n", OFF, colmask);
+        for (int j = 0; j < lt; ++j) {
+            if (j >= P.flow) o("if ((tg >> %d) & 1) r ^= %s;\n", j, offl(row_off(j - P.flow)).c_str());
+            o("if ((tg >> %d) & 1) s ^= %uu;\n", j, (unsigned)(16 * swz_h(1 << j)));
+        }
+    };
+    auto k_row = [&](int k) {
+        int64_t v = 0;
+        for (int b = 0; (1 << b) <= k; ++b)
+            if ((k >> b) & 1) v ^= row_off(lt - P.flow + b);
+        return v;
+    };
+    auto k_smem = [&](int k) { return (unsigned)(16 * swz_h(k * FTHREADS)); };
+    o("auto fill = [&](unsigned char *dstb, const d2 *p) {\n%s", kOpaqueTid);
+    thread_parts();
+    for (int k = 0; k < FREGS; ++k)
+        o("cpa(dstb + (s ^ %uu), p + (r ^ %s));\n", k_smem(k), offl(k_row(k)).c_str());
     o("asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\"); };\n(void)fill;\n");
     const char *wait_all = "asm volatile(\"cp.async.wait_group 0;\\n\" ::: \"memory\");\n";
     const bool direct_first = P.direct_first && mode == 0;
-    if (mode != 0) o("if (blockIdx.x < ntiles) fill(dsm, tbase(blockIdx.x));\n");
+    if (mode != 0)
+        o("if (blockIdx.x < ntiles) fill(reinterpret_cast<unsigned char *>(dsm), a + tbase(blockIdx.x));\n");
     o("int it = 0;\nfor (i64 tix = blockIdx.x; tix < ntiles; tix += gridDim.x, ++it) {\n");
-    o("const i64 base = tbase(tix);\n");
+    o("d2 *const pa = a + tbase(tix);\n");
     if (mode == 1) {
         o("d2 *buf = dsm + (it & 1) * %d;\n", FTILE);
         o.s += wait_all;
-        o("__syncthreads();\n{ const i64 nx = tix + gridDim.x; if (nx < ntiles) fill(dsm + ((it + 1) & 1) * %d, tbase(nx)); }\n",
+        o("__syncthreads();\n{ const i64 nx = tix + gridDim.x; if (nx < ntiles) "
+          "fill(reinterpret_cast<unsigned char *>(dsm + ((it + 1) & 1) * %d), a + tbase(nx)); }\n",
           FTILE);
     } else {
         o("d2 *buf = dsm;\n");
@@ -676,7 +752,7 @@ std::string jit_source(const FPass &P, int variant, double2 &F, bool last) {
             o.s += wait_all;
             o("__syncthreads();\n");
         } else if (!direct_first) {
-            o("fill(buf, base);\n");
+            o("fill(reinterpret_cast<unsigned char *>(buf), pa);\n");
             o.s += wait_all;
             o("__syncthreads();\n");
         }
@@ -688,11 +764,11 @@ std::string jit_source(const FPass &P, int variant, double2 &F, bool last) {
         const bool last = gi == P.ngroups - 1;
         o("{ // group %d\n", gi);
         if (gi == 0 && direct_first) {
-            o("i64 g0 = %lldll;\n", (long long)P.gl_b);
+            o("%s g0 = %s;\n", OFF, offl(P.gl_b).c_str());
             o.s += kOpaqueTid;
-            for (int j = 0; j < FTBITS; ++j) o("if ((tg >> %d) & 1) g0 ^= %lldll;\n", j, (long long)P.gl_t[j]);
+            for (int j = 0; j < FTBITS; ++j) o("if ((tg >> %d) & 1) g0 ^= %s;\n", j, offl(P.gl_t[j]).c_str());
             for (int i = 0; i < FREGS; ++i)
-                o("v[%d] = ldcs(a + (base | (g0 ^ %lldll)));\n", i, (long long)xcombo_g(P.gl_s, i));
+                o("v[%d] = ldcs(pa + (g0 ^ %s));\n", i, offl(xcombo_g(P.gl_s, i)).c_str());
         } else {
             o("unsigned a0 = %uu;\n", (unsigned)G.ld_b);
             o.s += kOpaqueTid;
@@ -702,7 +778,8 @@ std::string jit_source(const FPass &P, int variant, double2 &F, bool last) {
         }
         if (last && mode == 2) {
             // every thread has its registers: refill the buffer with the next tile
-            o("__syncthreads();\n{ const i64 nx = tix + gridDim.x; if (nx < ntiles) fill(dsm, tbase(nx)); }\n");
+            o("__syncthreads();\n{ const i64 nx = tix + gridDim.x; if (nx < ntiles) "
+              "fill(reinterpret_cast<unsigned char *>(dsm), a + tbase(nx)); }\n");
         }
         if (fast) {
             int code[FREGS] = {0};
@@ -726,12 +803,12 @@ std::string jit_source(const FPass &P, int variant, double2 &F, bool last) {
         }
         if (last && P.direct_last) {
             if (G.perm && gi == 0 && direct_first) o("__syncthreads();\n");
-            o("i64 s0 = %lldll;\n", (long long)P.gs_b);
+            o("%s s0 = %s;\n", OFF, offl(P.gs_b).c_str());
             o("{\n%s", kOpaqueTid);
-            for (int j = 0; j < FTBITS; ++j) o("if ((tg >> %d) & 1) s0 ^= %lldll;\n", j, (long long)P.gs_t[j]);
+            for (int j = 0; j < FTBITS; ++j) o("if ((tg >> %d) & 1) s0 ^= %s;\n", j, offl(P.gs_t[j]).c_str());
             o("}\n");
             for (int i = 0; i < FREGS; ++i)
-                o("stcs(a + (base | (s0 ^ %lldll)), v[%d]);\n", (long long)xcombo_g(P.gs_s, i), i);
+                o("stcs(pa + (s0 ^ %s), v[%d]);\n", offl(xcombo_g(P.gs_s, i)).c_str(), i);
         } else {
             if (G.perm) o("__syncthreads();\n");
             o("unsigned b0 = %uu;\n", (unsigned)G.st_b);
@@ -745,8 +822,11 @@ std::string jit_source(const FPass &P, int variant, double2 &F, bool last) {
         o("}\n");
     }
     if (!P.direct_last) {
-        o("{\n%s#pragma unroll\nfor (int k = 0; k < %d; ++k) { int e = tg + k * %d;\n", kOpaqueTid, FREGS, FTHREADS);
-        o("a[base + rowoff[e >> %d] + (e & %d)] = buf[swz(e)]; }\n}\n", P.flow, colmask);
+        o("{\n%s", kOpaqueTid);
+        thread_parts();
+        for (int k = 0; k < FREGS; ++k)
+            o("pa[r ^ %s] = *reinterpret_cast<const d2 *>(sb + (s ^ %uu));\n", offl(k_row(k)).c_str(), k_smem(k));
+        o("}\n");
     }
     // mode 0: the buffer must be free before the next tile's loads; modes 1/2
     // order reuse with the barrier after the next wait

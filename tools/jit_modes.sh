@@ -1,6 +1,9 @@
-# configs[1] bench
+# GPU tests + configs[1] bench
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
 run() {
   env $1 timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu --no-sweep > gpurun_out/$2.json 2> gpurun_out/$2.err
   python -c "import json;d=json.load(open('gpurun_out/$2.json'));r=d['roofline'];print('$2',d['value'],d['e2e']['value'],r['achieved'],r['avg_launch_ms'],r['launches'],d['config']['hbm_passes_per_step'],d['check'],d['first_step_s'])" || tail -5 gpurun_out/$2.err
 }
 run "X=1" default
+run "SVB_JIT_FM=11" fm11
+run "SVB_JIT_FM=13" fm13
