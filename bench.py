@@ -244,7 +244,7 @@ def run_gpu_arm(args) -> None:
     from paper_1801_01037_b200 import _lib, device, workloads
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1:
+    if world > 1 or os.environ.get("SVB_BENCH_DIST") == "1":  # (=1: the N>1 engine at world 1, a smoke test)
         from paper_1801_01037_b200 import dist
 
         dist.bench_main(args)
@@ -275,7 +275,7 @@ def run_gpu_arm(args) -> None:
     for _ in range(max(args.warmup - 1, 0)):
         step()
     torch.cuda.synchronize()
-    _lib.profile_enable(True)
+    _lib.profile_enable(os.environ.get("SVB_BENCH_NOPROF") != "1")  # (=1: measure the profiler's cost)
     launches0 = _lib.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device()) as clk:

@@ -142,7 +142,7 @@ def gate_array(g) -> ctypes.Array:
 _OP_DTYPE = np.dtype([("kind", "<i4"), ("target", "<i4"), ("control", "<i4"), ("reserved", "<i4"),
                       ("q", "<f8", (8,))])
 assert _OP_DTYPE.itemsize == ctypes.sizeof(SvbOp)
-_OPS_CACHE: dict = {}  # id(ops tuple) -> (the tuple, packed array, count); a few recent circuits
+_OPS_CACHE: dict = {}  # id(ops tuple) -> (the tuple, packed array, count); recent circuits / segments
 
 
 def ops_array(ops) -> tuple[ctypes.Array, int]:
@@ -164,7 +164,7 @@ def ops_array(ops) -> tuple[ctypes.Array, int]:
         packed["q"][:n] = [op.gate.as_doubles() for op in seq]
     arr = (SvbOp * max(n, 1)).from_buffer(packed)
     if key is not None:
-        if len(_OPS_CACHE) >= 8:
+        if len(_OPS_CACHE) >= 512:
             _OPS_CACHE.pop(next(iter(_OPS_CACHE)))
         _OPS_CACHE[key] = (ops, arr, n)
     return arr, n

@@ -1282,9 +1282,17 @@ static std::shared_ptr<const CompiledPlan> compiled_plan(int n, const svb_op *op
             for (int oi : pp.ops) cp->steps.push_back(PlanStep{oi});
         }
     }
+    // Bounded by descriptor bytes (~27 KiB per pass), not by count: the
+    // multi-process engine runs one op segment per exchange interval, so a
+    // circuit step may cycle through hundreds of small plans.
     std::lock_guard<std::mutex> lk(mu);
     cache.insert(cache.begin(), {key, cp});
-    if (cache.size() > 4) cache.pop_back();
+    size_t bytes = 0, keep = 0;
+    for (; keep < cache.size(); ++keep) {
+        bytes += cache[keep].second->passes.size() * sizeof(FPass) + cache[keep].second->ops.size() * sizeof(svb_op);
+        if (keep >= 4 && bytes > (size_t(256) << 20)) break;
+    }
+    cache.resize(std::max<size_t>(keep, 1));
     return cp;
 }
 

@@ -69,11 +69,12 @@ class CudaCompute:
     def to_numpy(self, t) -> np.ndarray:
         return t.cpu().numpy()
 
-    def run_ops(self, slab, ops, fuse: bool = True, strict: bool = False) -> None:
+    def run_ops(self, slab, ops, fuse: bool = True, strict: bool = False, fma: bool = False,
+                jit: bool = False) -> None:
         if not ops:
             return
-        arr, nops = self._lib.ops_array(ops)
-        flags = (self._lib.RUN_FUSE if fuse else 0) | (self._lib.RUN_STRICT_ORDER if strict else 0)
+        arr, nops = self._lib.ops_array(ops if isinstance(ops, tuple) else tuple(ops))
+        flags = self._lib.run_flags(fuse, strict, fma, jit)
         self._lib.check(self.lib.svb_run_ops(ctypes.c_void_p(slab.data_ptr()), slab.shape[0], arr,
                                              nops, flags, self._sp()), "run_ops")
 
@@ -122,7 +123,7 @@ class DistEngine:
     """This process's rank of a 2^k-way partitioned n-qubit state."""
 
     def __init__(self, n: int, compute=None, group=None, initial=None, chunk: int = DEFAULT_CHUNK,
-                 fuse: bool = True, elide_diagonal: bool = True):
+                 fuse: bool = True, elide_diagonal: bool = True, fma: bool = False, jit: bool = False):
         import torch.distributed as dist
 
         self.dist = dist
@@ -139,6 +140,7 @@ class DistEngine:
         self.compute = compute if compute is not None else CudaCompute()
         self.chunk = max(1, min(int(chunk), self.L))
         self.fuse = fuse
+        self.fma, self.jit = fma, jit  # local segments: FMA fused passes / NVRTC-specialised
         self.elide_diagonal = elide_diagonal
         self.stats = ExchangeStats()
         if initial is not None:
@@ -151,6 +153,8 @@ class DistEngine:
             if self.rank == 0:
                 self.slab[0] = 1.0
         self._pending: list[GateOp] = []
+        self._pending_key = None  # the cached tuple _pending was copied from, if any
+        self._scheds: dict = {}
         self._bufs = None
 
     # -- helpers ------------------------------------------------------------
@@ -163,8 +167,13 @@ class DistEngine:
 
     def _flush(self) -> None:
         if self._pending:
-            self.compute.run_ops(self.slab, self._pending, fuse=self.fuse)
+            ops = self._pending_key if self._pending_key is not None else tuple(self._pending)
+            if self.fma or self.jit:
+                self.compute.run_ops(self.slab, ops, fuse=self.fuse, fma=self.fma, jit=self.jit)
+            else:
+                self.compute.run_ops(self.slab, ops, fuse=self.fuse)
             self._pending = []
+        self._pending_key = None
 
     def _diag_local(self, g: Gate2x2, bit_set: bool, cbit: int | None) -> None:
         """Global-target diagonal gate: scale own amplitudes by q11 or q22."""
@@ -238,12 +247,52 @@ class DistEngine:
             return
         self._exchange(g, t, c)
 
+    def _schedule(self, ops: tuple) -> tuple[list, int]:
+        """This rank's action list for an op tuple -- ("local", op tuple) runs
+        and ("exchange", gate, target, control) steps -- as apply() would
+        produce it; cached per circuit so repeated runs do no per-op Python
+        work (the local tuples also hit the packed-op cache)."""
+        hit = self._scheds.get(id(ops))
+        if hit is not None and hit[0] is ops:
+            return hit[1], hit[2]
+        saved, self._pending = self._pending, []
+        actions, elided = [], 0
+        exchange = self._exchange
+        try:
+            def record(g, t, c):
+                if self._pending:
+                    actions.append(("local", tuple(self._pending)))
+                    self._pending = []
+                actions.append(("exchange", g, t, c))
+            self._exchange = record
+            before = self.stats.elided
+            for op in ops:
+                self.apply(op)
+            elided = self.stats.elided - before
+            self.stats.elided = before
+            if self._pending:
+                actions.append(("local", tuple(self._pending)))
+        finally:
+            self._exchange = exchange
+            self._pending = saved
+        if len(self._scheds) >= 8:
+            self._scheds.pop(next(iter(self._scheds)))
+        self._scheds[id(ops)] = (ops, actions, elided)
+        return actions, elided
+
     def run(self, circuit: Circuit) -> "DistEngine":
         if circuit.n != self.n:
             raise ValidationError(f"circuit has {circuit.n} qubits, engine has {self.n}")
-        for op in circuit.ops:
-            self.apply(op)
         self._flush()
+        actions, elided = self._schedule(circuit.ops)
+        for act in actions:
+            if act[0] == "local":
+                self._pending = list(act[1])
+                self._pending_key = act[1]
+                self._flush()
+            else:
+                self._exchange(act[1], act[2], act[3])
+        self.stats.elided += elided
         return self
 
     def norm2(self) -> float:
@@ -296,7 +345,7 @@ def bench_main(args) -> None:
     layers = int(os.environ.get("SVB_BENCH_LAYERS", "200"))
     circuit = workloads.random_layer_circuit(n, layers)
     nops = len(circuit.ops)
-    eng = DistEngine(n)
+    eng = DistEngine(n, fma=getattr(args, "fma", True), jit=getattr(args, "jit", True))
     stream = torch.cuda.current_stream()
 
     def step():

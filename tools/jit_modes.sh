@@ -1,9 +1,5 @@
-# GPU tests + configs[1] bench
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-run() {
-  env $1 timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu --no-sweep > gpurun_out/$2.json 2> gpurun_out/$2.err
-  python -c "import json;d=json.load(open('gpurun_out/$2.json'));r=d['roofline'];print('$2',d['value'],d['e2e']['value'],r['achieved'],r['avg_launch_ms'],r['launches'],d['config']['hbm_passes_per_step'],d['check'],d['first_step_s'])" || tail -5 gpurun_out/$2.err
-}
-run "X=1" default
-run "SVB_JIT_FM=11" fm11
-run "SVB_JIT_FM=13" fm13
+# N=1 bench with / without the in-library launch profiler, twice each
+for i in 1 2; do
+python bench.py --steps 5 --warmup 3 --no-cpu --no-sweep 2>/dev/null | python -c "import json,sys;d=json.loads(sys.stdin.read());print('prof',d['value'],d['ms_per_step'],d['clocks'])"
+SVB_BENCH_NOPROF=1 python bench.py --steps 5 --warmup 3 --no-cpu --no-sweep 2>/dev/null | python -c "import json,sys;d=json.loads(sys.stdin.read());print('noprof',d['value'],d['ms_per_step'],d['clocks'])"
+done
