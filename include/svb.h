@@ -50,9 +50,11 @@ typedef struct svb_op {
 /* svb_run_ops flags */
 #define SVB_RUN_FUSE 1u         /* plan multi-gate shared-memory passes        */
 #define SVB_RUN_STRICT_ORDER 2u /* fuse only contiguous runs (bit-exact order) */
-#define SVB_RUN_FMA 4u          /* fused passes may contract a*b+c (not with STRICT) */
+#define SVB_RUN_FMA 4u          /* fused passes may contract a*b+c and (with JIT) pull
+                                   scalars out of 1-qubit gates; <= 1e-12 (not with STRICT) */
 #define SVB_RUN_JIT 8u          /* compile each fused pass to straight-line code (NVRTC,
-                                   cached per op list; falls back to the interpreter) */
+                                   cached per op list): 12-qubit tiles, X/CNOT as register
+                                   renames; falls back to the interpreter without NVRTC */
 
 int svb_abi_version(void);
 const char *svb_last_error(void);
@@ -61,8 +63,8 @@ int64_t svb_launch_count(void);
 
 /* Launch profiler: while enabled, every gate/exchange launch is bracketed by
  * CUDA events on its own stream and aggregated per kernel class (0
- * k_pair_high, 1 k_pair_low, 2 k_diag, 3 k_tiny, 4 k_fused, 5 k_exchange)
- * with its algorithmic HBM bytes.  enable() resets the totals; read()
+ * k_pair_high, 1 k_pair_low, 2 k_diag, 3 k_tiny, 4 k_fused, 5 k_exchange,
+ * 6 k_norm, 7 kpass_jit) with its algorithmic HBM bytes.  enable() resets the totals; read()
  * synchronises on the recorded events. */
 int svb_profile_enable(int on);
 int svb_profile_read(int cls, int64_t *launches, double *total_ms, int64_t *alg_bytes);
