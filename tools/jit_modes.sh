@@ -1,5 +1,9 @@
-# N=1 bench with / without the in-library launch profiler, twice each
-for i in 1 2; do
-python bench.py --steps 5 --warmup 3 --no-cpu --no-sweep 2>/dev/null | python -c "import json,sys;d=json.loads(sys.stdin.read());print('prof',d['value'],d['ms_per_step'],d['clocks'])"
-SVB_BENCH_NOPROF=1 python bench.py --steps 5 --warmup 3 --no-cpu --no-sweep 2>/dev/null | python -c "import json,sys;d=json.loads(sys.stdin.read());print('noprof',d['value'],d['ms_per_step'],d['clocks'])"
-done
+# GPU tests + configs[1] bench (direct groups everywhere, default now)
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
+run() {
+  env $1 timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu --no-sweep $3 > gpurun_out/$2.json 2> gpurun_out/$2.err
+  python -c "import json;d=json.load(open('gpurun_out/$2.json'));r=d['roofline'];print('$2',d['value'],d['e2e']['value'],r['achieved'],r['avg_launch_ms'],r['launches'],d['config']['hbm_passes_per_step'],d['check'])" || tail -5 gpurun_out/$2.err
+}
+run "X=1" default
+run "X=1" interp --no-jit
+run "SVB_FUSE_DIRECT=1" interp_d1 --no-jit
