@@ -1020,9 +1020,10 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
         auto low3 = [](const int16_t *col) { return (col[0] >> 3) == 0 && (col[1] >> 3) == 0 && (col[2] >> 3) == 0; };
         const bool can_df = gi == 0 && slots_high && low3(G.qcol);
         const bool can_dl = gi == P.ngroups - 1 && slots_high && low3(G.mcol);
-        const bool any = direct_any();
-        thread_map(fm, slots, G.tmap, G.qcol, G.mcol, !(can_df || (any && gi == 0)),
-                   !(can_dl || (any && gi == P.ngroups - 1)), can_df || can_dl);
+        // (an uncoalesced first group still reads shared memory when a JIT
+        // pass prefetches tiles, so only coalesced direct sides skip the
+        // bank-conflict search)
+        thread_map(fm, slots, G.tmap, G.qcol, G.mcol, !can_df, !can_dl, can_df || can_dl);
         for (int j = 0; j < tbits; ++j) {
             G.ld_t[j] = (uint32_t)(16 * swz(gp.qcol[G.tmap[j]]));
             G.st_t[j] = (uint32_t)(16 * swz(gp.mcol[G.tmap[j]]));
