@@ -824,6 +824,11 @@ static bool reg_perm(unsigned flags) {
     return e ? atoi(e) != 0 : (flags & SVB_RUN_JIT) != 0;
 }
 
+static bool reg_perm_any_ctl() {
+    const char *e = getenv("SVB_FUSE_REGPERM_CTL");
+    return !e || atoi(e) != 0;
+}
+
 // Build the kernel descriptor for one pass; false if it does not fit.
 static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, bool strict, bool regperm,
                        int fm) {
@@ -950,7 +955,11 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
                     // an X / CNOT whose target fits the group's slots runs in
                     // registers (a masked register swap) instead of being
                     // deferred to the store map, so it blocks nothing
-                    const bool inreg = m.perm && mode == 0 && regperm && (bits & blocked) == 0 &&
+                    // (SVB_FUSE_REGPERM_CTL=0: only when the control is already a
+                    // slot -- a thread-bit control costs a divergent swap)
+                    const bool ctl_ok = m.cl < 0 || reg_perm_any_ctl() ||
+                                        std::find(g->slots.begin(), g->slots.end(), m.cl) != g->slots.end();
+                    const bool inreg = m.perm && mode == 0 && regperm && ctl_ok && (bits & blocked) == 0 &&
                                        (bits & g->permq) == 0 && fits(*g, m);
                     bool ok = (bits & blocked) == 0 &&
                               (m.perm ? (mode != 0 || inreg)

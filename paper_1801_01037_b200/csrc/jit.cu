@@ -289,10 +289,84 @@ std::string cm_fold(const double2 &a, int cx) {
            chain({{a.x, "X", 1, cx}, {a.y, "X", 0, cx}}) + ")";
 }
 
+// ---------------------------------------------------------------------------
+// Pending conditional swaps (FMA modes).  A CNOT whose control is a thread
+// bit and whose target is a slot swaps register pairs along that slot in
+// half of the threads; done in place that is a divergent branch whose
+// reconvergence costs 64 register moves.  Instead the generator records it
+// (t_pend[slot] = thread bits whose parity says "swapped") and lets it ride:
+// every later gate that pairs along another slot, is diagonal elsewhere, or
+// is uniform per thread commutes with it; a gate that does not flushes it
+// with branch-free selects; at the group's store the swap becomes a
+// per-thread XOR of the store address (free).  Pending unit factors stay
+// symmetric along a swapped slot, so they commute too.
+thread_local uint32_t *t_pend = nullptr;
+
+std::string pcond(uint32_t m) {
+    char b[64];
+    if ((m & (m - 1)) == 0) {
+        int bit = 0;
+        while (!((m >> bit) & 1)) ++bit;
+        snprintf(b, sizeof b, "((tid >> %d) & 1)", bit);
+    } else {
+        snprintf(b, sizeof b, "(__popc(tid & %uu) & 1)", m);
+    }
+    return b;
+}
+
+void pend_flush(Out &o, int s) {
+    if (!t_pend || !t_pend[s]) return;
+    o("{ const bool p = %s;\n", pcond(t_pend[s]).c_str());
+    for (int i = 0; i < FREGS; ++i) {
+        if (i & (1 << s)) continue;
+        const int j = i | (1 << s);
+        o("{ const d2 a = v[%d], b = v[%d]; v[%d] = p ? b : a; v[%d] = p ? a : b; }\n", i, j, i, j);
+    }
+    o("}\n");
+    t_pend[s] = 0;
+}
+
+int slot_of_mask(unsigned cmask, int t) {
+    for (int k = 0; k < FSLOTS; ++k) {
+        unsigned pat = slot_pat(k) & ~(t >= 0 ? slot_pat(t) : 0u);
+        if (k != t && pat == cmask) return k;
+    }
+    return -1;
+}
+
+// flush the pending swaps a gate does not commute with
+void pend_conflicts(Out &o, const FGate &g) {
+    if (!t_pend) return;
+    const int op = g.op;
+    if (op < FOP_DIAG) {
+        const int t = (op >> 1) % FSLOTS, ctrl = op & 1;
+        pend_flush(o, t);
+        if (ctrl) {
+            const int k = slot_of_mask(g.cmask, t);
+            if (k < 0)
+                for (int x = 0; x < FSLOTS; ++x) pend_flush(o, x);
+            else
+                pend_flush(o, k);
+        }
+    } else {
+        const int c = op - FOP_DIAG;
+        const int ctrl = c & 1, tpos = (c >> 1) % (FSLOTS + 1);
+        if (tpos < FSLOTS) pend_flush(o, tpos);
+        if (ctrl) {
+            const int k = slot_of_mask(g.cmask, -1);
+            if (k < 0)
+                for (int x = 0; x < FSLOTS; ++x) pend_flush(o, x);
+            else
+                pend_flush(o, k);
+        }
+    }
+}
+
 void emit_gate_fold(Out &o, const FGate &g, int *code) {
     const double2 *m = g.m;
     const int op = g.op;
     const bool thread_ctl = g.cl >= 0;
+    pend_conflicts(o, g);
     if (op < FOP_DIAG) {
         const int kind = (op >> 1) / FSLOTS, s = (op >> 1) % FSLOTS, ctrl = op & 1;
         const int u12 = unit_code(m[1]), u21 = unit_code(m[2]);
@@ -303,6 +377,18 @@ void emit_gate_fold(Out &o, const FGate &g, int *code) {
             if (i & (1 << s)) continue;
             if (ctrl && !((g.cmask >> i) & 1)) continue;
             lows.push_back(i);
+        }
+        if (thread_ctl && unit_anti && t_pend && u12 == 0 && u21 == 0 && !ctrl) {
+            // controlled X on a thread-bit control: becomes a pending swap
+            for (int i : lows) {
+                const int j = i | (1 << s);
+                if (code[i] != code[j]) {
+                    materialize(o, code, i);
+                    materialize(o, code, j);
+                }
+            }
+            t_pend[s] ^= 1u << g.cl;
+            return;
         }
         if (thread_ctl && unit_anti) {
             // controlled X / Y on a thread-bit control: a conditional swap (plus
@@ -540,6 +626,7 @@ double2 pick_factor(const double2 *m, bool diag) {
 
 void emit_gate_fast(Out &o, const FGate &g, int *code, double2 &F) {
     const int op = g.op;
+    pend_conflicts(o, g);
     const bool uncontrolled = g.cl < 0 && !(op & 1);
     if (!uncontrolled) {  // a controlled gate scales only part of the state
         emit_gate_fold(o, g, code);
@@ -600,6 +687,12 @@ void emit_gate_fast(Out &o, const FGate &g, int *code, double2 &F) {
 }
 
 }  // namespace
+
+// SVB_JIT_PEND=0 turns pending swaps off (measurement)
+bool pend_on() {
+    const char *e = getenv("SVB_JIT_PEND");
+    return !e || atoi(e) != 0;
+}
 
 // Tile pipelining modes of the generated kernel:
 //   0  one shared buffer, 4 CTAs/SM; the first group reads HBM directly when
@@ -781,6 +874,8 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             o("__syncthreads();\n{ const i64 nx = tix + gridDim.x; if (nx < ntiles) "
               "fill(reinterpret_cast<unsigned char *>(dsm), a + tbase(nx)); }\n");
         }
+        uint32_t pend[FSLOTS] = {0};
+        if (fma && pend_on()) t_pend = pend;
         if (fast) {
             int code[FREGS] = {0};
             for (int q = G.first; q < G.first + G.count; ++q) emit_gate_fast(o, P.gates[q], code, F);
@@ -801,11 +896,14 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
         } else {
             for (int q = G.first; q < G.first + G.count; ++q) emit_gate(o, P.gates[q]);
         }
+        t_pend = nullptr;
         if (last && P.direct_last) {
             if (G.perm && gi == 0 && direct_first) o("__syncthreads();\n");
             o("%s s0 = %s;\n", OFF, offl(P.gs_b).c_str());
             o("{\n%s", kOpaqueTid);
             for (int j = 0; j < FTBITS; ++j) o("if ((tg >> %d) & 1) s0 ^= %s;\n", j, offl(P.gs_t[j]).c_str());
+            for (int k = 0; k < FSLOTS; ++k)  // pending swaps: per-thread store address
+                if (pend[k]) o("if (%s) s0 ^= %s;\n", pcond(pend[k]).c_str(), offl(P.gs_s[k]).c_str());
             o("}\n");
             for (int i = 0; i < FREGS; ++i)
                 o("stcs(pa + (s0 ^ %s), v[%d]);\n", offl(xcombo_g(P.gs_s, i)).c_str(), i);
@@ -814,6 +912,8 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             o("unsigned b0 = %uu;\n", (unsigned)G.st_b);
             o("{\n%s", kOpaqueTid);
             for (int j = 0; j < FTBITS; ++j) o("if ((tg >> %d) & 1) b0 ^= %uu;\n", j, (unsigned)G.st_t[j]);
+            for (int k = 0; k < FSLOTS; ++k)
+                if (pend[k]) o("if (%s) b0 ^= %uu;\n", pcond(pend[k]).c_str(), (unsigned)G.st_s[k]);
             o("}\n");
             for (int i = 0; i < FREGS; ++i)
                 o("*reinterpret_cast<d2 *>(sb + (b0 ^ %uu)) = v[%d];\n", xcombo_h(G.st_s, i), i);
