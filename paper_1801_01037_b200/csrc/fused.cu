@@ -578,9 +578,23 @@ static std::vector<PlanPass> plan_lookahead(int n, const svb_op *ops, int nops, 
 // that pass greedily, then plan the following pass greedily too, and keep the
 // first growth that retires the most ops over both passes.  Host-only and
 // run once per circuit (compiled plans are cached).
+static bool rotate_low() {  // SVB_FUSE_ROTATE=0: qubits 0..flow-1 in every tile
+    const char *e = getenv("SVB_FUSE_ROTATE");
+    return !e || atoi(e) != 0;
+}
+
 static std::vector<PlanPass> plan_beam(int n, const svb_op *ops, int nops, int fm) {
     std::vector<PlanPass> passes;
     const uint64_t low = (uint64_t(1) << flow_bits()) - 1;
+    const int nlow = flow_bits();
+    // rotate: the qubits at physical bits 0..flow-1 change from pass to pass
+    // (a pass's store may move any of its qubits there), so a pass needs only
+    // nlow qubits of the previous pass's set -- not nlow fixed qubits
+    const bool rotate = rotate_low();
+    uint64_t anchor = low;  // the set S must share >= nlow qubits with
+    auto room = [&](uint64_t S) {  // tile bits S needs once topped up from the anchor
+        return popc(S) + std::max(0, nlow - popc(S & anchor));
+    };
     std::vector<Blocking> cls(nops);
     for (int i = 0; i < nops; ++i) cls[i] = op_class(ops[i]);
     const int window = 1024;
@@ -611,7 +625,7 @@ static std::vector<PlanPass> plan_beam(int n, const svb_op *ops, int nops, int f
             if (done[i]) continue;
             uint64_t m = op_mask(ops[i]);
             uint64_t add = m & ~p.S;
-            if (hoistable(cls[i], blocked) && add && popc(p.S | m) <= fm &&
+            if (hoistable(cls[i], blocked) && add && room(p.S | m) <= fm &&
                 std::find(out.begin(), out.end(), m) == out.end())
                 out.push_back(m);
             block_add(blocked, cls[i]);
@@ -621,11 +635,11 @@ static std::vector<PlanPass> plan_beam(int n, const svb_op *ops, int nops, int f
     // greedy pass (as plan_lookahead) from `first`, optionally forcing the first growth
     auto greedy = [&](std::vector<char> &done, int first, uint64_t forced) {
         PlanPass p;
-        p.S = low;
+        p.S = rotate ? 0 : low;
         bool forced_used = forced == 0;
         for (;;) {
             absorb(done, first, p, true);
-            if (popc(p.S) >= fm || (int)p.ops.size() >= FMAXG) break;
+            if (room(p.S) >= fm || (int)p.ops.size() >= FMAXG) break;
             uint64_t best = 0;
             if (!forced_used) {
                 best = forced;
@@ -658,7 +672,7 @@ static std::vector<PlanPass> plan_beam(int n, const svb_op *ops, int nops, int f
         // candidate first growths after the free absorb at S = low
         std::vector<char> d0 = done;
         PlanPass p0;
-        p0.S = low;
+        p0.S = rotate ? 0 : low;
         absorb(d0, first, p0, true);
         static const int ncand = getenv("SVB_BEAM_C") ? atoi(getenv("SVB_BEAM_C")) : 12;
         static const int wa = getenv("SVB_BEAM_W") ? atoi(getenv("SVB_BEAM_W")) : 2;
@@ -688,7 +702,11 @@ static std::vector<PlanPass> plan_beam(int n, const svb_op *ops, int nops, int f
             done[first] = 1;
         }
         first = advance(done, first);
+        // top up: anchor qubits first (at least nlow of them), then any
+        for (int q = 0; q < n && popc(p.S & anchor) < nlow; ++q)
+            if ((anchor >> q) & 1) p.S |= uint64_t(1) << q;
         for (int q = 0; q < n && popc(p.S) < fm; ++q) p.S |= uint64_t(1) << q;
+        if (rotate) anchor = p.S;
         passes.push_back(std::move(p));
     }
     return passes;
@@ -758,9 +776,11 @@ struct GateMeta {
 // Thread-bit -> local-bit map for a group: the 3 lowest thread bits (which
 // vary across the 8 lanes of an LDS.128 phase) go to non-slot local bits
 // with distinct (bit mod 3) so the swizzle spreads them over 8 chunks.
+// pref: 3 local bits for lanes 0-2 that make a direct HBM side coalesced
+// (nullptr: none); they win over bank-conflict freedom on the other side.
 static void thread_map(int fm, const int *slots, int8_t *tmap, const int16_t *qcol = nullptr,
                        const int16_t *mcol = nullptr, bool need_ld = false, bool need_st = false,
-                       bool keep012 = false) {
+                       const int *pref = nullptr) {
     bool is_slot[FMMAX] = {};
     for (int i = 0; i < FSLOTS; ++i) is_slot[slots[i]] = true;
     std::vector<int> free_bits;
@@ -795,9 +815,8 @@ static void thread_map(int fm, const int *slots, int8_t *tmap, const int16_t *qc
     auto cost = [&](int a, int b, int c) {
         return (need_ld ? ways(qcol, a, b, c) : 1) + (need_st ? ways(mcol, a, b, c) : 1);
     };
-    // (a first / last group on local bits 0-2 keeps them: direct HBM access wins)
-    const bool direct_pick = order.size() == 3 && order[0] == 0 && order[1] == 1 && order[2] == 2;
-    if (qcol && !(keep012 && direct_pick) && (order.size() < 3 || cost(order[0], order[1], order[2]) > 2)) {
+    if (pref) order = {pref[0], pref[1], pref[2]};
+    if (qcol && !pref && (order.size() < 3 || cost(order[0], order[1], order[2]) > 2)) {
         const int nf = (int)free_bits.size();
         int best = order.size() == 3 ? cost(order[0], order[1], order[2]) : 1 << 20;
         for (int i = 0; i < nf && best > 2; ++i)
@@ -830,25 +849,55 @@ static bool reg_perm_any_ctl() {
 }
 
 // Build the kernel descriptor for one pass; false if it does not fit.
+// Qubit layout: logical qubit q lives at physical index bit phys[q] (nullptr:
+// identity).  A pass tiles over the physical bits of its qubit set S -- which
+// must include physical bits 0..flow-1 (whole 2^flow-amplitude rows) -- and
+// may leave the state in a new layout phys_next that differs only inside S:
+// its last group then stores every register through the extra bit
+// permutation.  Gates name logical qubits; everything on the device is
+// physical.
 static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, bool strict, bool regperm,
-                       int fm) {
+                       int fm, const int8_t *phys = nullptr, const int8_t *phys_next = nullptr) {
     memset(&P, 0, sizeof(P));
     P.flow = flow_bits();
     P.fm = fm;
     const int tbits = fm - FSLOTS;
+    auto ph = [&](int q) { return phys ? (int)phys[q] : q; };
+    auto phn = [&](int q) { return phys_next ? (int)phys_next[q] : ph(q); };
     int local_of[64];
-    int nl = 0, nc = 0;
-    for (int q = 0; q < n; ++q) {
-        if ((pp.S >> q) & 1) {
-            local_of[q] = nl;
-            if (nl >= P.flow) P.rowbit[nl - P.flow] = (int8_t)q;
-            ++nl;
-        } else {
-            local_of[q] = -1;
-            P.comp[nc++] = (int8_t)q;
+    int glob_of[FMMAX];  // local bit -> physical bit
+    {
+        std::vector<std::pair<int, int>> pq;  // (physical bit, logical qubit) of the tile
+        for (int q = 0; q < n; ++q)
+            if ((pp.S >> q) & 1) pq.push_back({ph(q), q});
+        if ((int)pq.size() != fm) return false;
+        std::sort(pq.begin(), pq.end());
+        for (int j = 0; j < P.flow; ++j)
+            if (pq[j].first != j) return false;  // rows must be physical bits 0..flow-1
+        uint64_t tile_phys = 0;
+        for (int q = 0; q < n; ++q) local_of[q] = -1;
+        for (int j = 0; j < fm; ++j) {
+            local_of[pq[j].second] = j;
+            glob_of[j] = pq[j].first;
+            tile_phys |= uint64_t(1) << pq[j].first;
+            if (j >= P.flow) P.rowbit[j - P.flow] = (int8_t)pq[j].first;
         }
+        int nc = 0;
+        for (int b = 0; b < n; ++b)
+            if (!((tile_phys >> b) & 1)) P.comp[nc++] = (int8_t)b;
+        P.ncomp = nc;
     }
-    P.ncomp = nc;
+    // store remap: old local bit of q -> local bit of phn(q) among the same physical bits
+    int sig[FMMAX];
+    bool remap = false;
+    for (int q = 0; q < n; ++q) {
+        if (local_of[q] < 0) continue;
+        int r = 0;
+        while (r < fm && glob_of[r] != phn(q)) ++r;
+        if (r == fm) return false;  // phys_next must permute the tile's own bits
+        sig[local_of[q]] = r;
+        remap |= r != local_of[q];
+    }
     if ((int)pp.ops.size() > FMAXG) return false;
     std::vector<GateMeta> meta;
     for (int oi : pp.ops) {
@@ -964,6 +1013,9 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
                     bool ok = (bits & blocked) == 0 &&
                               (m.perm ? (mode != 0 || inreg)
                                       : (mode != 2 && (bits & g->permq) == 0 && fits(*g, m)));
+                    // a CNOT between local bits 0-2 and the rest, folded into the
+                    // first group's load map, would break its coalesced HBM rows
+                    if (mode == 2 && g == &gps[0] && (bits & 7) && (bits & ~uint64_t(7))) ok = false;
                     if (ok) {
                         take(*g, q, inreg);
                         placed[q] = 1;
@@ -983,6 +1035,18 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
                 if (!scan(1)) break;
             }
         }
+    }
+    if (gps.empty()) new_group();  // a pure layout pass (no gates)
+    if (remap) {  // the last group stores through sigma o P
+        GroupPlan &gl = gps.back();
+        auto sg = [&](int x) {
+            int y = 0;
+            for (int b = 0; b < fm; ++b)
+                if ((x >> b) & 1) y |= 1 << sig[b];
+            return y;
+        };
+        for (int j = 0; j < fm; ++j) gl.mcol[j] = sg(gl.mcol[j]);
+        gl.mb = sg(gl.mb);
     }
     if ((int)gps.size() > FMAXGRP) return false;
     if (getenv("SVB_PLAN_DEBUG") && atoi(getenv("SVB_PLAN_DEBUG")) >= 2) {
@@ -1024,15 +1088,37 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
         // can this group reach HBM directly (see direct_first / direct_last
         // below)?  Then its HBM side needs no bank-friendly lanes, and its
         // lanes 0-2 must stay on local bits 0-2.
-        bool slots_high = !no_direct();
-        for (int k = 0; k < FSLOTS; ++k) slots_high &= slots[k] >= 3;
-        auto low3 = [](const int16_t *col) { return (col[0] >> 3) == 0 && (col[1] >> 3) == 0 && (col[2] >> 3) == 0; };
-        const bool can_df = gi == 0 && slots_high && low3(G.qcol);
-        const bool can_dl = gi == P.ngroups - 1 && slots_high && low3(G.mcol);
+        // Lanes 0-7 of a direct HBM access cover one 128 B line iff lanes 0-2
+        // sit on three non-slot local bits that the group's map sends
+        // (invertibly) into local bits 0-2, i.e. physical bits 0-2.
+        bool is_slot_l[FMMAX] = {};
+        for (int k = 0; k < FSLOTS; ++k) is_slot_l[slots[k]] = true;
+        auto coal = [&](const int16_t *col, int *out) {
+            if (no_direct()) return false;
+            std::vector<int> cand;
+            for (int j = 0; j < fm; ++j)
+                if (!is_slot_l[j] && col[j] != 0 && (col[j] >> 3) == 0) cand.push_back(j);
+            for (size_t a = 0; a < cand.size(); ++a)
+                for (size_t b = a + 1; b < cand.size(); ++b)
+                    for (size_t c = b + 1; c < cand.size(); ++c) {
+                        const int x = col[cand[a]], y = col[cand[b]], z = col[cand[c]];
+                        if (x != y && x != z && y != z && (x ^ y) != z) {
+                            out[0] = cand[a], out[1] = cand[b], out[2] = cand[c];
+                            return true;
+                        }
+                    }
+            return false;
+        };
+        int pf[3], pl[3];
+        const bool cf = gi == 0 && coal(G.qcol, pf);
+        const bool cl = gi == P.ngroups - 1 && coal(G.mcol, pl);
+        const int *pref = cl ? pl : (cf ? pf : nullptr);
+        const bool same = cf && cl && pf[0] == pl[0] && pf[1] == pl[1] && pf[2] == pl[2];
+        const bool can_df = cf && (!cl || same), can_dl = cl;
         // (an uncoalesced first group still reads shared memory when a JIT
         // pass prefetches tiles, so only coalesced direct sides skip the
         // bank-conflict search)
-        thread_map(fm, slots, G.tmap, G.qcol, G.mcol, !can_df, !can_dl, can_df || can_dl);
+        thread_map(fm, slots, G.tmap, G.qcol, G.mcol, !can_df, !can_dl, pref);
         for (int j = 0; j < tbits; ++j) {
             G.ld_t[j] = (uint32_t)(16 * swz(gp.qcol[G.tmap[j]]));
             G.st_t[j] = (uint32_t)(16 * swz(gp.mcol[G.tmap[j]]));
@@ -1113,35 +1199,25 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
     // direct HBM access for the first / last group when the coalescing
     // condition holds: no slot on local bits 0-2, thread bits 0-2 = local bits
     // 0-2, and (last group) a store map that leaves bits 0-2 alone
-    int glob_of[FMMAX];
-    for (int q = 0, b = 0; q < n; ++q)
-        if ((pp.S >> q) & 1) glob_of[b++] = q;
     auto gidx = [&](int l) {
         int64_t g = 0;
         for (int b = 0; b < fm; ++b)
             if ((l >> b) & 1) g |= int64_t(1) << glob_of[b];
         return g;
     };
-    auto coalesced = [&](const FGroup &G) {
-        for (int k = 0; k < FSLOTS; ++k)
-            if (G.pos[k] < 3) return false;
-        return G.tmap[0] == 0 && G.tmap[1] == 1 && G.tmap[2] == 2;
-    };
-    // the 8 lanes of a phase vary local bits 0-2; through an (invertible)
-    // affine map they still cover one 128 B line iff columns 0-2 stay inside
-    // bits 0-2 (other columns may add a per-line constant in bits 0-2)
-    auto low_fixed = [&](const int16_t *col) {
-        for (int j = 0; j < 3; ++j)
-            if (col[j] >> 3) return false;
-        return true;
+    // lanes 0-2 (local bits tmap[0..2]) map into local bits 0-2, invertibly
+    auto coalesced = [&](const FGroup &G, const int16_t *col) {
+        const int x = col[G.tmap[0]], y = col[G.tmap[1]], z = col[G.tmap[2]];
+        if ((x | y | z) >> 3) return false;
+        return x && y && z && x != y && x != z && y != z && (x ^ y) != z;
     };
     const FGroup &G0 = P.groups[0];
-    P.direct_first = (coalesced(G0) && low_fixed(G0.qcol) && !no_direct()) || direct_any();
+    P.direct_first = (coalesced(G0, G0.qcol) && !no_direct()) || direct_any();
     P.gl_b = gidx(G0.qb);
     for (int j = 0; j < tbits; ++j) P.gl_t[j] = gidx(G0.qcol[G0.tmap[j]]);
     for (int k = 0; k < FSLOTS; ++k) P.gl_s[k] = gidx(G0.qcol[G0.pos[k]]);
     const FGroup &GL = P.groups[P.ngroups - 1];
-    P.direct_last = (coalesced(GL) && low_fixed(GL.mcol) && !no_direct()) || direct_any();
+    P.direct_last = (coalesced(GL, GL.mcol) && !no_direct()) || direct_any();
     P.gs_b = gidx(GL.mb);
     for (int j = 0; j < tbits; ++j) P.gs_t[j] = gidx(GL.mcol[GL.tmap[j]]);
     for (int k = 0; k < FSLOTS; ++k) P.gs_s[k] = gidx(GL.mcol[GL.pos[k]]);
@@ -1157,7 +1233,8 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
             }
             return w;
         };
-        fprintf(stderr, "  banks: df %d dl %d |", P.direct_first, P.direct_last);
+        fprintf(stderr, "  banks: df %d dl %d coal %d %d |", P.direct_first, P.direct_last,
+                (int)coalesced(G0, G0.qcol), (int)coalesced(GL, GL.mcol));
         for (int gi = 0; gi < P.ngroups; ++gi) {
             const FGroup &G = P.groups[gi];
             const bool ld_smem = !(gi == 0 && P.direct_first), st_smem = !(gi == P.ngroups - 1 && P.direct_last);
@@ -1199,14 +1276,180 @@ static int plan_fm(int n, unsigned flags) {
     return std::max(FM, std::min(FMMAX, fm));
 }
 
+struct PlanStep {
+    int op;      // >= 0: run `mapped` (ops[op] on physical qubits) with the single-gate kernels
+    svb_op mapped;
+    // -1: next fused pass
+};
+
+// Plan an op list and lower it to steps + pass descriptors, tracking the
+// qubit layout: non-strict plans let each pass move three qubits of the next
+// pass's set to physical bits 0-2 (so no qubit is pinned into every tile:
+// configs[1] 203 -> 170 passes at fm 12), the others of its set go home
+// when they can, and gate-free layout passes at the end restore the
+// identity layout the caller expects.
+static void lower_plan(int n, const svb_op *ops, int nops, bool strict, bool regperm, int fm,
+                       std::vector<PlanStep> &steps, std::vector<FPass> &passes) {
+    const std::vector<PlanPass> plans = plan(n, ops, nops, strict, fm);
+    const int nlow = flow_bits();
+    const bool rotate = !strict && rotate_low() && planner_kind() == 3;
+    std::vector<int8_t> phys(64), nxt(64);
+    for (int q = 0; q < 64; ++q) phys[q] = (int8_t)q;
+    auto single = [&](int oi) {
+        PlanStep st;
+        st.op = oi;
+        st.mapped = ops[oi];
+        st.mapped.target = phys[ops[oi].target];
+        if (ops[oi].kind == 1) st.mapped.control = phys[ops[oi].control];
+        steps.push_back(st);
+    };
+    auto fused = [&](const PlanPass &pp, const int8_t *next) {
+        FPass P;
+        if (!build_pass(n, ops, pp, P, strict, regperm, fm, phys.data(), next)) return false;
+        PlanStep st;
+        st.op = -1;
+        memset(&st.mapped, 0, sizeof st.mapped);
+        steps.push_back(st);
+        passes.push_back(P);
+        if (next) phys.assign(next, next + 64);
+        return true;
+    };
+    for (size_t k = 0; k < plans.size(); ++k) {
+        const PlanPass &pp = plans[k];
+        // (with a rotating layout even a one-op pass runs as a tile pass: it
+        // is the pass that brings the next pass's qubits to bits 0-2)
+        if (pp.ops.size() <= 1 && !rotate) {
+            for (int oi : pp.ops) single(oi);
+            continue;
+        }
+        const int8_t *next = nullptr;
+        if (rotate) {
+            // new physical bits 0..nlow-1: nlow qubits of this set that the next
+            // pass also tiles (the planner guarantees >= nlow), those already
+            // low first; among the choices, the first whose last-group store
+            // stays coalesced (its lanes need the new low qubits off the slots)
+            const uint64_t want = k + 1 < plans.size() ? (pp.S & plans[k + 1].S) : (pp.S & ((1ull << nlow) - 1));
+            std::vector<int> pool;
+            for (int pass2 = 0; pass2 < 2; ++pass2)
+                for (int q = 0; q < n; ++q)
+                    if (((want >> q) & 1) && ((phys[q] < nlow) == (pass2 == 0))) pool.push_back(q);
+            for (int q = 0; q < n && (int)pool.size() < nlow; ++q)  // (last pass: any current low qubit)
+                if (((pp.S >> q) & 1) && phys[q] < nlow && std::find(pool.begin(), pool.end(), q) == pool.end())
+                    pool.push_back(q);
+            std::vector<std::vector<int>> choices;
+            const int np = (int)pool.size();
+            for (int a = 0; a < np && choices.size() < 24; ++a)
+                for (int b = a + 1; b < np && choices.size() < 24; ++b)
+                    for (int c = b + 1; c < np && choices.size() < 24; ++c)
+                        if (nlow == 3) choices.push_back({pool[a], pool[b], pool[c]});
+            if (choices.empty()) choices.push_back(std::vector<int>(pool.begin(), pool.begin() + std::min(np, nlow)));
+            bool built = false;
+            for (size_t ci = 0; ci < choices.size() && !built; ++ci) {
+            const std::vector<int> &lowq = choices[ci];
+            nxt = phys;
+            uint64_t T = 0;  // the tile's physical bits
+            for (int q = 0; q < n; ++q)
+                if ((pp.S >> q) & 1) T |= uint64_t(1) << phys[q];
+            uint64_t taken = 0;
+            std::vector<int> rest;
+            for (int q : lowq)  // already-low ones keep their bit
+                if (phys[q] < nlow) taken |= uint64_t(1) << phys[q];
+            for (int q : lowq)
+                if (phys[q] >= nlow) {
+                    int b = 0;
+                    while ((taken >> b) & 1) ++b;
+                    nxt[q] = (int8_t)b;
+                    taken |= uint64_t(1) << b;
+                }
+            for (int q = 0; q < n; ++q) {
+                if (!((pp.S >> q) & 1) || std::find(lowq.begin(), lowq.end(), q) != lowq.end()) continue;
+                if (q >= nlow && ((T >> q) & 1) && !((taken >> q) & 1)) {
+                    nxt[q] = (int8_t)q;  // home
+                    taken |= uint64_t(1) << q;
+                } else {
+                    rest.push_back(q);
+                }
+            }
+            for (int q : rest) {
+                int b = 0;
+                while (!((T >> b) & 1) || ((taken >> b) & 1)) ++b;
+                nxt[q] = (int8_t)b;
+                taken |= uint64_t(1) << b;
+            }
+            FPass P;
+            if (!build_pass(n, ops, pp, P, strict, regperm, fm, phys.data(), nxt.data())) continue;
+            const FGroup &GL = P.groups[P.ngroups - 1];
+            int lanes = 0;  // store columns of lanes 0-2 span local bits 0-2?
+            for (int b = 0; b < 3; ++b) lanes |= GL.mcol[GL.tmap[b]];
+            const bool coal = lanes == 7 && !((GL.mcol[GL.tmap[0]] | GL.mcol[GL.tmap[1]] | GL.mcol[GL.tmap[2]]) >> 3);
+            if (!coal && ci + 1 < choices.size()) continue;
+            PlanStep st;
+            st.op = -1;
+            memset(&st.mapped, 0, sizeof st.mapped);
+            steps.push_back(st);
+            passes.push_back(P);
+            phys = nxt;
+            built = true;
+            }
+            if (!built)
+                for (int oi : pp.ops) single(oi);
+            continue;
+        }
+        if (!fused(pp, next))
+            for (int oi : pp.ops) single(oi);
+    }
+    // restore the identity layout with gate-free passes
+    for (int guard = 0; guard < 64; ++guard) {
+        std::vector<int> inv(n);
+        uint64_t disp = 0;
+        for (int q = 0; q < n; ++q) {
+            inv[phys[q]] = q;
+            if (phys[q] != q) disp |= uint64_t(1) << phys[q];
+        }
+        if (!disp) break;
+        uint64_t T = (uint64_t(1) << nlow) - 1;
+        // whole cycles while they fit, then a segment of the next one
+        for (int p0 = 0; p0 < n && popc(T) < fm; ++p0) {
+            if (!((disp >> p0) & 1) || ((T >> p0) & 1 && p0 >= nlow)) continue;
+            for (int p = p0; popc(T) < fm; p = inv[p]) {
+                T |= uint64_t(1) << p;
+                if (inv[p] == p0) break;
+            }
+        }
+        for (int b = n - 1; b >= 0 && popc(T) < fm; --b) T |= uint64_t(1) << b;
+        PlanPass pp;
+        for (int b = 0; b < n; ++b)
+            if ((T >> b) & 1) pp.S |= uint64_t(1) << inv[b];
+        nxt = phys;
+        uint64_t taken = 0;
+        std::vector<int> rest;
+        for (int b = 0; b < n; ++b) {
+            if (!((T >> b) & 1)) continue;
+            const int q = inv[b];
+            if ((T >> q) & 1) {
+                nxt[q] = (int8_t)q;
+                taken |= uint64_t(1) << q;
+            } else {
+                rest.push_back(q);
+            }
+        }
+        for (int q : rest) {
+            int b = 0;
+            while (!((T >> b) & 1) || ((taken >> b) & 1)) ++b;
+            nxt[q] = (int8_t)b;
+            taken |= uint64_t(1) << b;
+        }
+        if (!fused(pp, nxt.data())) break;  // cannot happen: a gate-free pass always builds
+    }
+}
+
 // host-only: plan, lower and NVRTC-compile every fused pass (no device work)
 int jit_check(int n, const svb_op *ops, int nops, unsigned flags) {
     const bool strict = flags & SVB_RUN_STRICT_ORDER;
     std::vector<FPass> passes;
-    FPass P;
+    std::vector<PlanStep> steps;
     const int fm = plan_fm(n, flags | SVB_RUN_JIT);
-    for (const PlanPass &pp : plan(n, ops, nops, strict, fm))
-        if (pp.ops.size() > 1 && build_pass(n, ops, pp, P, strict, reg_perm(flags), fm)) passes.push_back(P);
+    lower_plan(n, ops, nops, strict, reg_perm(flags), fm, steps, passes);
     std::string err;
     int r = jit_compile_only(passes, jit_variant((flags & SVB_RUN_FMA) && !strict), err);
     if (r < 0) set_error("jit compile failed: %.400s", err.c_str());
@@ -1218,31 +1461,33 @@ int plan_passes(int n, const svb_op *ops, int nops, unsigned flags, int *groups)
     if (!fuse_enabled(n, flags)) return nops;
     const bool strict = flags & SVB_RUN_STRICT_ORDER;
     const int fm = plan_fm(n, flags);
-    auto passes = plan(n, ops, nops, strict, fm);
-    if (groups) {
-        FPass P;
-        int df = 0, dl = 0, nf = 0;
-        for (const PlanPass &pp : passes)
-            if (pp.ops.size() > 1 && build_pass(n, ops, pp, P, strict, reg_perm(flags), fm)) {
-                *groups += P.ngroups;
-                df += P.direct_first;
-                dl += P.direct_last;
-                ++nf;
-            }
-        if (getenv("SVB_PLAN_DEBUG"))
-            fprintf(stderr, "plan: %zu passes (%d fused), %d groups, direct first %d, direct last %d\n",
-                    passes.size(), nf, *groups, df, dl);
+    std::vector<FPass> passes;
+    std::vector<PlanStep> steps;
+    lower_plan(n, ops, nops, strict, reg_perm(flags), fm, steps, passes);
+    int df = 0, dl = 0, cf = 0, cl = 0;
+    auto coal = [](const FGroup &G, const int16_t *col) {
+        const int x = col[G.tmap[0]], y = col[G.tmap[1]], z = col[G.tmap[2]];
+        return !((x | y | z) >> 3) && (x | y | z) == 7 && x != y && x != z && y != z && (x ^ y) != z;
+    };
+    for (const FPass &P : passes) {
+        if (groups) *groups += P.ngroups;
+        df += P.direct_first;
+        dl += P.direct_last;
+        cf += coal(P.groups[0], P.groups[0].qcol);
+        cl += coal(P.groups[P.ngroups - 1], P.groups[P.ngroups - 1].mcol);
     }
-    return (int)passes.size();
+    if (getenv("SVB_PLAN_DEBUG"))
+        fprintf(stderr,
+                "plan: %zu steps (%zu fused passes), %d groups, direct first %d (coalesced %d), "
+                "direct last %d (coalesced %d)\n",
+                steps.size(), passes.size(), groups ? *groups : -1, df, cf, dl, cl);
+    return (int)steps.size();
 }
 
 // ---------------------------------------------------------------------------
 // compiled plans, cached: a circuit run repeatedly (bench steps, parameter
 // sweeps) is planned and lowered to kernel descriptors once.
 
-struct PlanStep {
-    int op;  // >= 0: run ops[op] with the single-gate kernels; -1: next fused pass
-};
 struct CompiledPlan {
     int n, fm;
     bool strict, regperm;
@@ -1294,15 +1539,7 @@ static std::shared_ptr<const CompiledPlan> compiled_plan(int n, const svb_op *op
     cp->strict = strict;
     cp->regperm = regperm;
     cp->ops.assign(ops, ops + nops);
-    FPass P;
-    for (const PlanPass &pp : plan(n, ops, nops, strict, fm)) {
-        if (pp.ops.size() > 1 && build_pass(n, ops, pp, P, strict, regperm, fm)) {
-            cp->steps.push_back(PlanStep{-1});
-            cp->passes.push_back(P);
-        } else {
-            for (int oi : pp.ops) cp->steps.push_back(PlanStep{oi});
-        }
-    }
+    lower_plan(n, ops, nops, strict, regperm, fm, cp->steps, cp->passes);
     // Bounded by descriptor bytes (~27 KiB per pass), not by count: the
     // multi-process engine runs one op segment per exchange interval, so a
     // circuit step may cycle through hundreds of small plans.
@@ -1356,7 +1593,7 @@ int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsi
     }
     for (const PlanStep &st : cp->steps) {
         if (st.op >= 0) {
-            single(ops[st.op]);
+            single(st.mapped);
             continue;
         }
         const size_t pi = next_pass++;
