@@ -1221,27 +1221,6 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
     P.gs_b = gidx(GL.mb);
     for (int j = 0; j < tbits; ++j) P.gs_t[j] = gidx(GL.mcol[GL.tmap[j]]);
     for (int k = 0; k < FSLOTS; ++k) P.gs_s[k] = gidx(GL.mcol[GL.pos[k]]);
-    if (getenv("SVB_PLAN_DEBUG") && atoi(getenv("SVB_PLAN_DEBUG")) >= 3) {
-        // shared-memory wavefronts per LDS/STS.128 phase of 8 lanes (1 = conflict-free)
-        auto ways = [](const uint32_t *t) {
-            int seen[8] = {0}, w = 0;
-            for (int l = 0; l < 8; ++l) {
-                unsigned a = 0;
-                for (int j = 0; j < 3; ++j)
-                    if ((l >> j) & 1) a ^= t[j];
-                w = std::max(w, ++seen[(a >> 4) & 7]);
-            }
-            return w;
-        };
-        fprintf(stderr, "  banks: df %d dl %d coal %d %d |", P.direct_first, P.direct_last,
-                (int)coalesced(G0, G0.qcol), (int)coalesced(GL, GL.mcol));
-        for (int gi = 0; gi < P.ngroups; ++gi) {
-            const FGroup &G = P.groups[gi];
-            const bool ld_smem = !(gi == 0 && P.direct_first), st_smem = !(gi == P.ngroups - 1 && P.direct_last);
-            fprintf(stderr, " g%d ld %d st %d", gi, ld_smem ? ways(G.ld_t) : 0, st_smem ? ways(G.st_t) : 0);
-        }
-        fprintf(stderr, "\n");
-    }
     return true;
 }
 
@@ -1281,6 +1260,18 @@ struct PlanStep {
     svb_op mapped;
     // -1: next fused pass
 };
+
+// shared-memory wavefronts of one 8-lane LDS/STS.128 phase (1 = conflict-free)
+static int phase_ways(const uint32_t *t) {
+    int seen[8] = {0}, w = 0;
+    for (int l = 0; l < 8; ++l) {
+        unsigned a = 0;
+        for (int j = 0; j < 3; ++j)
+            if ((l >> j) & 1) a ^= t[j];
+        w = std::max(w, ++seen[(a >> 4) & 7]);
+    }
+    return w;
+}
 
 // Plan an op list and lower it to steps + pass descriptors, tracking the
 // qubit layout: non-strict plans let each pass move three qubits of the next
@@ -1344,7 +1335,10 @@ static void lower_plan(int n, const svb_op *ops, int nops, bool strict, bool reg
                         if (nlow == 3) choices.push_back({pool[a], pool[b], pool[c]});
             if (choices.empty()) choices.push_back(std::vector<int>(pool.begin(), pool.begin() + std::min(np, nlow)));
             bool built = false;
-            for (size_t ci = 0; ci < choices.size() && !built; ++ci) {
+            FPass best;
+            std::vector<int8_t> best_next;
+            int best_score = 1 << 20;
+            for (size_t ci = 0; ci < choices.size() && best_score > 0; ++ci) {
             const std::vector<int> &lowq = choices[ci];
             nxt = phys;
             uint64_t T = 0;  // the tile's physical bits
@@ -1378,21 +1372,31 @@ static void lower_plan(int n, const svb_op *ops, int nops, bool strict, bool reg
             }
             FPass P;
             if (!build_pass(n, ops, pp, P, strict, regperm, fm, phys.data(), nxt.data())) continue;
+            // score: uncoalesced last-group HBM store (2) + shared-memory
+            // conflicts of the last group's loads and the groups' stores
             const FGroup &GL = P.groups[P.ngroups - 1];
-            int lanes = 0;  // store columns of lanes 0-2 span local bits 0-2?
-            for (int b = 0; b < 3; ++b) lanes |= GL.mcol[GL.tmap[b]];
-            const bool coal = lanes == 7 && !((GL.mcol[GL.tmap[0]] | GL.mcol[GL.tmap[1]] | GL.mcol[GL.tmap[2]]) >> 3);
-            if (!coal && ci + 1 < choices.size()) continue;
-            PlanStep st;
-            st.op = -1;
-            memset(&st.mapped, 0, sizeof st.mapped);
-            steps.push_back(st);
-            passes.push_back(P);
-            phys = nxt;
-            built = true;
+            const int x = GL.mcol[GL.tmap[0]], y = GL.mcol[GL.tmap[1]], z = GL.mcol[GL.tmap[2]];
+            const bool coal = !((x | y | z) >> 3) && (x | y | z) == 7 && x != y && x != z && y != z && (x ^ y) != z;
+            int score = coal ? 0 : 2;
+            score += phase_ways(GL.ld_t) - 1;
+            for (int gi = 0; gi + 1 < P.ngroups; ++gi) score += phase_ways(P.groups[gi].st_t) - 1;
+            if (score < best_score) {
+                best_score = score;
+                best = P;
+                best_next = nxt;
+                built = true;
             }
-            if (!built)
+            }
+            if (built) {
+                PlanStep st;
+                st.op = -1;
+                memset(&st.mapped, 0, sizeof st.mapped);
+                steps.push_back(st);
+                passes.push_back(best);
+                phys = best_next;
+            } else {
                 for (int oi : pp.ops) single(oi);
+            }
             continue;
         }
         if (!fused(pp, next))
@@ -1469,12 +1473,34 @@ int plan_passes(int n, const svb_op *ops, int nops, unsigned flags, int *groups)
         const int x = col[G.tmap[0]], y = col[G.tmap[1]], z = col[G.tmap[2]];
         return !((x | y | z) >> 3) && (x | y | z) == 7 && x != y && x != z && y != z && (x ^ y) != z;
     };
+    const bool dbg3 = getenv("SVB_PLAN_DEBUG") && atoi(getenv("SVB_PLAN_DEBUG")) >= 3;
+    auto ways = [](const uint32_t *t) {  // wavefronts per LDS/STS.128 phase of 8 lanes (1 = conflict-free)
+        int seen[8] = {0}, w = 0;
+        for (int l = 0; l < 8; ++l) {
+            unsigned a = 0;
+            for (int j = 0; j < 3; ++j)
+                if ((l >> j) & 1) a ^= t[j];
+            w = std::max(w, ++seen[(a >> 4) & 7]);
+        }
+        return w;
+    };
     for (const FPass &P : passes) {
         if (groups) *groups += P.ngroups;
         df += P.direct_first;
         dl += P.direct_last;
-        cf += coal(P.groups[0], P.groups[0].qcol);
-        cl += coal(P.groups[P.ngroups - 1], P.groups[P.ngroups - 1].mcol);
+        const bool c0 = coal(P.groups[0], P.groups[0].qcol), c1 = coal(P.groups[P.ngroups - 1], P.groups[P.ngroups - 1].mcol);
+        cf += c0;
+        cl += c1;
+        if (dbg3) {
+            fprintf(stderr, "pass: %d gates, %d groups, coalesced %d %d | banks:", P.ngates, P.ngroups, c0, c1);
+            for (int gi = 0; gi < P.ngroups; ++gi) {
+                const FGroup &G = P.groups[gi];
+                // JIT passes with prefetch read group 0 from shared memory too
+                const bool st_smem = !(gi == P.ngroups - 1 && P.direct_last);
+                fprintf(stderr, " g%d ld %d st %d", gi, ways(G.ld_t), st_smem ? ways(G.st_t) : 0);
+            }
+            fprintf(stderr, "\n");
+        }
     }
     if (getenv("SVB_PLAN_DEBUG"))
         fprintf(stderr,
