@@ -36,6 +36,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -1048,6 +1049,37 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
         for (int j = 0; j < fm; ++j) gl.mcol[j] = sg(gl.mcol[j]);
         gl.mb = sg(gl.mb);
     }
+    // The last group stores straight to HBM; its rows stay whole 128 B lines
+    // only if three non-slot local bits map (invertibly) onto local bits 0-2.
+    // When its gate targets occupy them, a gate-free group is appended to
+    // carry the store map: one more shared-memory transition (conflict-free)
+    // costs less than uncoalesced HBM stores.
+    auto low_cands = [&](const GroupPlan &g, std::vector<int> &out) {
+        out.clear();
+        for (int j = 0; j < fm; ++j)
+            if (g.mcol[j] && !(g.mcol[j] >> 3) &&
+                std::find(g.slots.begin(), g.slots.end(), j) == g.slots.end())
+                out.push_back(j);
+        for (size_t a = 0; a < out.size(); ++a)
+            for (size_t b = a + 1; b < out.size(); ++b)
+                for (size_t c = b + 1; c < out.size(); ++c) {
+                    const int x = g.mcol[out[a]], y = g.mcol[out[b]], z = g.mcol[out[c]];
+                    if (x != y && x != z && y != z && (x ^ y) != z) return true;
+                }
+        return false;
+    };
+    {
+        std::vector<int> cands;
+        if (!strict && !no_direct() && !gps.back().gates.empty() && !low_cands(gps.back(), cands)) {
+            GroupPlan &gl = gps.back();
+            int mcol[FMMAX], mb = gl.mb;
+            for (int j = 0; j < fm; ++j) mcol[j] = gl.mcol[j], gl.mcol[j] = 1 << j;
+            gl.mb = 0;
+            GroupPlan *g2 = new_group();
+            for (int j = 0; j < fm; ++j) g2->mcol[j] = mcol[j];
+            g2->mb = mb;
+        }
+    }
     if ((int)gps.size() > FMAXGRP) return false;
     if (getenv("SVB_PLAN_DEBUG") && atoi(getenv("SVB_PLAN_DEBUG")) >= 2) {
         int nperm = 0;
@@ -1067,11 +1099,19 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
         int slots[FSLOTS];
         int ns = 0;
         for (int s : gp.slots) slots[ns++] = s;
-        for (int b = fm - 1; ns < FSLOTS && b >= 0; --b) {
-            bool used = false;
-            for (int i = 0; i < ns; ++i) used |= slots[i] == b;
-            if (!used) slots[ns++] = b;
-        }
+        // fill the free slots from the top, keeping off the local bits a
+        // coalesced direct access needs as lanes (first group: bits 0-2; last
+        // group: the bits its store map sends to 0-2)
+        auto lane_bit = [&](int b) {
+            if (gi == 0 && b < 3) return true;
+            return gi == (int)gps.size() - 1 && gp.mcol[b] && !(gp.mcol[b] >> 3);
+        };
+        for (int pass2 = 0; pass2 < 2; ++pass2)
+            for (int b = fm - 1; ns < FSLOTS && b >= 0; --b) {
+                bool used = false;
+                for (int i = 0; i < ns; ++i) used |= slots[i] == b;
+                if (!used && (pass2 == 1 || !lane_bit(b))) slots[ns++] = b;
+            }
         std::sort(slots, slots + FSLOTS);
         FGroup &G = P.groups[gi];
         for (int i = 0; i < FSLOTS; ++i) G.pos[i] = (int8_t)slots[i];
@@ -1118,17 +1158,13 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
         // (an uncoalesced first group still reads shared memory when a JIT
         // pass prefetches tiles, so only coalesced direct sides skip the
         // bank-conflict search)
-        thread_map(fm, slots, G.tmap, G.qcol, G.mcol, !can_df, !can_dl, pref);
-        for (int j = 0; j < tbits; ++j) {
-            G.ld_t[j] = (uint32_t)(16 * swz(gp.qcol[G.tmap[j]]));
-            G.st_t[j] = (uint32_t)(16 * swz(gp.mcol[G.tmap[j]]));
-        }
-        for (int k = 0; k < FSLOTS; ++k) {
-            G.ld_s[k] = (uint32_t)(16 * swz(gp.qcol[slots[k]]));
-            G.st_s[k] = (uint32_t)(16 * swz(gp.mcol[slots[k]]));
-        }
-        G.ld_b = (uint32_t)(16 * swz(gp.qb));
-        G.st_b = (uint32_t)(16 * swz(gp.mb));
+        // Only the shared-memory sides that use the fixed swizzle constrain
+        // the lanes here -- group 0's loads (tiles filled by cp.async) and an
+        // indirect last store; every transition between two groups gets its
+        // own swizzle below.
+        (void)can_df;
+        (void)can_dl;
+        thread_map(fm, slots, G.tmap, G.qcol, G.mcol, gi == 0, gi == P.ngroups - 1 && !direct_any(), pref);
         auto slot_of = [&](int l) {
             for (int i = 0; i < FSLOTS; ++i)
                 if (slots[i] == l) return i;
@@ -1195,6 +1231,72 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
         k0 += (int)gp.gates.size();
     }
     P.ngates = k0;
+
+    // Shared-memory swizzle per transition.  A swizzle adds to a local index's
+    // 16 B chunk number (bits 0-2) an XOR-linear function H of its higher
+    // bits; any H is invertible.  The fill (cp.async) and the final copy use
+    // the fixed fold3 one (H[j] = 1 << j % 3); between groups g and g+1 the
+    // buffer is rewritten anyway, so H is searched such that g's STS.128 and
+    // g+1's LDS.128 phases both hit 8 distinct bank groups.
+    {
+        const int G = P.ngroups;
+        std::vector<std::array<int, FMMAX>> H(G + 1);  // H[t]: transition into group t (t = G: final copy)
+        std::array<int, FMMAX> fold{};
+        for (int j = 3; j < fm; ++j) fold[j] = 1 << (j % 3);
+        auto bank = [&](int v, const std::array<int, FMMAX> &h) {
+            int c = v & 7;
+            for (int j = 3; j < fm; ++j)
+                if ((v >> j) & 1) c ^= h[j];
+            return c;
+        };
+        auto ways3 = [&](int a, int b, int c) {  // wavefronts of the 8-lane phase spanned by banks a, b, c
+            int seen[8] = {0}, w = 0;
+            for (int l = 0; l < 8; ++l) w = std::max(w, ++seen[((l & 1) ? a : 0) ^ ((l & 2) ? b : 0) ^ ((l & 4) ? c : 0)]);
+            return w;
+        };
+        H[0] = fold;
+        H[G] = fold;
+        uint32_t rng = 0x9e3779b9u;
+        for (int t = 1; t < G; ++t) {
+            const FGroup &A = P.groups[t - 1], &B = P.groups[t];
+            auto cost = [&](const std::array<int, FMMAX> &h) {
+                return ways3(bank(A.mcol[A.tmap[0]], h), bank(A.mcol[A.tmap[1]], h), bank(A.mcol[A.tmap[2]], h)) +
+                       ways3(bank(B.qcol[B.tmap[0]], h), bank(B.qcol[B.tmap[1]], h), bank(B.qcol[B.tmap[2]], h));
+            };
+            std::array<int, FMMAX> best = fold;
+            int bc = cost(fold);
+            for (int tries = 0; tries < 400 && bc > 2; ++tries) {
+                std::array<int, FMMAX> h{};
+                for (int j = 3; j < fm; ++j) {
+                    rng = rng * 1664525u + 1013904223u;
+                    h[j] = (rng >> 29) & 7;
+                }
+                const int c = cost(h);
+                if (c < bc) {
+                    bc = c;
+                    best = h;
+                }
+            }
+            H[t] = best;
+        }
+        auto off = [&](int v, const std::array<int, FMMAX> &h) {
+            return (uint32_t)(16 * ((v & ~7) | bank(v, h)));
+        };
+        for (int gi = 0; gi < G; ++gi) {
+            FGroup &Gr = P.groups[gi];
+            const auto &hin = H[gi], &hout = H[gi + 1];
+            for (int j = 0; j < tbits; ++j) {
+                Gr.ld_t[j] = off(Gr.qcol[Gr.tmap[j]], hin);
+                Gr.st_t[j] = off(Gr.mcol[Gr.tmap[j]], hout);
+            }
+            for (int k = 0; k < FSLOTS; ++k) {
+                Gr.ld_s[k] = off(Gr.qcol[Gr.pos[k]], hin);
+                Gr.st_s[k] = off(Gr.mcol[Gr.pos[k]], hout);
+            }
+            Gr.ld_b = off(Gr.qb, hin);
+            Gr.st_b = off(Gr.mb, hout);
+        }
+    }
 
     // direct HBM access for the first / last group when the coalescing
     // condition holds: no slot on local bits 0-2, thread bits 0-2 = local bits
@@ -1338,7 +1440,7 @@ static void lower_plan(int n, const svb_op *ops, int nops, bool strict, bool reg
             FPass best;
             std::vector<int8_t> best_next;
             int best_score = 1 << 20;
-            for (size_t ci = 0; ci < choices.size() && best_score > 0; ++ci) {
+            for (size_t ci = 0; ci < choices.size(); ++ci) {
             const std::vector<int> &lowq = choices[ci];
             nxt = phys;
             uint64_t T = 0;  // the tile's physical bits
@@ -1377,7 +1479,9 @@ static void lower_plan(int n, const svb_op *ops, int nops, bool strict, bool reg
             const FGroup &GL = P.groups[P.ngroups - 1];
             const int x = GL.mcol[GL.tmap[0]], y = GL.mcol[GL.tmap[1]], z = GL.mcol[GL.tmap[2]];
             const bool coal = !((x | y | z) >> 3) && (x | y | z) == 7 && x != y && x != z && y != z && (x ^ y) != z;
-            int score = coal ? 0 : 2;
+            // (a gate-free last group was appended when the store could not
+            // be coalesced otherwise: fewer groups first)
+            int score = 4 * P.ngroups + (coal ? 0 : 2);
             score += phase_ways(GL.ld_t) - 1;
             for (int gi = 0; gi + 1 < P.ngroups; ++gi) score += phase_ways(P.groups[gi].st_t) - 1;
             if (score < best_score) {

@@ -3,5 +3,6 @@ run() {
   env $1 timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu --no-sweep $3 > gpurun_out/$2.json 2> gpurun_out/$2.err
   python -c "import json;d=json.load(open('gpurun_out/$2.json'));r=d['roofline'];print('$2',d['value'],d['e2e']['value'],r['achieved'],r['avg_launch_ms'],r['launches'],d['config']['hbm_passes_per_step'],d['check'])" || tail -5 gpurun_out/$2.err
 }
-run "X=1" rotate
-run "SVB_FUSE_ROTATE=0" norot
+run "X=1" default
+run "X=1" interp --no-jit
+bash tools/pass_fit.sh
