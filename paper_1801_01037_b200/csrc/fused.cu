@@ -148,9 +148,11 @@ __device__ __forceinline__ void diag_gate(double2 (&v)[FREGS], const FGate &fg, 
     }
 }
 
+#define SVB_OPND(K, S, C) (((K) * FSMAX + (S)) * 2 + (C))
+#define SVB_OPDG(V, T, C) (FOP_DIAG + ((V) * (FSMAX + 1) + (T)) * 2 + (C))
 #define SVB_ND2(K, S) \
-    case ((K)*FSLOTS + (S)) * 2 + 0: nd_gate<K, S, 0, FMA>(v, fg); break; \
-    case ((K)*FSLOTS + (S)) * 2 + 1: nd_gate<K, S, 1, FMA>(v, fg); break;
+    case SVB_OPND(K, S, 0): nd_gate<K, S, 0, FMA>(v, fg); break; \
+    case SVB_OPND(K, S, 1): nd_gate<K, S, 1, FMA>(v, fg); break;
 #if SVB_FSLOTS == 5
 #define SVB_ND(K) SVB_ND2(K, 0) SVB_ND2(K, 1) SVB_ND2(K, 2) SVB_ND2(K, 3) SVB_ND2(K, 4)
 #elif SVB_FSLOTS == 4
@@ -159,14 +161,18 @@ __device__ __forceinline__ void diag_gate(double2 (&v)[FREGS], const FGate &fg, 
 #define SVB_ND(K) SVB_ND2(K, 0) SVB_ND2(K, 1) SVB_ND2(K, 2)
 #endif
 #define SVB_DG2(V, T) \
-    case FOP_DIAG + ((V) * (FSLOTS + 1) + (T)) * 2 + 0: diag_gate<V, T, 0, FMA>(v, fg, l0); break; \
-    case FOP_DIAG + ((V) * (FSLOTS + 1) + (T)) * 2 + 1: diag_gate<V, T, 1, FMA>(v, fg, l0); break;
+    case SVB_OPDG(V, T, 0): diag_gate<V, T, 0, FMA>(v, fg, l0); break; \
+    case SVB_OPDG(V, T, 1): diag_gate<V, T, 1, FMA>(v, fg, l0); break;
+// target on a thread bit: encoded tpos FTPOS_THREAD, the kernel's TP = FSLOTS
+#define SVB_DGT(V) \
+    case SVB_OPDG(V, FTPOS_THREAD, 0): diag_gate<V, FSLOTS, 0, FMA>(v, fg, l0); break; \
+    case SVB_OPDG(V, FTPOS_THREAD, 1): diag_gate<V, FSLOTS, 1, FMA>(v, fg, l0); break;
 #if SVB_FSLOTS == 5
-#define SVB_DG(V) SVB_DG2(V, 0) SVB_DG2(V, 1) SVB_DG2(V, 2) SVB_DG2(V, 3) SVB_DG2(V, 4) SVB_DG2(V, 5)
+#define SVB_DG(V) SVB_DG2(V, 0) SVB_DG2(V, 1) SVB_DG2(V, 2) SVB_DG2(V, 3) SVB_DG2(V, 4) SVB_DGT(V)
 #elif SVB_FSLOTS == 4
-#define SVB_DG(V) SVB_DG2(V, 0) SVB_DG2(V, 1) SVB_DG2(V, 2) SVB_DG2(V, 3) SVB_DG2(V, 4)
+#define SVB_DG(V) SVB_DG2(V, 0) SVB_DG2(V, 1) SVB_DG2(V, 2) SVB_DG2(V, 3) SVB_DGT(V)
 #else
-#define SVB_DG(V) SVB_DG2(V, 0) SVB_DG2(V, 1) SVB_DG2(V, 2) SVB_DG2(V, 3)
+#define SVB_DG(V) SVB_DG2(V, 0) SVB_DG2(V, 1) SVB_DG2(V, 2) SVB_DGT(V)
 #endif
 
 // Register-permuting ops (X, Y, unit phases) as their own cases make every
@@ -191,8 +197,8 @@ __device__ __forceinline__ void run_gate(double2 (&v)[FREGS], const FGate &fg, i
 #if SVB_COMPACT_DISPATCH
         // controlled arithmetic gates all take the general arm (exact for every
         // matrix class); uncontrolled ones get their specialised arm
-#define SVB_NDU(K, S) case ((K)*FSLOTS + (S)) * 2 + 0: nd_gate<K, S, 0, FMA>(v, fg); break;
-#define SVB_NDC(S) case ((FK_GENERAL)*FSLOTS + (S)) * 2 + 1: nd_gate<FK_GENERAL, S, 1, FMA>(v, fg); break;
+#define SVB_NDU(K, S) case SVB_OPND(K, S, 0): nd_gate<K, S, 0, FMA>(v, fg); break;
+#define SVB_NDC(S) case SVB_OPND(FK_GENERAL, S, 1): nd_gate<FK_GENERAL, S, 1, FMA>(v, fg); break;
 #if SVB_FSLOTS == 5
 #define SVB_SLOTS(M, K) M(K, 0) M(K, 1) M(K, 2) M(K, 3) M(K, 4)
 #elif SVB_FSLOTS == 4
@@ -206,8 +212,9 @@ __device__ __forceinline__ void run_gate(double2 (&v)[FREGS], const FGate &fg, i
         SVB_SLOTS(SVB_NDU, FK_ANTI)
         SVB_SLOTS(SVB_NDU, FK_RX)
         SVB_SLOTS(SVB_NDC2, 0)
-#define SVB_DGU(V, T) case FOP_DIAG + ((V) * (FSLOTS + 1) + (T)) * 2 + 0: diag_gate<V, T, 0, FMA>(v, fg, l0); break;
-        SVB_SLOTS(SVB_DGU, FD_Z) SVB_DGU(FD_Z, FSLOTS)
+#define SVB_DGU(V, T) case SVB_OPDG(V, T, 0): diag_gate<V, T, 0, FMA>(v, fg, l0); break;
+        SVB_SLOTS(SVB_DGU, FD_Z)
+        case SVB_OPDG(FD_Z, FTPOS_THREAD, 0): diag_gate<FD_Z, FSLOTS, 0, FMA>(v, fg, l0); break;
         SVB_DG(FD_GENERAL)
         SVB_DG(FD_D1)
         default: break;
@@ -759,10 +766,10 @@ static int unit_code(double2 z) {
     return -1;
 }
 
-// registers (0..15) whose slot-s bit is set
-static unsigned slot_pattern(int s) {
+// registers (0..2^fs-1) whose slot-s bit is set
+static unsigned slot_pattern(int s, int fs = FSLOTS) {
     unsigned m = 0;
-    for (int i = 0; i < FREGS; ++i)
+    for (int i = 0; i < (1 << fs); ++i)
         if ((i >> s) & 1) m |= 1u << i;
     return m;
 }
@@ -779,11 +786,11 @@ struct GateMeta {
 // with distinct (bit mod 3) so the swizzle spreads them over 8 chunks.
 // pref: 3 local bits for lanes 0-2 that make a direct HBM side coalesced
 // (nullptr: none); they win over bank-conflict freedom on the other side.
-static void thread_map(int fm, const int *slots, int8_t *tmap, const int16_t *qcol = nullptr,
+static void thread_map(int fm, int fs, const int *slots, int8_t *tmap, const int16_t *qcol = nullptr,
                        const int16_t *mcol = nullptr, bool need_ld = false, bool need_st = false,
                        const int *pref = nullptr) {
     bool is_slot[FMMAX] = {};
-    for (int i = 0; i < FSLOTS; ++i) is_slot[slots[i]] = true;
+    for (int i = 0; i < fs; ++i) is_slot[slots[i]] = true;
     std::vector<int> free_bits;
     for (int b = 0; b < fm; ++b)
         if (!is_slot[b]) free_bits.push_back(b);
@@ -832,7 +839,7 @@ static void thread_map(int fm, const int *slots, int8_t *tmap, const int16_t *qc
     }
     for (int b : free_bits)
         if (std::find(order.begin(), order.end(), b) == order.end()) order.push_back(b);
-    for (int j = 0; j < fm - FSLOTS; ++j) tmap[j] = (int8_t)order[j];
+    for (int j = 0; j < fm - fs; ++j) tmap[j] = (int8_t)order[j];
 }
 
 // In-register X / CNOT (see the group scan) pays off when passes are JIT
@@ -858,11 +865,13 @@ static bool reg_perm_any_ctl() {
 // permutation.  Gates name logical qubits; everything on the device is
 // physical.
 static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, bool strict, bool regperm,
-                       int fm, const int8_t *phys = nullptr, const int8_t *phys_next = nullptr) {
+                       int fm, const int8_t *phys = nullptr, const int8_t *phys_next = nullptr,
+                       int fs = FSLOTS) {
     memset(&P, 0, sizeof(P));
     P.flow = flow_bits();
     P.fm = fm;
-    const int tbits = fm - FSLOTS;
+    P.fs = fs;
+    const int tbits = fm - fs;
     auto ph = [&](int q) { return phys ? (int)phys[q] : q; };
     auto phn = [&](int q) { return phys_next ? (int)phys_next[q] : ph(q); };
     int local_of[64];
@@ -962,7 +971,7 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
         // straight from HBM with coalesced 128 B lines (direct_first)
         if (!strict && &g == &gps[0] && m.tl < 3) return false;
         return std::find(g.slots.begin(), g.slots.end(), m.tl) != g.slots.end() ||
-               (int)g.slots.size() < FSLOTS;
+               (int)g.slots.size() < fs;
     };
     auto take = [&](GroupPlan &g, int q, bool inreg = false) {
         const GateMeta &m = meta[q];
@@ -1096,7 +1105,7 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
     int k0 = 0;
     for (int gi = 0; gi < P.ngroups; ++gi) {
         const GroupPlan &gp = gps[gi];
-        int slots[FSLOTS];
+        int slots[FSMAX];
         int ns = 0;
         for (int s : gp.slots) slots[ns++] = s;
         // fill the free slots from the top, keeping off the local bits a
@@ -1107,14 +1116,14 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
             return gi == (int)gps.size() - 1 && gp.mcol[b] && !(gp.mcol[b] >> 3);
         };
         for (int pass2 = 0; pass2 < 2; ++pass2)
-            for (int b = fm - 1; ns < FSLOTS && b >= 0; --b) {
+            for (int b = fm - 1; ns < fs && b >= 0; --b) {
                 bool used = false;
                 for (int i = 0; i < ns; ++i) used |= slots[i] == b;
                 if (!used && (pass2 == 1 || !lane_bit(b))) slots[ns++] = b;
             }
-        std::sort(slots, slots + FSLOTS);
+        std::sort(slots, slots + fs);
         FGroup &G = P.groups[gi];
-        for (int i = 0; i < FSLOTS; ++i) G.pos[i] = (int8_t)slots[i];
+        for (int i = 0; i < fs; ++i) G.pos[i] = (int8_t)slots[i];
         G.first = (int16_t)k0;
         G.count = (int16_t)gp.gates.size();
         G.mb = (int16_t)gp.mb;
@@ -1132,7 +1141,7 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
         // sit on three non-slot local bits that the group's map sends
         // (invertibly) into local bits 0-2, i.e. physical bits 0-2.
         bool is_slot_l[FMMAX] = {};
-        for (int k = 0; k < FSLOTS; ++k) is_slot_l[slots[k]] = true;
+        for (int k = 0; k < fs; ++k) is_slot_l[slots[k]] = true;
         auto coal = [&](const int16_t *col, int *out) {
             if (no_direct()) return false;
             std::vector<int> cand;
@@ -1164,9 +1173,9 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
         // own swizzle below.
         (void)can_df;
         (void)can_dl;
-        thread_map(fm, slots, G.tmap, G.qcol, G.mcol, gi == 0, gi == P.ngroups - 1 && !direct_any(), pref);
+        thread_map(fm, fs, slots, G.tmap, G.qcol, G.mcol, gi == 0, gi == P.ngroups - 1 && !direct_any(), pref);
         auto slot_of = [&](int l) {
-            for (int i = 0; i < FSLOTS; ++i)
+            for (int i = 0; i < fs; ++i)
                 if (slots[i] == l) return i;
             return -1;
         };
@@ -1183,10 +1192,10 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
             fg.tl = -1;
             int cs = m.cl >= 0 ? slot_of(m.cl) : -1;
             fg.cl = (int8_t)(m.cl >= 0 && cs < 0 ? tbit_of(m.cl) : -1);
-            fg.cmask = cs >= 0 ? slot_pattern(cs) : 0xffffffffu;
+            fg.cmask = cs >= 0 ? slot_pattern(cs, fs) : 0xffffffffu;
             if (m.diag) {
                 int ts = slot_of(m.tl);
-                int tpos = ts >= 0 ? ts : FSLOTS;
+                int tpos = ts >= 0 ? ts : FTPOS_THREAD;
                 fg.tl = (int8_t)(ts >= 0 ? -1 : tbit_of(m.tl));
                 int var = FD_GENERAL;
                 if (m.g.d0_one) {
@@ -1201,7 +1210,7 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
                         var = FD_D1;
                 }
                 if (kCompact && cs >= 0 && var == FD_Z) var = FD_D1;  // exact: cmul by (-1, 0)
-                fg.op = (uint8_t)(FOP_DIAG + (var * (FSLOTS + 1) + tpos) * 2 + (cs >= 0 ? 1 : 0));
+                fg.op = (uint8_t)(FOP_DIAG + (var * (FSMAX + 1) + tpos) * 2 + (cs >= 0 ? 1 : 0));
             } else {
                 int ts = slot_of(m.tl);
                 int kind;
@@ -1223,9 +1232,9 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
                     }
                 }
                 // pair loops visit lo registers (slot bit clear) whose control holds
-                fg.cmask = fg.cmask & ~slot_pattern(ts);
+                fg.cmask = fg.cmask & ~slot_pattern(ts, fs);
                 if (kCompact && cs >= 0) kind = FK_GENERAL;  // general formula = reference's, exact
-                fg.op = (uint8_t)((kind * FSLOTS + ts) * 2 + (cs >= 0 ? 1 : 0));
+                fg.op = (uint8_t)((kind * FSMAX + ts) * 2 + (cs >= 0 ? 1 : 0));
             }
         }
         k0 += (int)gp.gates.size();
@@ -1289,7 +1298,7 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
                 Gr.ld_t[j] = off(Gr.qcol[Gr.tmap[j]], hin);
                 Gr.st_t[j] = off(Gr.mcol[Gr.tmap[j]], hout);
             }
-            for (int k = 0; k < FSLOTS; ++k) {
+            for (int k = 0; k < fs; ++k) {
                 Gr.ld_s[k] = off(Gr.qcol[Gr.pos[k]], hin);
                 Gr.st_s[k] = off(Gr.mcol[Gr.pos[k]], hout);
             }
@@ -1317,12 +1326,12 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
     P.direct_first = (coalesced(G0, G0.qcol) && !no_direct()) || direct_any();
     P.gl_b = gidx(G0.qb);
     for (int j = 0; j < tbits; ++j) P.gl_t[j] = gidx(G0.qcol[G0.tmap[j]]);
-    for (int k = 0; k < FSLOTS; ++k) P.gl_s[k] = gidx(G0.qcol[G0.pos[k]]);
+    for (int k = 0; k < fs; ++k) P.gl_s[k] = gidx(G0.qcol[G0.pos[k]]);
     const FGroup &GL = P.groups[P.ngroups - 1];
     P.direct_last = (coalesced(GL, GL.mcol) && !no_direct()) || direct_any();
     P.gs_b = gidx(GL.mb);
     for (int j = 0; j < tbits; ++j) P.gs_t[j] = gidx(GL.mcol[GL.tmap[j]]);
-    for (int k = 0; k < FSLOTS; ++k) P.gs_s[k] = gidx(GL.mcol[GL.pos[k]]);
+    for (int k = 0; k < fs; ++k) P.gs_s[k] = gidx(GL.mcol[GL.pos[k]]);
     return true;
 }
 
@@ -1357,6 +1366,17 @@ static int plan_fm(int n, unsigned flags) {
     return std::max(FM, std::min(FMMAX, fm));
 }
 
+// Slot bits per thread of a plan: FSLOTS for the interpreter; specialised
+// passes hold 32 amplitudes per thread (5 slots, 255 registers, 2 CTAs of
+// 128 threads per SM at fm 12): fewer register groups -- each a full
+// shared-memory transposition of the tile -- per pass.  SVB_JIT_FS overrides.
+static int plan_fs(unsigned flags) {
+    if (!(flags & SVB_RUN_JIT) || !jit_available()) return FSLOTS;
+    const char *e = getenv("SVB_JIT_FS");
+    const int fs = e ? atoi(e) : 5;
+    return std::max(4, std::min(FSMAX, fs));
+}
+
 struct PlanStep {
     int op;      // >= 0: run `mapped` (ops[op] on physical qubits) with the single-gate kernels
     svb_op mapped;
@@ -1381,7 +1401,7 @@ static int phase_ways(const uint32_t *t) {
 // configs[1] 203 -> 170 passes at fm 12), the others of its set go home
 // when they can, and gate-free layout passes at the end restore the
 // identity layout the caller expects.
-static void lower_plan(int n, const svb_op *ops, int nops, bool strict, bool regperm, int fm,
+static void lower_plan(int n, const svb_op *ops, int nops, bool strict, bool regperm, int fm, int fs,
                        std::vector<PlanStep> &steps, std::vector<FPass> &passes) {
     const std::vector<PlanPass> plans = plan(n, ops, nops, strict, fm);
     const int nlow = flow_bits();
@@ -1398,7 +1418,7 @@ static void lower_plan(int n, const svb_op *ops, int nops, bool strict, bool reg
     };
     auto fused = [&](const PlanPass &pp, const int8_t *next) {
         FPass P;
-        if (!build_pass(n, ops, pp, P, strict, regperm, fm, phys.data(), next)) return false;
+        if (!build_pass(n, ops, pp, P, strict, regperm, fm, phys.data(), next, fs)) return false;
         PlanStep st;
         st.op = -1;
         memset(&st.mapped, 0, sizeof st.mapped);
@@ -1473,7 +1493,7 @@ static void lower_plan(int n, const svb_op *ops, int nops, bool strict, bool reg
                 taken |= uint64_t(1) << b;
             }
             FPass P;
-            if (!build_pass(n, ops, pp, P, strict, regperm, fm, phys.data(), nxt.data())) continue;
+            if (!build_pass(n, ops, pp, P, strict, regperm, fm, phys.data(), nxt.data(), fs)) continue;
             // score: uncoalesced last-group HBM store (2) + shared-memory
             // conflicts of the last group's loads and the groups' stores
             const FGroup &GL = P.groups[P.ngroups - 1];
@@ -1557,7 +1577,7 @@ int jit_check(int n, const svb_op *ops, int nops, unsigned flags) {
     std::vector<FPass> passes;
     std::vector<PlanStep> steps;
     const int fm = plan_fm(n, flags | SVB_RUN_JIT);
-    lower_plan(n, ops, nops, strict, reg_perm(flags), fm, steps, passes);
+    lower_plan(n, ops, nops, strict, reg_perm(flags), fm, plan_fs(flags | SVB_RUN_JIT), steps, passes);
     std::string err;
     int r = jit_compile_only(passes, jit_variant((flags & SVB_RUN_FMA) && !strict), err);
     if (r < 0) set_error("jit compile failed: %.400s", err.c_str());
@@ -1571,7 +1591,7 @@ int plan_passes(int n, const svb_op *ops, int nops, unsigned flags, int *groups)
     const int fm = plan_fm(n, flags);
     std::vector<FPass> passes;
     std::vector<PlanStep> steps;
-    lower_plan(n, ops, nops, strict, reg_perm(flags), fm, steps, passes);
+    lower_plan(n, ops, nops, strict, reg_perm(flags), fm, plan_fs(flags), steps, passes);
     int df = 0, dl = 0, cf = 0, cl = 0;
     auto coal = [](const FGroup &G, const int16_t *col) {
         const int x = col[G.tmap[0]], y = col[G.tmap[1]], z = col[G.tmap[2]];
@@ -1619,7 +1639,7 @@ int plan_passes(int n, const svb_op *ops, int nops, unsigned flags, int *groups)
 // sweeps) is planned and lowered to kernel descriptors once.
 
 struct CompiledPlan {
-    int n, fm;
+    int n, fm, fs;
     bool strict, regperm;
     std::vector<svb_op> ops;  // exact key
     std::vector<PlanStep> steps;
@@ -1641,7 +1661,7 @@ static uint64_t fnv1a(const void *p, size_t len, uint64_t h) {
 }
 
 static std::shared_ptr<const CompiledPlan> compiled_plan(int n, const svb_op *ops, int nops, bool strict,
-                                                         bool regperm, int fm) {
+                                                         bool regperm, int fm, int fs) {
     static std::mutex mu;
     static std::vector<std::pair<uint64_t, std::shared_ptr<const CompiledPlan>>> cache;  // MRU first
     uint64_t key = fnv1a(ops, sizeof(svb_op) * size_t(nops), 1469598103934665603ull);
@@ -1649,11 +1669,12 @@ static std::shared_ptr<const CompiledPlan> compiled_plan(int n, const svb_op *op
     key = fnv1a(&strict, sizeof strict, key);
     key = fnv1a(&regperm, sizeof regperm, key);
     key = fnv1a(&fm, sizeof fm, key);
+    key = fnv1a(&fs, sizeof fs, key);
     {
         std::lock_guard<std::mutex> lk(mu);
         for (size_t i = 0; i < cache.size(); ++i) {
             const auto &c = cache[i].second;
-            if (cache[i].first == key && c->n == n && c->fm == fm && c->strict == strict && c->regperm == regperm &&
+            if (cache[i].first == key && c->n == n && c->fm == fm && c->fs == fs && c->strict == strict && c->regperm == regperm &&
                 (int)c->ops.size() == nops &&
                 std::memcmp(c->ops.data(), ops, sizeof(svb_op) * size_t(nops)) == 0) {
                 auto hit = cache[i];
@@ -1666,10 +1687,11 @@ static std::shared_ptr<const CompiledPlan> compiled_plan(int n, const svb_op *op
     auto cp = std::make_shared<CompiledPlan>();
     cp->n = n;
     cp->fm = fm;
+    cp->fs = fs;
     cp->strict = strict;
     cp->regperm = regperm;
     cp->ops.assign(ops, ops + nops);
-    lower_plan(n, ops, nops, strict, regperm, fm, cp->steps, cp->passes);
+    lower_plan(n, ops, nops, strict, regperm, fm, fs, cp->steps, cp->passes);
     // Bounded by descriptor bytes (~27 KiB per pass), not by count: the
     // multi-process engine runs one op segment per exchange interval, so a
     // circuit step may cycle through hundreds of small plans.
@@ -1706,7 +1728,8 @@ int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsi
     }
     const bool strict = flags & SVB_RUN_STRICT_ORDER;
     const bool fma = (flags & SVB_RUN_FMA) && !strict;
-    std::shared_ptr<const CompiledPlan> cp = compiled_plan(n, ops, nops, strict, reg_perm(flags), plan_fm(n, flags));
+    std::shared_ptr<const CompiledPlan> cp =
+        compiled_plan(n, ops, nops, strict, reg_perm(flags), plan_fm(n, flags), plan_fs(flags));
     size_t next_pass = 0;
     bool jit = (flags & SVB_RUN_JIT) && !cp->passes.empty();
     const std::vector<void *> *jit_fns = nullptr;
@@ -1717,8 +1740,8 @@ int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsi
         if (state == 0) state = jit_build(cp->passes, variant, cp->jit_fns[variant]) ? 1 : -1;
         if (state == 1) jit_fns = &cp->jit_fns[variant];
     }
-    if (!jit_fns && cp->fm != FM) {  // JIT unavailable: the interpreter runs FM tiles
-        cp = compiled_plan(n, ops, nops, strict, reg_perm(flags & ~SVB_RUN_JIT), FM);
+    if (!jit_fns && (cp->fm != FM || cp->fs != FSLOTS)) {  // JIT unavailable: the interpreter's geometry
+        cp = compiled_plan(n, ops, nops, strict, reg_perm(flags & ~SVB_RUN_JIT), FM, FSLOTS);
         jit = false;
     }
     for (const PlanStep &st : cp->steps) {

@@ -34,6 +34,11 @@ namespace svb {
 
 namespace {
 
+// slot bits / registers per thread of the pass being generated
+thread_local int t_fs = FSLOTS;
+inline int NS() { return t_fs; }
+inline int NR() { return 1 << t_fs; }
+
 struct Out {
     std::string s;
     void operator()(const char *fmt, ...) {
@@ -134,19 +139,19 @@ int swz_h(int l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9) ^ (l >> 12)) & 7)
 
 unsigned xcombo_h(const uint32_t *s, int i) {
     unsigned r = 0;
-    for (int k = 0; k < FSLOTS; ++k)
+    for (int k = 0; k < NS(); ++k)
         if ((i >> k) & 1) r ^= s[k];
     return r;
 }
 int64_t xcombo_g(const int64_t *s, int i) {
     int64_t r = 0;
-    for (int k = 0; k < FSLOTS; ++k)
+    for (int k = 0; k < NS(); ++k)
         if ((i >> k) & 1) r ^= s[k];
     return r;
 }
 unsigned slot_pat(int s) {
     unsigned m = 0;
-    for (int i = 0; i < FREGS; ++i)
+    for (int i = 0; i < NR(); ++i)
         if ((i >> s) & 1) m |= 1u << i;
     return m;
 }
@@ -158,8 +163,8 @@ void emit_gate(Out &o, const FGate &g) {
     const bool thread_ctl = g.cl >= 0;
     if (thread_ctl) o("if ((tid >> %d) & 1) {\n", g.cl);
     if (op < FOP_DIAG) {
-        const int kind = (op >> 1) / FSLOTS, s = (op >> 1) % FSLOTS, ctrl = op & 1;
-        for (int i = 0; i < FREGS; ++i) {
+        const int kind = (op >> 1) / FSMAX, s = (op >> 1) % FSMAX, ctrl = op & 1;
+        for (int i = 0; i < NR(); ++i) {
             if (i & (1 << s)) continue;
             if (ctrl && !((g.cmask >> i) & 1)) continue;
             const int j = i | (1 << s);
@@ -185,7 +190,7 @@ void emit_gate(Out &o, const FGate &g) {
         }
     } else {
         const int code = op - FOP_DIAG;
-        const int ctrl = code & 1, tpos = (code >> 1) % (FSLOTS + 1), var = (code >> 1) / (FSLOTS + 1);
+        const int ctrl = code & 1, tpos = (code >> 1) % (FSMAX + 1), var = (code >> 1) / (FSMAX + 1);
         auto mul = [&](int i, const double2 &d) {
             if (var == FD_Z && d.x == -1.0)
                 o("v[%d] = mk(-v[%d].x, -v[%d].y);\n", i, i, i);
@@ -193,20 +198,20 @@ void emit_gate(Out &o, const FGate &g) {
                 o("v[%d] = cm(%s, %s, v[%d]);\n", i, lit(d.x).c_str(), lit(d.y).c_str(), i);
         };
         const bool d0_one = var != FD_GENERAL;
-        if (tpos == FSLOTS) {  // target on a thread bit: one factor per thread
+        if (tpos == FTPOS_THREAD) {  // target on a thread bit: one factor per thread
             o("if ((tid >> %d) & 1) {\n", g.tl);
-            for (int i = 0; i < FREGS; ++i)
+            for (int i = 0; i < NR(); ++i)
                 if (!ctrl || ((g.cmask >> i) & 1)) mul(i, m[3]);
             o("}");
             if (!d0_one) {
                 o(" else {\n");
-                for (int i = 0; i < FREGS; ++i)
+                for (int i = 0; i < NR(); ++i)
                     if (!ctrl || ((g.cmask >> i) & 1)) mul(i, m[0]);
                 o("}");
             }
             o("\n");
         } else {
-            for (int i = 0; i < FREGS; ++i) {
+            for (int i = 0; i < NR(); ++i) {
                 if (ctrl && !((g.cmask >> i) & 1)) continue;
                 const bool b = (i >> tpos) & 1;
                 if (b)
@@ -317,7 +322,7 @@ std::string pcond(uint32_t m) {
 void pend_flush(Out &o, int s) {
     if (!t_pend || !t_pend[s]) return;
     o("{ const bool p = %s;\n", pcond(t_pend[s]).c_str());
-    for (int i = 0; i < FREGS; ++i) {
+    for (int i = 0; i < NR(); ++i) {
         if (i & (1 << s)) continue;
         const int j = i | (1 << s);
         o("{ const d2 a = v[%d], b = v[%d]; v[%d] = p ? b : a; v[%d] = p ? a : b; }\n", i, j, i, j);
@@ -327,7 +332,7 @@ void pend_flush(Out &o, int s) {
 }
 
 int slot_of_mask(unsigned cmask, int t) {
-    for (int k = 0; k < FSLOTS; ++k) {
+    for (int k = 0; k < NS(); ++k) {
         unsigned pat = slot_pat(k) & ~(t >= 0 ? slot_pat(t) : 0u);
         if (k != t && pat == cmask) return k;
     }
@@ -339,23 +344,23 @@ void pend_conflicts(Out &o, const FGate &g) {
     if (!t_pend) return;
     const int op = g.op;
     if (op < FOP_DIAG) {
-        const int t = (op >> 1) % FSLOTS, ctrl = op & 1;
+        const int t = (op >> 1) % FSMAX, ctrl = op & 1;
         pend_flush(o, t);
         if (ctrl) {
             const int k = slot_of_mask(g.cmask, t);
             if (k < 0)
-                for (int x = 0; x < FSLOTS; ++x) pend_flush(o, x);
+                for (int x = 0; x < NS(); ++x) pend_flush(o, x);
             else
                 pend_flush(o, k);
         }
     } else {
         const int c = op - FOP_DIAG;
-        const int ctrl = c & 1, tpos = (c >> 1) % (FSLOTS + 1);
-        if (tpos < FSLOTS) pend_flush(o, tpos);
+        const int ctrl = c & 1, tpos = (c >> 1) % (FSMAX + 1);
+        if (tpos < FTPOS_THREAD) pend_flush(o, tpos);
         if (ctrl) {
             const int k = slot_of_mask(g.cmask, -1);
             if (k < 0)
-                for (int x = 0; x < FSLOTS; ++x) pend_flush(o, x);
+                for (int x = 0; x < NS(); ++x) pend_flush(o, x);
             else
                 pend_flush(o, k);
         }
@@ -368,12 +373,12 @@ void emit_gate_fold(Out &o, const FGate &g, int *code) {
     const bool thread_ctl = g.cl >= 0;
     pend_conflicts(o, g);
     if (op < FOP_DIAG) {
-        const int kind = (op >> 1) / FSLOTS, s = (op >> 1) % FSLOTS, ctrl = op & 1;
+        const int kind = (op >> 1) / FSMAX, s = (op >> 1) % FSMAX, ctrl = op & 1;
         const int u12 = unit_code(m[1]), u21 = unit_code(m[2]);
         const bool unit_anti = m[0].x == 0.0 && m[0].y == 0.0 && m[3].x == 0.0 && m[3].y == 0.0 && u12 >= 0 &&
                                u21 >= 0;
         std::vector<int> lows;
-        for (int i = 0; i < FREGS; ++i) {
+        for (int i = 0; i < NR(); ++i) {
             if (i & (1 << s)) continue;
             if (ctrl && !((g.cmask >> i) & 1)) continue;
             lows.push_back(i);
@@ -405,7 +410,7 @@ void emit_gate_fold(Out &o, const FGate &g, int *code) {
             for (int i : lows) {
                 const int j = i | (1 << s);
                 o("{ const d2 t = v[%d]; v[%d] = v[%d]; v[%d] = t; }\n", i, i, j, j);
-                int tmp[FREGS] = {0};
+                int tmp[FREGMAX] = {0};
                 tmp[i] = u12;
                 tmp[j] = u21;
                 materialize(o, tmp, i);
@@ -473,11 +478,11 @@ void emit_gate_fold(Out &o, const FGate &g, int *code) {
         return;
     }
     const int code_ = op - FOP_DIAG;
-    const int ctrl = code_ & 1, tpos = (code_ >> 1) % (FSLOTS + 1), var = (code_ >> 1) / (FSLOTS + 1);
+    const int ctrl = code_ & 1, tpos = (code_ >> 1) % (FSMAX + 1), var = (code_ >> 1) / (FSMAX + 1);
     const bool d0_one = var != FD_GENERAL;
-    const bool branch = thread_ctl || tpos == FSLOTS;
+    const bool branch = thread_ctl || tpos == FTPOS_THREAD;
     std::vector<int> regs;
-    for (int i = 0; i < FREGS; ++i)
+    for (int i = 0; i < NR(); ++i)
         if (!ctrl || ((g.cmask >> i) & 1)) regs.push_back(i);
     auto mul = [&](int i, const double2 &d) {
         const int u = unit_code(d);
@@ -495,7 +500,7 @@ void emit_gate_fold(Out &o, const FGate &g, int *code) {
     if (branch)
         for (int i : regs) materialize(o, code, i);
     if (thread_ctl) o("if ((tid >> %d) & 1) {\n", g.cl);
-    if (tpos == FSLOTS) {
+    if (tpos == FTPOS_THREAD) {
         o("if ((tid >> %d) & 1) {\n", g.tl);
         for (int i : regs) mul(i, m[3]);
         o("}");
@@ -633,7 +638,7 @@ void emit_gate_fast(Out &o, const FGate &g, int *code, double2 &F) {
         return;
     }
     if (op < FOP_DIAG) {
-        const int s = (op >> 1) % FSLOTS;
+        const int s = (op >> 1) % FSMAX;
         const int u12 = unit_code(g.m[1]), u21 = unit_code(g.m[2]);
         if (g.m[0].x == 0.0 && g.m[0].y == 0.0 && g.m[3].x == 0.0 && g.m[3].y == 0.0 && u12 >= 0 && u21 >= 0) {
             emit_gate_fold(o, g, code);  // a pure rename already
@@ -643,7 +648,7 @@ void emit_gate_fast(Out &o, const FGate &g, int *code, double2 &F) {
         double2 v[4];
         for (int i = 0; i < 4; ++i) v[i] = cdivh(g.m[i], a);
         F = cmulh(F, a);
-        for (int i = 0; i < FREGS; ++i) {
+        for (int i = 0; i < NR(); ++i) {
             if (i & (1 << s)) continue;
             const int j = i | (1 << s);
             o("{ const d2 L = v[%d], H = v[%d];\nv[%d] = %s;\nv[%d] = %s; }\n", i, j, i,
@@ -653,7 +658,7 @@ void emit_gate_fast(Out &o, const FGate &g, int *code, double2 &F) {
         return;
     }
     const int c = op - FOP_DIAG;
-    const int tpos = (c >> 1) % (FSLOTS + 1);
+    const int tpos = (c >> 1) % (FSMAX + 1);
     const double2 a = pick_factor(g.m, true);
     const double2 d0 = cdivh(g.m[0], a), d1 = cdivh(g.m[3], a);
     F = cmulh(F, a);
@@ -668,22 +673,22 @@ void emit_gate_fast(Out &o, const FGate &g, int *code, double2 &F) {
           fast_sum({{d.x, "X", 1, code[i]}, {d.y, "X", 0, code[i]}}).c_str());
         code[i] = 0;
     };
-    if (tpos == FSLOTS) {  // target on a thread bit: the factor depends on the thread
+    if (tpos == FTPOS_THREAD) {  // target on a thread bit: the factor depends on the thread
         const bool one0 = unit_code(d0) == 0, one1 = unit_code(d1) == 0;
-        for (int i = 0; i < FREGS; ++i) materialize(o, code, i);
+        for (int i = 0; i < NR(); ++i) materialize(o, code, i);
         if (!one1) {
             o("if ((tid >> %d) & 1) {\n", g.tl);
-            for (int i = 0; i < FREGS; ++i) mul(i, d1, true);
+            for (int i = 0; i < NR(); ++i) mul(i, d1, true);
             o("}\n");
         }
         if (!one0) {
             o("if (!((tid >> %d) & 1)) {\n", g.tl);
-            for (int i = 0; i < FREGS; ++i) mul(i, d0, true);
+            for (int i = 0; i < NR(); ++i) mul(i, d0, true);
             o("}\n");
         }
         return;
     }
-    for (int i = 0; i < FREGS; ++i) mul(i, ((i >> tpos) & 1) ? d1 : d0, false);
+    for (int i = 0; i < NR(); ++i) mul(i, ((i >> tpos) & 1) ? d1 : d0, false);
 }
 
 }  // namespace
@@ -723,10 +728,10 @@ int jit_pass_mode(const FPass &P) {
     return m;
 }
 
-int jit_threads(const FPass &P) { return (1 << P.fm) / FREGS; }
+int jit_threads(const FPass &P) { return (1 << P.fm) >> P.fs; }
 
 // resident CTAs per SM the generated kernel is built for (__launch_bounds__):
-// 128 registers per thread (16 amplitudes + addresses), so 64K / (128 x threads)
+// 64K registers / (threads x registers per thread)
 int jit_ctas_per_sm(const FPass &P) {
     static int c = [] {
         const char *e = getenv("SVB_JIT_CTAS");
@@ -735,7 +740,8 @@ int jit_ctas_per_sm(const FPass &P) {
     }();
     if (jit_pass_mode(P) == 1) return 3;
     if (c) return c;
-    return std::max(1, 512 / jit_threads(P));
+    // 16 amplitudes per thread fit 128 registers, 32 need the full 255
+    return std::max(1, 65536 / (jit_threads(P) * (P.fs >= 5 ? 256 : 128)));
 }
 // tile buffers live in dynamic shared memory when they exceed the 48 KiB
 // static limit (double buffering, or tiles of 12+ qubits)
@@ -757,6 +763,7 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last);
 std::string jit_source(const FPass &P, int variant, double2 &F, bool last) {
     ConstPool pool;
     t_pool = &pool;
+    t_fs = P.fs;
     std::string body = jit_body(P, variant, F, last);
     t_pool = nullptr;
     Out o;
@@ -773,7 +780,7 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
     const bool fma = variant >= 1, fast = variant == 2;
     const int mode = jit_pass_mode(P);
     Out o;
-    const int FTILE = 1 << P.fm, FTHREADS = jit_threads(P), FTBITS = P.fm - FSLOTS;
+    const int FTILE = 1 << P.fm, FTHREADS = jit_threads(P), FTBITS = P.fm - P.fs;
     const int colmask = (1 << P.flow) - 1;
     // Tile-local global offsets are XOR-linear in the thread index and the
     // register number: thread parts are computed per use from the opaque
@@ -824,7 +831,7 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
     auto k_smem = [&](int k) { return (unsigned)(16 * swz_h(k * FTHREADS)); };
     o("auto fill = [&](unsigned char *dstb, const d2 *p) {\n%s", kOpaqueTid);
     thread_parts();
-    for (int k = 0; k < FREGS; ++k)
+    for (int k = 0; k < NR(); ++k)
         o("cpa(dstb + (s ^ %uu), p + (r ^ %s));\n", k_smem(k), offl(k_row(k)).c_str());
     o("asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\"); };\n(void)fill;\n");
     const char *wait_all = "asm volatile(\"cp.async.wait_group 0;\\n\" ::: \"memory\");\n";
@@ -851,7 +858,7 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
         }
     }
     o("unsigned char *sb = reinterpret_cast<unsigned char *>(buf);\n");
-    o("d2 v[%d];\n", FREGS);
+    o("d2 v[%d];\n", NR());
     for (int gi = 0; gi < P.ngroups; ++gi) {
         const FGroup &G = P.groups[gi];
         const bool last = gi == P.ngroups - 1;
@@ -860,13 +867,13 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             o("%s g0 = %s;\n", OFF, offl(P.gl_b).c_str());
             o.s += kOpaqueTid;
             for (int j = 0; j < FTBITS; ++j) o("if ((tg >> %d) & 1) g0 ^= %s;\n", j, offl(P.gl_t[j]).c_str());
-            for (int i = 0; i < FREGS; ++i)
+            for (int i = 0; i < NR(); ++i)
                 o("v[%d] = ldcs(pa + (g0 ^ %s));\n", i, offl(xcombo_g(P.gl_s, i)).c_str());
         } else {
             o("unsigned a0 = %uu;\n", (unsigned)G.ld_b);
             o.s += kOpaqueTid;
             for (int j = 0; j < FTBITS; ++j) o("if ((tg >> %d) & 1) a0 ^= %uu;\n", j, (unsigned)G.ld_t[j]);
-            for (int i = 0; i < FREGS; ++i)
+            for (int i = 0; i < NR(); ++i)
                 o("v[%d] = *reinterpret_cast<const d2 *>(sb + (a0 ^ %uu));\n", i, xcombo_h(G.ld_s, i));
         }
         if (last && mode == 2) {
@@ -874,25 +881,25 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             o("__syncthreads();\n{ const i64 nx = tix + gridDim.x; if (nx < ntiles) "
               "fill(reinterpret_cast<unsigned char *>(dsm), a + tbase(nx)); }\n");
         }
-        uint32_t pend[FSLOTS] = {0};
+        uint32_t pend[FSMAX] = {0};
         if (fma && pend_on()) t_pend = pend;
         if (fast) {
-            int code[FREGS] = {0};
+            int code[FREGMAX] = {0};
             for (int q = G.first; q < G.first + G.count; ++q) emit_gate_fast(o, P.gates[q], code, F);
             const double mag = cabsh(F);
             if (gi == P.ngroups - 1 && (last || mag < 0x1p-200 || mag > 0x1p200) &&
                 !(F.x == 1.0 && F.y == 0.0)) {
-                for (int i = 0; i < FREGS; ++i) {  // stored * F = true amplitude
+                for (int i = 0; i < NR(); ++i) {  // stored * F = true amplitude
                     o("{ const d2 X = v[%d]; v[%d] = %s; }\n", i, i, cm_fold(F, code[i]).c_str());
                     code[i] = 0;
                 }
                 F = make_double2(1.0, 0.0);
             }
-            for (int i = 0; i < FREGS; ++i) materialize(o, code, i);
+            for (int i = 0; i < NR(); ++i) materialize(o, code, i);
         } else if (fma) {
-            int code[FREGS] = {0};
+            int code[FREGMAX] = {0};
             for (int q = G.first; q < G.first + G.count; ++q) emit_gate_fold(o, P.gates[q], code);
-            for (int i = 0; i < FREGS; ++i) materialize(o, code, i);
+            for (int i = 0; i < NR(); ++i) materialize(o, code, i);
         } else {
             for (int q = G.first; q < G.first + G.count; ++q) emit_gate(o, P.gates[q]);
         }
@@ -902,20 +909,20 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             o("%s s0 = %s;\n", OFF, offl(P.gs_b).c_str());
             o("{\n%s", kOpaqueTid);
             for (int j = 0; j < FTBITS; ++j) o("if ((tg >> %d) & 1) s0 ^= %s;\n", j, offl(P.gs_t[j]).c_str());
-            for (int k = 0; k < FSLOTS; ++k)  // pending swaps: per-thread store address
+            for (int k = 0; k < NS(); ++k)  // pending swaps: per-thread store address
                 if (pend[k]) o("if (%s) s0 ^= %s;\n", pcond(pend[k]).c_str(), offl(P.gs_s[k]).c_str());
             o("}\n");
-            for (int i = 0; i < FREGS; ++i)
+            for (int i = 0; i < NR(); ++i)
                 o("stcs(pa + (s0 ^ %s), v[%d]);\n", offl(xcombo_g(P.gs_s, i)).c_str(), i);
         } else {
             if (G.perm) o("__syncthreads();\n");
             o("unsigned b0 = %uu;\n", (unsigned)G.st_b);
             o("{\n%s", kOpaqueTid);
             for (int j = 0; j < FTBITS; ++j) o("if ((tg >> %d) & 1) b0 ^= %uu;\n", j, (unsigned)G.st_t[j]);
-            for (int k = 0; k < FSLOTS; ++k)
+            for (int k = 0; k < NS(); ++k)
                 if (pend[k]) o("if (%s) b0 ^= %uu;\n", pcond(pend[k]).c_str(), (unsigned)G.st_s[k]);
             o("}\n");
-            for (int i = 0; i < FREGS; ++i)
+            for (int i = 0; i < NR(); ++i)
                 o("*reinterpret_cast<d2 *>(sb + (b0 ^ %uu)) = v[%d];\n", xcombo_h(G.st_s, i), i);
             o("__syncthreads();\n");
         }
@@ -924,7 +931,7 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
     if (!P.direct_last) {
         o("{\n%s", kOpaqueTid);
         thread_parts();
-        for (int k = 0; k < FREGS; ++k)
+        for (int k = 0; k < NR(); ++k)
             o("pa[r ^ %s] = *reinterpret_cast<const d2 *>(sb + (s ^ %uu));\n", offl(k_row(k)).c_str(), k_smem(k));
         o("}\n");
     }

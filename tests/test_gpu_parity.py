@@ -170,12 +170,14 @@ def test_bench_path_deep_circuit_vs_oracle(cuda_ok):
     assert abs(device.norm2(st) - 1.0) < 1e-12
 
 
-@pytest.mark.parametrize("fm", [11, 12, 13])
-def test_jit_tile_sizes_vs_oracle(cuda_ok, fm, monkeypatch):
+@pytest.mark.parametrize("fm,fs", [(11, 4), (11, 5), (12, 4), (12, 5), (13, 4), (13, 5)])
+def test_jit_tile_sizes_vs_oracle(cuda_ok, fm, fs, monkeypatch):
     # runtime-specialised passes may use 2^12 / 2^13-amplitude tiles (64 /
-    # 128 KiB of shared memory, 256 / 512 threads): every tile size agrees
-    # with the oracle, exact arithmetic bit-identical to the interpreter's
+    # 128 KiB of shared memory) and 16 or 32 amplitudes per thread: every
+    # geometry agrees with the oracle, strict order bit-identical to the
+    # interpreter's
     monkeypatch.setenv("SVB_JIT_FM", str(fm))
+    monkeypatch.setenv("SVB_JIT_FS", str(fs))
     n = 22
     rng = np.random.default_rng(900 + fm)
     circ = w.random_layer_circuit(n, 12, seed=fm)
@@ -193,10 +195,13 @@ def test_jit_passes_bit_identical_to_interpreter(cuda_ok, n, monkeypatch):
     # SVB_RUN_JIT compiles each fused pass to straight-line code; on the same
     # plan it must give exactly the interpreter's bits (exact and FMA
     # arithmetic, perms, controls).  JIT plans run X / CNOT in registers by
-    # default; SVB_FUSE_REGPERM=1 gives the interpreter that same plan, and
-    # SVB_JIT_FACTOR=0 turns off the (rounding-level) scalar extraction.
+    # default; SVB_FUSE_REGPERM=1 gives the interpreter that same plan,
+    # SVB_JIT_FS=4 its 16 amplitudes per thread (register groups decide which
+    # commuting gates meet first), and SVB_JIT_FACTOR=0 turns off the
+    # (rounding-level) scalar extraction.
     monkeypatch.setenv("SVB_FUSE_REGPERM", "1")
     monkeypatch.setenv("SVB_JIT_FACTOR", "0")
+    monkeypatch.setenv("SVB_JIT_FS", "4")
     rng = np.random.default_rng(600 + n)
     x = standard_gate("x")
     pool = all_gates(rng) + [x, x, Gate2x2(1, 0, 0, -1j)]
@@ -221,6 +226,7 @@ def test_jit_passes_bit_identical_to_interpreter(cuda_ok, n, monkeypatch):
         # to rounding, and strict order stays bit-exact through the JIT
         monkeypatch.delenv("SVB_FUSE_REGPERM")
         monkeypatch.delenv("SVB_JIT_FACTOR")
+        monkeypatch.delenv("SVB_JIT_FS")
         got = device.simulate(circ, a.copy(), fma=True, jit=True)
         assert np.max(np.abs(got - want)) <= TOL
         got = device.simulate(circ, a.copy(), strict_order=True, jit=True)
@@ -228,6 +234,7 @@ def test_jit_passes_bit_identical_to_interpreter(cuda_ok, n, monkeypatch):
         assert np.array_equal(got, ref)
         monkeypatch.setenv("SVB_FUSE_REGPERM", "1")
         monkeypatch.setenv("SVB_JIT_FACTOR", "0")
+        monkeypatch.setenv("SVB_JIT_FS", "4")
 
 
 @pytest.mark.parametrize("n", [14, 17])
