@@ -856,6 +856,14 @@ static bool reg_perm_any_ctl() {
     return !e || atoi(e) != 0;
 }
 
+// SVB_FUSE_GROUPLA=1: choose each register group's slot set by a dry-run
+// lookahead instead of first come (configs[1]: 544 -> 535 groups for 2x the
+// planning time; off by default)
+static bool group_lookahead() {
+    const char *e = getenv("SVB_FUSE_GROUPLA");
+    return e && atoi(e) != 0;
+}
+
 // Build the kernel descriptor for one pass; false if it does not fit.
 // Qubit layout: logical qubit q lives at physical index bit phys[q] (nullptr:
 // identity).  A pass tiles over the physical bits of its qubit set S -- which
@@ -965,11 +973,13 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
     auto gbits = [&](const GateMeta &m) {
         return (uint64_t(1) << m.tl) | (m.cl >= 0 ? uint64_t(1) << m.cl : 0);
     };
-    auto fits = [&](const GroupPlan &g, const GateMeta &m) {
+    // allowed: the group's slot set when chosen up front (0: first come)
+    auto fits = [&](const GroupPlan &g, const GateMeta &m, bool first, uint64_t allowed) {
         if (m.diag) return true;
         // the first group keeps local bits 0-2 out of its slots so it can load
         // straight from HBM with coalesced 128 B lines (direct_first)
-        if (!strict && &g == &gps[0] && m.tl < 3) return false;
+        if (!strict && first && m.tl < 3) return false;
+        if (allowed) return ((allowed >> m.tl) & 1) != 0;
         return std::find(g.slots.begin(), g.slots.end(), m.tl) != g.slots.end() ||
                (int)g.slots.size() < fs;
     };
@@ -989,26 +999,24 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
         GroupPlan *g = new_group();
         for (int q = 0; q < ng; ++q) {
             const GateMeta &m = meta[q];
-            bool ok = m.perm || ((gbits(m) & g->permq) == 0 && fits(*g, m));
+            bool ok = m.perm || ((gbits(m) & g->permq) == 0 && fits(*g, m, gps.size() == 1, 0));
             if (!ok) g = new_group();
             take(*g, q);
         }
     } else {
         std::vector<char> placed(ng, 0);
         int left = ng;
-        while (left > 0) {
-            GroupPlan *g = new_group();
-            // allow_perm = false: take arithmetic gates only (an unplaced
-            // permutation blocks its qubits like any unplaced gate); only when
-            // that stalls, admit permutations -- each one closes its qubits
-            // for the rest of the group, so they go last.
-            // mode 0: arithmetic only; 1: permutations too (post map);
-            // 2: permutations only -- run first, they fold into the load map
+        // Fill group g from the unplaced gates: repeated scans taking every
+        // ready gate (no earlier unplaced gate on its qubits) that fits.
+        // mode 0: arithmetic only; 1: permutations too (post map);
+        // 2: permutations only -- run first, they fold into the load map.
+        auto fill_group = [&](GroupPlan &g, std::vector<char> &pl, int &lft, bool first, uint64_t allowed) {
+            int taken = 0;
             auto scan = [&](int mode) {
                 bool progress = false;
                 uint64_t blocked = 0;  // local bits touched by an unplaced earlier gate
                 for (int q = 0; q < ng; ++q) {
-                    if (placed[q]) continue;
+                    if (pl[q]) continue;
                     const GateMeta &m = meta[q];
                     const uint64_t bits = gbits(m);
                     // an X / CNOT whose target fits the group's slots runs in
@@ -1017,19 +1025,20 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
                     // (SVB_FUSE_REGPERM_CTL=0: only when the control is already a
                     // slot -- a thread-bit control costs a divergent swap)
                     const bool ctl_ok = m.cl < 0 || reg_perm_any_ctl() ||
-                                        std::find(g->slots.begin(), g->slots.end(), m.cl) != g->slots.end();
+                                        std::find(g.slots.begin(), g.slots.end(), m.cl) != g.slots.end();
                     const bool inreg = m.perm && mode == 0 && regperm && ctl_ok && (bits & blocked) == 0 &&
-                                       (bits & g->permq) == 0 && fits(*g, m);
+                                       (bits & g.permq) == 0 && fits(g, m, first, allowed);
                     bool ok = (bits & blocked) == 0 &&
                               (m.perm ? (mode != 0 || inreg)
-                                      : (mode != 2 && (bits & g->permq) == 0 && fits(*g, m)));
+                                      : (mode != 2 && (bits & g.permq) == 0 && fits(g, m, first, allowed)));
                     // a CNOT between local bits 0-2 and the rest, folded into the
                     // first group's load map, would break its coalesced HBM rows
-                    if (mode == 2 && g == &gps[0] && (bits & 7) && (bits & ~uint64_t(7))) ok = false;
+                    if (mode == 2 && first && (bits & 7) && (bits & ~uint64_t(7))) ok = false;
                     if (ok) {
-                        take(*g, q, inreg);
-                        placed[q] = 1;
-                        --left;
+                        take(g, q, inreg);
+                        pl[q] = 1;
+                        --lft;
+                        ++taken;
                         progress = true;
                     } else {
                         blocked |= bits;
@@ -1043,6 +1052,46 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
                 while (scan(0)) {
                 }
                 if (!scan(1)) break;
+            }
+            return taken;
+        };
+        auto fresh = [&]() {
+            GroupPlan g;
+            for (int j = 0; j < fm; ++j) g.mcol[j] = g.qcol[j] = 1 << j;
+            return g;
+        };
+        while (left > 0) {
+            const bool first = gps.empty();
+            // Choose the slot set up front: grow it one local bit at a time,
+            // each time the bit whose addition lets the group take the most
+            // gates (a dry run of the same scans); stop when no bit helps.
+            uint64_t allowed = 0;
+            if (group_lookahead()) {
+                int have = -1;
+                for (int k = 0; k < fs; ++k) {
+                    int best = have, bb = -1;
+                    for (int b = 0; b < fm; ++b) {
+                        if ((allowed >> b) & 1) continue;
+                        if (first && b < 3) continue;
+                        std::vector<char> pl = placed;
+                        int lft = left;
+                        GroupPlan tmp = fresh();
+                        const int c = fill_group(tmp, pl, lft, first, allowed | (uint64_t(1) << b));
+                        if (c > best) {
+                            best = c;
+                            bb = b;
+                        }
+                    }
+                    if (bb < 0) break;
+                    allowed |= uint64_t(1) << bb;
+                    have = best;
+                }
+            }
+            GroupPlan *g = new_group();
+            fill_group(*g, placed, left, first, allowed);
+            if (g->gates.empty() && g->permq == 0 && g->qb == 0 && allowed) {
+                // (nothing fit the chosen set -- cannot happen, but never loop)
+                fill_group(*g, placed, left, first, 0);
             }
         }
     }
@@ -1616,7 +1665,15 @@ int plan_passes(int n, const svb_op *ops, int nops, unsigned flags, int *groups)
         cf += c0;
         cl += c1;
         if (dbg3) {
-            fprintf(stderr, "pass: %d gates, %d groups, coalesced %d %d | banks:", P.ngates, P.ngroups, c0, c1);
+            // distinct non-diagonal targets: a lower bound of ceil(targets / fs) groups
+            uint32_t tg = 0;
+            for (int gi = 0; gi < P.ngroups; ++gi) {
+                const FGroup &G = P.groups[gi];
+                for (int q = G.first; q < G.first + G.count; ++q)
+                    if (P.gates[q].op < FOP_DIAG) tg |= 1u << G.pos[(P.gates[q].op >> 1) % FSMAX];
+            }
+            fprintf(stderr, "pass: %d gates, %d groups, %d targets, coalesced %d %d | banks:", P.ngates, P.ngroups,
+                    __builtin_popcount(tg), c0, c1);
             for (int gi = 0; gi < P.ngroups; ++gi) {
                 const FGroup &G = P.groups[gi];
                 // JIT passes with prefetch read group 0 from shared memory too

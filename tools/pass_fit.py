@@ -20,7 +20,7 @@ ids = sorted(by)
 plan = [ln for ln in open(sys.argv[2]) if ln.startswith("pass:") and "| banks:" in ln]
 X, Y = [], []
 for i, ln in zip(ids, plan):
-    g, gr, c0, c1 = map(int, re.match(r"pass: (\d+) gates, (\d+) groups, coalesced (\d) (\d)", ln).groups())
+    g, gr, c0, c1 = map(int, re.match(r"pass: (\d+) gates, (\d+) groups, (?:\d+ targets, )?coalesced (\d) (\d)", ln).groups())
     conf = sum(int(w) - 1 for w in re.findall(r" (?:ld|st) (\d)", ln) if int(w) > 0)
     d = by[i]
     X.append((g, gr, 1 - c1 + conf))
