@@ -127,6 +127,16 @@ int svb_permute_qubits(const void *src, void *dst, int64_t n_amps, const int *ph
  * [0, count).  own_row_packed: own[that index] = own-row update with
  * other_packed[p]. */
 int svb_pack_ctrl(const void *src, void *dst, int64_t count, int cbit, int64_t offset, void *stream);
+
+/* Half-slab gather / scatter for swapping a global (rank) qubit with a local
+ * one (dynamic layout): packed index p stands for local index
+ * insert_bit(offset + p, bit, value).  pack: dst[p] = src[that index];
+ * unpack: dst[that index] = src[p].  A swap of rank bit g with local bit l
+ * sends the half with local bit l != the rank's bit g to the partner rank
+ * (rank ^ (1 << g)) and unpacks the partner's half into the same positions:
+ * 8 L bytes each way instead of 16 L per global gate. */
+int svb_pack_half(const void *src, void *dst, int64_t count, int bit, int value, int64_t offset, void *stream);
+int svb_unpack_half(void *dst, const void *src, int64_t count, int bit, int value, int64_t offset, void *stream);
 int svb_exchange_own_row_packed(void *own, const void *other_packed, int64_t count, const double q[8],
                                 int own_is_low, int cbit, int64_t offset, void *stream);
 

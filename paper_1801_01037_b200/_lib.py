@@ -64,6 +64,8 @@ _SIGS = {
     "svb_exchange_own_row": ([_vp, _vp, _i64, _dp, _int, _int, _i64, _vp], _int),
     "svb_pair_update": ([_vp, _vp, _i64, _i64, _dp, _int, _vp], _int),
     "svb_pack_ctrl": ([_vp, _vp, _i64, _int, _i64, _vp], _int),
+    "svb_pack_half": ([_vp, _vp, _i64, _int, _int, _i64, _vp], _int),
+    "svb_unpack_half": ([_vp, _vp, _i64, _int, _int, _i64, _vp], _int),
     "svb_permute_qubits": ([_vp, _vp, _i64, ctypes.POINTER(_int), _int, _vp], _int),
     "svb_exchange_own_row_packed": ([_vp, _vp, _i64, _dp, _int, _int, _i64, _vp], _int),
     "svb_host_apply_1q": ([_vp, _i64, _dp, _int], _int),

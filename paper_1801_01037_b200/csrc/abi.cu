@@ -27,6 +27,10 @@ LaunchInfo launch_exchange_own_row(double2 *own, const double2 *other, int64_t c
                                    int own_is_low, int cbit, int64_t offset, cudaStream_t s);
 LaunchInfo launch_pair_update(double2 *lo_slab, double2 *hi_slab, int64_t begin, int64_t end,
                               const Gate &g, int cbit, cudaStream_t s);
+LaunchInfo launch_pack_half(const double2 *src, double2 *dst, int64_t count, int bit, int value, int64_t offset,
+                            cudaStream_t s);
+LaunchInfo launch_unpack_half(double2 *dst, const double2 *src, int64_t count, int bit, int value, int64_t offset,
+                              cudaStream_t s);
 LaunchInfo launch_pack_ctrl(const double2 *src, double2 *dst, int64_t count, int cbit, int64_t offset,
                             cudaStream_t s);
 LaunchInfo launch_exchange_packed(double2 *own, const double2 *other, int64_t count, const Gate &g,
@@ -341,6 +345,34 @@ int svb_pack_ctrl(const void *src, void *dst, int64_t count, int cbit, int64_t o
     prof_end((cudaStream_t)stream, li);
     g_launches += li.kernels;
     SVB_CHECK_LAUNCH("svb_pack_ctrl");
+    return SVB_OK;
+}
+
+int svb_pack_half(const void *src, void *dst, int64_t count, int bit, int value, int64_t offset, void *stream) {
+    if (!src || !dst || count < 0 || bit < 0 || bit > 62 || (value != 0 && value != 1) || offset < 0) {
+        set_error("bad arguments to svb_pack_half");
+        return SVB_EINVAL;
+    }
+    prof_begin((cudaStream_t)stream);
+    LaunchInfo li = launch_pack_half((const double2 *)src, (double2 *)dst, count, bit, value, offset,
+                                     (cudaStream_t)stream);
+    prof_end((cudaStream_t)stream, li);
+    g_launches += li.kernels;
+    SVB_CHECK_LAUNCH("svb_pack_half");
+    return SVB_OK;
+}
+
+int svb_unpack_half(void *dst, const void *src, int64_t count, int bit, int value, int64_t offset, void *stream) {
+    if (!src || !dst || count < 0 || bit < 0 || bit > 62 || (value != 0 && value != 1) || offset < 0) {
+        set_error("bad arguments to svb_unpack_half");
+        return SVB_EINVAL;
+    }
+    prof_begin((cudaStream_t)stream);
+    LaunchInfo li = launch_unpack_half((double2 *)dst, (const double2 *)src, count, bit, value, offset,
+                                       (cudaStream_t)stream);
+    prof_end((cudaStream_t)stream, li);
+    g_launches += li.kernels;
+    SVB_CHECK_LAUNCH("svb_unpack_half");
     return SVB_OK;
 }
 

@@ -85,6 +85,31 @@ __global__ void __launch_bounds__(kXThreads) k_pack_ctrl(const double2 *__restri
     }
 }
 
+// Half-slab gather / scatter for a global<->local qubit swap: the elements
+// whose local bit `bit` equals `value`, in index order (packed index p is
+// local index insert_bit(offset + p, bit, value)).
+__global__ void __launch_bounds__(kXThreads) k_pack_half(const double2 *__restrict__ src,
+                                                         double2 *__restrict__ dst, int64_t count, int bit,
+                                                         int value, int64_t offset) {
+    const int64_t base = int64_t(blockIdx.x) * kXThreads * kXUpt + threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < kXUpt; ++k) {
+        int64_t p = base + int64_t(k) * kXThreads;
+        if (p < count) dst[p] = src[insert_bit(offset + p, bit, value)];
+    }
+}
+
+__global__ void __launch_bounds__(kXThreads) k_unpack_half(double2 *__restrict__ dst,
+                                                           const double2 *__restrict__ src, int64_t count,
+                                                           int bit, int value, int64_t offset) {
+    const int64_t base = int64_t(blockIdx.x) * kXThreads * kXUpt + threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < kXUpt; ++k) {
+        int64_t p = base + int64_t(k) * kXThreads;
+        if (p < count) dst[insert_bit(offset + p, bit, value)] = src[p];
+    }
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(kXThreads) k_exchange_packed(double2 *__restrict__ own,
                                                                const double2 *__restrict__ other,
@@ -134,6 +159,20 @@ LaunchInfo launch_pack_ctrl(const double2 *src, double2 *dst, int64_t count, int
                             cudaStream_t s) {
     if (count <= 0) return LaunchInfo{0, PROF_EXCHANGE, 0};
     k_pack_ctrl<<<grid_for(count), kXThreads, 0, s>>>(src, dst, count, cbit, offset);
+    return LaunchInfo{1, PROF_EXCHANGE, count * 32};
+}
+
+LaunchInfo launch_pack_half(const double2 *src, double2 *dst, int64_t count, int bit, int value, int64_t offset,
+                            cudaStream_t s) {
+    if (count <= 0) return LaunchInfo{0, PROF_EXCHANGE, 0};
+    k_pack_half<<<grid_for(count), kXThreads, 0, s>>>(src, dst, count, bit, value, offset);
+    return LaunchInfo{1, PROF_EXCHANGE, count * 32};
+}
+
+LaunchInfo launch_unpack_half(double2 *dst, const double2 *src, int64_t count, int bit, int value, int64_t offset,
+                              cudaStream_t s) {
+    if (count <= 0) return LaunchInfo{0, PROF_EXCHANGE, 0};
+    k_unpack_half<<<grid_for(count), kXThreads, 0, s>>>(dst, src, count, bit, value, offset);
     return LaunchInfo{1, PROF_EXCHANGE, count * 32};
 }
 

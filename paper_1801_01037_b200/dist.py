@@ -78,6 +78,14 @@ class CudaCompute:
         self._lib.check(self.lib.svb_run_ops(ctypes.c_void_p(slab.data_ptr()), slab.shape[0], arr,
                                              nops, flags, self._sp()), "run_ops")
 
+    def pack_half(self, src, dst, count: int, bit: int, value: int, offset: int) -> None:
+        self._lib.check(self.lib.svb_pack_half(ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(dst.data_ptr()),
+                                               count, bit, value, offset, self._sp()), "pack_half")
+
+    def unpack_half(self, dst, src, count: int, bit: int, value: int, offset: int) -> None:
+        self._lib.check(self.lib.svb_unpack_half(ctypes.c_void_p(dst.data_ptr()), ctypes.c_void_p(src.data_ptr()),
+                                                 count, bit, value, offset, self._sp()), "unpack_half")
+
     def pack(self, src, dst, count: int, cbit: int, offset: int) -> None:
         self._lib.check(self.lib.svb_pack_ctrl(ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(dst.data_ptr()),
                                                count, cbit, offset, self._sp()), "pack")
@@ -109,6 +117,7 @@ class CudaCompute:
 @dataclass
 class ExchangeStats:
     exchanges: int = 0
+    swaps: int = 0
     elided: int = 0
     bytes_sent: int = 0
     bytes_recv: int = 0
@@ -123,7 +132,8 @@ class DistEngine:
     """This process's rank of a 2^k-way partitioned n-qubit state."""
 
     def __init__(self, n: int, compute=None, group=None, initial=None, chunk: int = DEFAULT_CHUNK,
-                 fuse: bool = True, elide_diagonal: bool = True, fma: bool = False, jit: bool = False):
+                 fuse: bool = True, elide_diagonal: bool = True, fma: bool = False, jit: bool = False,
+                 layout: bool = False):
         import torch.distributed as dist
 
         self.dist = dist
@@ -141,6 +151,10 @@ class DistEngine:
         self.chunk = max(1, min(int(chunk), self.L))
         self.fuse = fuse
         self.fma, self.jit = fma, jit  # local segments: FMA fused passes / NVRTC-specialised
+        # layout: run() swaps a global qubit into a local position (half-slab
+        # exchange) when a non-diagonal gate targets it, instead of one
+        # exchange per global gate; the identity layout is restored at the end
+        self.layout = layout
         self.elide_diagonal = elide_diagonal
         self.stats = ExchangeStats()
         if initial is not None:
@@ -227,6 +241,119 @@ class DistEngine:
         self.stats.bytes_sent += 16 * count
         self.stats.bytes_recv += 16 * count
 
+    def _swap(self, g: int, l: int) -> None:
+        """Swap rank bit (physical qubit) g with local bit l: each rank sends
+        the half of its slab whose bit l differs from its own bit g to the
+        partner and unpacks the partner's half into the same positions."""
+        self._flush()
+        dist = self.dist
+        partner = self.rank ^ (1 << (g - self.boundary))
+        v = 1 - ((self.rank >> (g - self.boundary)) & 1)  # the half that leaves
+        count = self.L // 2
+        m = self._buffers(count, True)
+        recv = self._bufs[0:2]
+        send = self._bufs[2:4]
+        nchunks = math.ceil(count / m)
+        peer = dist.get_global_rank(self.group, partner) if self.group is not None else partner
+
+        def post(ci):
+            off = ci * m
+            cnt = min(m, count - off)
+            self.compute.pack_half(self.slab, send[ci % 2], cnt, l, v, off)
+            ops = [dist.P2POp(dist.isend, send[ci % 2][:cnt], peer, self.group),
+                   dist.P2POp(dist.irecv, recv[ci % 2][:cnt], peer, self.group)]
+            return dist.batch_isend_irecv(ops)
+
+        works = post(0)
+        for ci in range(nchunks):
+            nxt = post(ci + 1) if ci + 1 < nchunks else None
+            for w in works:
+                w.wait()
+            off = ci * m
+            cnt = min(m, count - off)
+            self.compute.unpack_half(self.slab, recv[ci % 2], cnt, l, v, off)
+            works = nxt
+        self.stats.swaps += 1
+        self.stats.messages += nchunks
+        self.stats.bytes_sent += 16 * count
+        self.stats.bytes_recv += 16 * count
+
+    def _schedule_layout(self, ops: tuple) -> tuple[list, int]:
+        """Action list with dynamic global<->local qubit swaps.
+        The layout is kept as disjoint transpositions (global home position
+        <-> local home position): a non-diagonal gate on a qubit that sits at
+        a rank bit first swaps it with the local qubit whose next use as a
+        non-diagonal target is farthest away (Belady), or swaps back a local
+        qubit that was parked there.  Gates then address physical positions;
+        the transpositions are undone at the end."""
+        n, b = self.n, self.boundary
+        pi = list(range(n))   # logical -> physical
+        inv = list(range(n))  # physical -> logical
+        uses = [[] for _ in range(n)]  # op indices where a qubit is a non-diagonal target
+        for i, op in enumerate(ops):
+            if not _is_diag(op.gate):
+                uses[op.target].append(i)
+        ptr = [0] * n
+        actions, pending = [], []
+        elided = 0
+
+        def flush():
+            if pending:
+                actions.append(("local", tuple(pending)))
+                pending.clear()
+
+        def swap(gp, lp):
+            flush()
+            actions.append(("swap", gp, lp))
+            qg, ql = inv[gp], inv[lp]
+            pi[qg], pi[ql] = lp, gp
+            inv[gp], inv[lp] = ql, qg
+
+        def next_use(q, i):
+            u = uses[q]
+            while ptr[q] < len(u) and u[ptr[q]] < i:
+                ptr[q] += 1
+            return u[ptr[q]] if ptr[q] < len(u) else len(ops) + 1
+
+        for i, op in enumerate(ops):
+            g = op.gate
+            t = pi[op.target]
+            c = pi[op.control] if op.control is not None else None
+            if t >= b and not (self.elide_diagonal and _is_diag(g)):
+                if inv[t] >= b:  # a global qubit at home: park a local one there
+                    best, far = -1, -1
+                    for lp in range(b):
+                        q = inv[lp]
+                        if q != lp or lp == c:  # keep transpositions disjoint; keep the control local
+                            continue
+                        nu = next_use(q, i)
+                        if nu > far:
+                            best, far = lp, nu
+                    swap(t, best)
+                else:  # a parked local qubit p = inv[t]: swap it back to its home p
+                    swap(t, inv[t])
+                t = pi[op.target]
+                c = pi[op.control] if op.control is not None else None
+            if c is not None and c >= b:
+                if not (self.rank >> (c - b)) & 1:
+                    continue
+                c = None
+            if t < b:
+                pending.append(GateOp("single", g, t) if c is None else GateOp("controlled", g, t, c))
+                continue
+            bit_set = bool((self.rank >> (t - b)) & 1)  # diagonal on a rank bit: a local phase
+            s_ = complex(g.q22) if bit_set else complex(g.q11)
+            elided += 1
+            if s_ != 1:
+                d = Gate2x2(s_, 0, 0, s_)
+                pending.append(GateOp("single", d, 0) if c is None else
+                               GateOp("controlled", d, 1 if c == 0 else 0, c))
+        for gp in range(b, n):  # undo the parked transpositions
+            if inv[gp] != gp:
+                swap(gp, pi[gp])
+        flush()
+        return actions, elided
+
     # -- public ---------------------------------------------------------------
 
     def apply(self, op: GateOp) -> None:
@@ -255,6 +382,12 @@ class DistEngine:
         hit = self._scheds.get(id(ops))
         if hit is not None and hit[0] is ops:
             return hit[1], hit[2]
+        if self.layout:
+            actions, elided = self._schedule_layout(ops)
+            if len(self._scheds) >= 8:
+                self._scheds.pop(next(iter(self._scheds)))
+            self._scheds[id(ops)] = (ops, actions, elided)
+            return actions, elided
         saved, self._pending = self._pending, []
         actions, elided = [], 0
         exchange = self._exchange
@@ -290,6 +423,8 @@ class DistEngine:
                 self._pending = list(act[1])
                 self._pending_key = act[1]
                 self._flush()
+            elif act[0] == "swap":
+                self._swap(act[1], act[2])
             else:
                 self._exchange(act[1], act[2], act[3])
         self.stats.elided += elided
@@ -345,7 +480,8 @@ def bench_main(args) -> None:
     layers = int(os.environ.get("SVB_BENCH_LAYERS", "200"))
     circuit = workloads.random_layer_circuit(n, layers)
     nops = len(circuit.ops)
-    eng = DistEngine(n, fma=getattr(args, "fma", True), jit=getattr(args, "jit", True))
+    eng = DistEngine(n, fma=getattr(args, "fma", True), jit=getattr(args, "jit", True),
+                     layout=os.environ.get("SVB_DIST_LAYOUT", "1") != "0")
     stream = torch.cuda.current_stream()
 
     def step():
@@ -357,7 +493,7 @@ def bench_main(args) -> None:
     for _ in range(max(args.warmup, 0)):
         step()
     launches0 = _lib.launch_count()
-    stats0 = (eng.stats.exchanges, eng.stats.bytes_sent)
+    stats0 = (eng.stats.exchanges, eng.stats.bytes_sent, eng.stats.swaps)
     dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -383,6 +519,7 @@ def bench_main(args) -> None:
                                    f"2^26 amplitudes per GPU, {k} global qubits",
                        "n_qubits": n, "global_qubits": k, "parallelism": f"state partition x{world}"},
             "exchanges_per_step": ex / args.steps,
+            "layout_swaps_per_step": (eng.stats.swaps - stats0[2]) / args.steps,
             "nvlink_bytes_sent_per_gpu_per_step": sent / args.steps,
             "gpu_launches": _lib.launch_count() - launches0,
             "check": {"norm": norm},

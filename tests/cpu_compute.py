@@ -19,6 +19,11 @@ def _insert_one(p: np.ndarray, cbit: int) -> np.ndarray:
     return ((p >> cbit) << (cbit + 1)) | (1 << cbit) | low
 
 
+def _insert(p: np.ndarray, bit: int, value: int) -> np.ndarray:
+    low = p & ((1 << bit) - 1)
+    return ((p >> bit) << (bit + 1)) | (value << bit) | low
+
+
 class CpuCompute:
     def zeros(self, count):
         return torch.zeros(count, dtype=torch.complex128)
@@ -29,9 +34,17 @@ class CpuCompute:
     def to_numpy(self, t):
         return t.numpy().copy()
 
-    def run_ops(self, slab, ops, fuse=True, strict=False):
+    def run_ops(self, slab, ops, fuse=True, strict=False, fma=False, jit=False):
         a = slab.numpy()
         oracle.run_ops(a, [(op.gate, op.target, op.control) for op in ops])
+
+    def pack_half(self, src, dst, count, bit, value, offset):
+        idx = _insert(np.arange(offset, offset + count, dtype=np.int64), bit, value)
+        dst.numpy()[:count] = src.numpy()[idx]
+
+    def unpack_half(self, dst, src, count, bit, value, offset):
+        idx = _insert(np.arange(offset, offset + count, dtype=np.int64), bit, value)
+        dst.numpy()[idx] = src.numpy()[:count]
 
     def pack(self, src, dst, count, cbit, offset):
         idx = _insert_one(np.arange(offset, offset + count, dtype=np.int64), cbit)

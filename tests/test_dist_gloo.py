@@ -54,7 +54,7 @@ def _circuit(n, k, seed):
     return Circuit(n, tuple(ops))
 
 
-def _worker(rank, world, port, n, chunk, elide, queue):
+def _worker(rank, world, port, n, chunk, elide, layout, queue):
     sys.path.insert(0, HERE)
     sys.path.insert(0, os.path.dirname(HERE))
     sys.path.insert(0, os.path.join(os.path.dirname(HERE), "oracle"))
@@ -68,7 +68,7 @@ def _worker(rank, world, port, n, chunk, elide, queue):
         k = world.bit_length() - 1
         a0 = w.seeded_state(n, 5)
         circ = _circuit(n, k, seed=n * 10 + world)
-        eng = DistEngine(n, compute=CpuCompute(), initial=a0, chunk=chunk, elide_diagonal=elide)
+        eng = DistEngine(n, compute=CpuCompute(), initial=a0, chunk=chunk, elide_diagonal=elide, layout=layout)
         eng.run(circ)
         nrm = eng.norm2()
         full = eng.gather()
@@ -77,18 +77,20 @@ def _worker(rank, world, port, n, chunk, elide, queue):
 
             want = oracle.run_ops(a0.copy(), w.oracle_ops(circ))
             queue.put((bool(np.array_equal(full, want)), float(np.max(np.abs(full - want))), nrm,
-                       eng.stats.exchanges, eng.stats.elided))
+                       eng.stats.exchanges + eng.stats.swaps, eng.stats.elided))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n,chunk,elide", [(2, 9, 16, True), (2, 9, 1 << 20, False),
-                                                 (4, 10, 7, True), (4, 8, 3, False)])
-def test_dist_engine_matches_oracle(world, n, chunk, elide):
+@pytest.mark.parametrize("world,n,chunk,elide,layout", [(2, 9, 16, True, False), (2, 9, 1 << 20, False, False),
+                                                        (4, 10, 7, True, False), (4, 8, 3, False, False),
+                                                        (2, 9, 16, True, True), (4, 10, 7, True, True),
+                                                        (4, 8, 3, False, True)])
+def test_dist_engine_matches_oracle(world, n, chunk, elide, layout):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, chunk, elide, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, chunk, elide, layout, q)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:

@@ -116,3 +116,36 @@ def test_dist_engine_single_rank_on_gpu(cuda_ok):
         assert abs(eng.norm2() - 1) < 1e-12
     finally:
         dist.destroy_process_group()
+
+
+def test_half_slab_swap_kernels(cuda_ok):
+    # svb_pack_half / svb_unpack_half: the two halves of a global<->local
+    # qubit swap (DistEngine layout mode).  Emulate two ranks on one GPU and
+    # check the swapped slabs against the index permutation that exchanges
+    # rank bit g and local bit l.
+    import torch
+
+    from paper_1801_01037_b200.dist import CudaCompute
+
+    cc = CudaCompute()
+    rng = np.random.default_rng(3)
+    n_loc = 10
+    L = 1 << n_loc
+    for l in (0, 4, n_loc - 1):
+        slabs = [w.random_state_array(rng, n_loc) for _ in range(2)]
+        full = np.concatenate(slabs)  # rank bit = bit n_loc of the global index
+        d = [cc.from_numpy(x) for x in slabs]
+        bufs = [cc.zeros(L // 2) for _ in range(2)]
+        for r in range(2):  # rank r sends its half with bit l != r
+            cc.pack_half(d[r], bufs[r], L // 2, l, 1 - r, 0)
+        for r in range(2):
+            for off in range(0, L // 2, 100):  # chunked, like the pipelined exchange
+                cnt = min(100, L // 2 - off)
+                cc.unpack_half(d[r], bufs[1 - r][off:off + cnt], cnt, l, 1 - r, off)
+        torch.cuda.synchronize()
+        idx = np.arange(2 * L)
+        bl, bg = (idx >> l) & 1, (idx >> n_loc) & 1
+        src = idx ^ ((bl ^ bg) << l) ^ ((bl ^ bg) << n_loc)  # swap the two bits
+        want = full[src]
+        got = np.concatenate([cc.to_numpy(x) for x in d])
+        assert np.array_equal(got, want)
