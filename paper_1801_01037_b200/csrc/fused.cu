@@ -390,6 +390,7 @@ __global__ void __launch_bounds__(FTHREADS, FCTAS_PER_SM) k_fused(double2 *__res
 
 struct PlanPass {
     uint64_t S = 0;  // global qubits in the tile
+    uint64_t T = 0;  // targets of its non-diagonal ops
     std::vector<int> ops;
 };
 
@@ -604,15 +605,24 @@ static std::vector<PlanPass> plan_beam(int n, const svb_op *ops, int nops, int f
         return popc(S) + std::max(0, nlow - popc(S & anchor));
     };
     std::vector<Blocking> cls(nops);
-    for (int i = 0; i < nops; ++i) cls[i] = op_class(ops[i]);
+    std::vector<uint64_t> tgt(nops);  // non-diagonal target bit (0 for diagonal ops)
+    for (int i = 0; i < nops; ++i) {
+        cls[i] = op_class(ops[i]);
+        tgt[i] = make_gate(ops[i].q).kind == K_DIAG ? 0 : uint64_t(1) << ops[i].target;
+    }
+    // SVB_FUSE_TCAP: at most this many distinct non-diagonal targets per pass
+    static const int tcap = getenv("SVB_FUSE_TCAP") ? atoi(getenv("SVB_FUSE_TCAP")) : 64;
     const int window = 1024;
     auto absorb = [&](std::vector<char> &done, int first, PlanPass &p, bool mark) {
         Blocking blocked;
         int cnt = 0;
+        uint64_t T = p.T;
         for (int i = first; i < nops && i < first + window && (int)p.ops.size() + cnt < FMAXG; ++i) {
             if (done[i]) continue;
             uint64_t m = op_mask(ops[i]);
-            if (hoistable(cls[i], blocked) && (m & ~p.S) == 0) {
+            const bool tfit = !(tgt[i] & ~T) || popc(T) < tcap;
+            if (hoistable(cls[i], blocked) && (m & ~p.S) == 0 && tfit) {
+                T |= tgt[i];
                 if (mark) {
                     p.ops.push_back(i);
                     done[i] = 1;
@@ -623,6 +633,7 @@ static std::vector<PlanPass> plan_beam(int n, const svb_op *ops, int nops, int f
                 block_add(blocked, cls[i]);
             }
         }
+        if (mark) p.T = T;
         return cnt;
     };
     // candidate growths of p.S (distinct op masks, ready, fitting)
