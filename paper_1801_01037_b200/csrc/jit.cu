@@ -1013,9 +1013,10 @@ static bool nvrtc_compile(const std::string &src, std::vector<char> &cubin, std:
         log = "nvrtcCreateProgram failed";
         return false;
     }
-    const char *opts[] = {"-arch=sm_100a", "-std=c++17", "-default-device", "-fmad=false", "-lineinfo"};
-    static const int nopts = getenv("SVB_JIT_LINEINFO") ? 5 : 4;  // for ncu source pages
-    if (nv.compile(prog, nopts, opts) != 0) {
+    std::vector<const char *> opts = {"-arch=sm_100a", "-std=c++17", "-default-device", "-fmad=false"};
+    if (getenv("SVB_JIT_LINEINFO")) opts.push_back("-lineinfo");  // for ncu source pages
+    if (const char *x = getenv("SVB_JIT_OPT")) opts.push_back(x);   // one extra option (measurement)
+    if (nv.compile(prog, (int)opts.size(), opts.data()) != 0) {
         size_t n = 0;
         nv.log_size(prog, &n);
         log.assign(n, '\0');
