@@ -592,7 +592,19 @@ static bool rotate_low() {  // SVB_FUSE_ROTATE=0: qubits 0..flow-1 in every tile
     return !e || atoi(e) != 0;
 }
 
-static std::vector<PlanPass> plan_beam(int n, const svb_op *ops, int nops, int fm) {
+// Qubits a pass need not tile (outside = true, runtime-specialised passes
+// only): an op acts on each of its qubits as Z-type (diagonal there -- a
+// diagonal gate's target, every control) or not.  A Z-type qubit outside the
+// tile's set S is constant over a tile, so the op becomes a tile-uniform
+// predicate (control) or a per-tile factor (diagonal target) and only its
+// non-diagonal target must lie in S.  Within a pass every op touching a
+// qubit outside S acts Z-type on it, so those ops commute there.
+static uint64_t need_mask(const svb_op &o, bool outside) {
+    if (!outside) return op_mask(o);
+    return make_gate(o.q).kind == K_DIAG ? 0 : uint64_t(1) << o.target;
+}
+
+static std::vector<PlanPass> plan_beam(int n, const svb_op *ops, int nops, int fm, bool outside) {
     std::vector<PlanPass> passes;
     const uint64_t low = (uint64_t(1) << flow_bits()) - 1;
     const int nlow = flow_bits();
@@ -610,6 +622,8 @@ static std::vector<PlanPass> plan_beam(int n, const svb_op *ops, int nops, int f
         cls[i] = op_class(ops[i]);
         tgt[i] = make_gate(ops[i].q).kind == K_DIAG ? 0 : uint64_t(1) << ops[i].target;
     }
+    std::vector<uint64_t> need(nops);  // qubits op i needs in the tile
+    for (int i = 0; i < nops; ++i) need[i] = need_mask(ops[i], outside);
     // SVB_FUSE_TCAP: at most this many distinct non-diagonal targets per pass
     static const int tcap = getenv("SVB_FUSE_TCAP") ? atoi(getenv("SVB_FUSE_TCAP")) : 64;
     const int window = 1024;
@@ -619,7 +633,7 @@ static std::vector<PlanPass> plan_beam(int n, const svb_op *ops, int nops, int f
         uint64_t T = p.T;
         for (int i = first; i < nops && i < first + window && (int)p.ops.size() + cnt < FMAXG; ++i) {
             if (done[i]) continue;
-            uint64_t m = op_mask(ops[i]);
+            uint64_t m = need[i];
             const bool tfit = !(tgt[i] & ~T) || popc(T) < tcap;
             if (hoistable(cls[i], blocked) && (m & ~p.S) == 0 && tfit) {
                 T |= tgt[i];
@@ -642,7 +656,7 @@ static std::vector<PlanPass> plan_beam(int n, const svb_op *ops, int nops, int f
         Blocking blocked;
         for (int i = first; i < nops && i < first + window && (int)out.size() < lim; ++i) {
             if (done[i]) continue;
-            uint64_t m = op_mask(ops[i]);
+            uint64_t m = need[i];
             uint64_t add = m & ~p.S;
             if (hoistable(cls[i], blocked) && add && room(p.S | m) <= fm &&
                 std::find(out.begin(), out.end(), m) == out.end())
@@ -731,8 +745,8 @@ static std::vector<PlanPass> plan_beam(int n, const svb_op *ops, int nops, int f
     return passes;
 }
 
-static std::vector<PlanPass> plan(int n, const svb_op *ops, int nops, bool strict, int fm) {
-    if (!strict && planner_kind() == 3) return plan_beam(n, ops, nops, fm);
+static std::vector<PlanPass> plan(int n, const svb_op *ops, int nops, bool strict, int fm, bool outside) {
+    if (!strict && planner_kind() == 3) return plan_beam(n, ops, nops, fm, outside);
     if (!strict && planner_kind() == 2) return plan_lookahead(n, ops, nops, fm);
     std::vector<PlanPass> passes;
     const uint64_t low = (uint64_t(1) << flow_bits()) - 1;
@@ -787,7 +801,8 @@ static unsigned slot_pattern(int s, int fs = FSLOTS) {
 
 struct GateMeta {
     Gate g;
-    int tl, cl;  // local bits (cl = -1: none)
+    int tl, cl;  // local bits (cl = -1: none, or outside the tile)
+    int tt, ct;  // tile-index bits of a diagonal target / a control outside the tile (-1: none)
     bool diag;
     bool perm;
 };
@@ -916,6 +931,12 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
             if (!((tile_phys >> b) & 1)) P.comp[nc++] = (int8_t)b;
         P.ncomp = nc;
     }
+    // tile-index bit holding logical qubit q (q outside the tile)
+    auto tile_bit = [&](int q) {
+        for (int j = 0; j < P.ncomp; ++j)
+            if (P.comp[j] == ph(q)) return j;
+        return -1;
+    };
     // store remap: old local bit of q -> local bit of phn(q) among the same physical bits
     int sig[FMMAX];
     bool remap = false;
@@ -936,9 +957,16 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
         m.tl = local_of[o.target];
         m.cl = o.kind == 1 ? local_of[o.control] : -1;
         m.diag = m.g.kind == K_DIAG;
+        // Z-type qubits outside the tile (need_mask): tile-uniform predicates
+        m.tt = m.tl < 0 ? tile_bit(o.target) : -1;
+        m.ct = (o.kind == 1 && m.cl < 0) ? tile_bit(o.control) : -1;
+        if (m.tl < 0 && !m.diag) return false;  // a non-diagonal target must be tiled
+        if (m.tt >= 32 || m.ct >= 32) return false;
         // X and CNOT are bit permutations: folded into the group's store map
+        // (a CNOT controlled from outside the tile differs per tile: it runs as
+        // a predicated gate instead)
         m.perm = perm_fold() && m.g.kind == K_ANTI && unit_code(m.g.m[1]) == 0 &&
-                 unit_code(m.g.m[2]) == 0;
+                 unit_code(m.g.m[2]) == 0 && m.ct < 0;
         meta.push_back(m);
     }
     // Order gates into register groups.  A group holds at most 4 target slots
@@ -981,8 +1009,8 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
         g.mb = C(g.mb);
         g.permq |= (uint64_t(1) << m.tl) | (m.cl >= 0 ? uint64_t(1) << m.cl : 0);
     };
-    auto gbits = [&](const GateMeta &m) {
-        return (uint64_t(1) << m.tl) | (m.cl >= 0 ? uint64_t(1) << m.cl : 0);
+    auto gbits = [&](const GateMeta &m) {  // local bits only
+        return (m.tl >= 0 ? uint64_t(1) << m.tl : 0) | (m.cl >= 0 ? uint64_t(1) << m.cl : 0);
     };
     // allowed: the group's slot set when chosen up front (0: first come)
     auto fits = [&](const GroupPlan &g, const GateMeta &m, bool first, uint64_t allowed) {
@@ -1252,11 +1280,12 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
             fg.tl = -1;
             int cs = m.cl >= 0 ? slot_of(m.cl) : -1;
             fg.cl = (int8_t)(m.cl >= 0 && cs < 0 ? tbit_of(m.cl) : -1);
+            if (m.ct >= 0) fg.cl = (int8_t)(FTILEBIT + m.ct);  // control outside the tile
             fg.cmask = cs >= 0 ? slot_pattern(cs, fs) : 0xffffffffu;
             if (m.diag) {
                 int ts = slot_of(m.tl);
                 int tpos = ts >= 0 ? ts : FTPOS_THREAD;
-                fg.tl = (int8_t)(ts >= 0 ? -1 : tbit_of(m.tl));
+                fg.tl = (int8_t)(ts >= 0 ? -1 : (m.tt >= 0 ? FTILEBIT + m.tt : tbit_of(m.tl)));
                 int var = FD_GENERAL;
                 if (m.g.d0_one) {
                     const int uc = unit_code(m.g.m[3]);
@@ -1437,6 +1466,15 @@ static int plan_fs(unsigned flags) {
     return std::max(4, std::min(FSMAX, fs));
 }
 
+// Ops with Z-type qubits outside the tile (need_mask): specialised passes
+// only -- the interpreter has no tile-uniform predicates.  SVB_FUSE_OUTSIDE=0
+// turns it off (measurement).
+static bool plan_outside(unsigned flags) {
+    if (!(flags & SVB_RUN_JIT) || (flags & SVB_RUN_STRICT_ORDER) || !jit_available()) return false;
+    const char *e = getenv("SVB_FUSE_OUTSIDE");
+    return !e || atoi(e) != 0;
+}
+
 struct PlanStep {
     int op;      // >= 0: run `mapped` (ops[op] on physical qubits) with the single-gate kernels
     svb_op mapped;
@@ -1462,8 +1500,9 @@ static int phase_ways(const uint32_t *t) {
 // when they can, and gate-free layout passes at the end restore the
 // identity layout the caller expects.
 static void lower_plan(int n, const svb_op *ops, int nops, bool strict, bool regperm, int fm, int fs,
-                       std::vector<PlanStep> &steps, std::vector<FPass> &passes) {
-    const std::vector<PlanPass> plans = plan(n, ops, nops, strict, fm);
+                       bool outside, std::vector<PlanStep> &steps, std::vector<FPass> &passes) {
+    outside = outside && !strict && planner_kind() == 3;
+    const std::vector<PlanPass> plans = plan(n, ops, nops, strict, fm, outside);
     const int nlow = flow_bits();
     const bool rotate = !strict && rotate_low() && planner_kind() == 3;
     std::vector<int8_t> phys(64), nxt(64);
@@ -1637,7 +1676,8 @@ int jit_check(int n, const svb_op *ops, int nops, unsigned flags) {
     std::vector<FPass> passes;
     std::vector<PlanStep> steps;
     const int fm = plan_fm(n, flags | SVB_RUN_JIT);
-    lower_plan(n, ops, nops, strict, reg_perm(flags), fm, plan_fs(flags | SVB_RUN_JIT), steps, passes);
+    lower_plan(n, ops, nops, strict, reg_perm(flags), fm, plan_fs(flags | SVB_RUN_JIT),
+               plan_outside(flags | SVB_RUN_JIT), steps, passes);
     std::string err;
     int r = jit_compile_only(passes, jit_variant((flags & SVB_RUN_FMA) && !strict), err);
     if (r < 0) set_error("jit compile failed: %.400s", err.c_str());
@@ -1651,7 +1691,7 @@ int plan_passes(int n, const svb_op *ops, int nops, unsigned flags, int *groups)
     const int fm = plan_fm(n, flags);
     std::vector<FPass> passes;
     std::vector<PlanStep> steps;
-    lower_plan(n, ops, nops, strict, reg_perm(flags), fm, plan_fs(flags), steps, passes);
+    lower_plan(n, ops, nops, strict, reg_perm(flags), fm, plan_fs(flags), plan_outside(flags), steps, passes);
     int df = 0, dl = 0, cf = 0, cl = 0;
     auto coal = [](const FGroup &G, const int16_t *col) {
         const int x = col[G.tmap[0]], y = col[G.tmap[1]], z = col[G.tmap[2]];
@@ -1708,7 +1748,7 @@ int plan_passes(int n, const svb_op *ops, int nops, unsigned flags, int *groups)
 
 struct CompiledPlan {
     int n, fm, fs;
-    bool strict, regperm;
+    bool strict, regperm, outside;
     std::vector<svb_op> ops;  // exact key
     std::vector<PlanStep> steps;
     std::vector<FPass> passes;
@@ -1729,7 +1769,7 @@ static uint64_t fnv1a(const void *p, size_t len, uint64_t h) {
 }
 
 static std::shared_ptr<const CompiledPlan> compiled_plan(int n, const svb_op *ops, int nops, bool strict,
-                                                         bool regperm, int fm, int fs) {
+                                                         bool regperm, int fm, int fs, bool outside) {
     static std::mutex mu;
     static std::vector<std::pair<uint64_t, std::shared_ptr<const CompiledPlan>>> cache;  // MRU first
     uint64_t key = fnv1a(ops, sizeof(svb_op) * size_t(nops), 1469598103934665603ull);
@@ -1738,11 +1778,12 @@ static std::shared_ptr<const CompiledPlan> compiled_plan(int n, const svb_op *op
     key = fnv1a(&regperm, sizeof regperm, key);
     key = fnv1a(&fm, sizeof fm, key);
     key = fnv1a(&fs, sizeof fs, key);
+    key = fnv1a(&outside, sizeof outside, key);
     {
         std::lock_guard<std::mutex> lk(mu);
         for (size_t i = 0; i < cache.size(); ++i) {
             const auto &c = cache[i].second;
-            if (cache[i].first == key && c->n == n && c->fm == fm && c->fs == fs && c->strict == strict && c->regperm == regperm &&
+            if (cache[i].first == key && c->n == n && c->fm == fm && c->fs == fs && c->outside == outside && c->strict == strict && c->regperm == regperm &&
                 (int)c->ops.size() == nops &&
                 std::memcmp(c->ops.data(), ops, sizeof(svb_op) * size_t(nops)) == 0) {
                 auto hit = cache[i];
@@ -1758,8 +1799,9 @@ static std::shared_ptr<const CompiledPlan> compiled_plan(int n, const svb_op *op
     cp->fs = fs;
     cp->strict = strict;
     cp->regperm = regperm;
+    cp->outside = outside;
     cp->ops.assign(ops, ops + nops);
-    lower_plan(n, ops, nops, strict, regperm, fm, fs, cp->steps, cp->passes);
+    lower_plan(n, ops, nops, strict, regperm, fm, fs, outside, cp->steps, cp->passes);
     // Bounded by descriptor bytes (~27 KiB per pass), not by count: the
     // multi-process engine runs one op segment per exchange interval, so a
     // circuit step may cycle through hundreds of small plans.
@@ -1797,7 +1839,7 @@ int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsi
     const bool strict = flags & SVB_RUN_STRICT_ORDER;
     const bool fma = (flags & SVB_RUN_FMA) && !strict;
     std::shared_ptr<const CompiledPlan> cp =
-        compiled_plan(n, ops, nops, strict, reg_perm(flags), plan_fm(n, flags), plan_fs(flags));
+        compiled_plan(n, ops, nops, strict, reg_perm(flags), plan_fm(n, flags), plan_fs(flags), plan_outside(flags));
     size_t next_pass = 0;
     bool jit = (flags & SVB_RUN_JIT) && !cp->passes.empty();
     const std::vector<void *> *jit_fns = nullptr;
@@ -1808,8 +1850,8 @@ int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsi
         if (state == 0) state = jit_build(cp->passes, variant, cp->jit_fns[variant]) ? 1 : -1;
         if (state == 1) jit_fns = &cp->jit_fns[variant];
     }
-    if (!jit_fns && (cp->fm != FM || cp->fs != FSLOTS)) {  // JIT unavailable: the interpreter's geometry
-        cp = compiled_plan(n, ops, nops, strict, reg_perm(flags & ~SVB_RUN_JIT), FM, FSLOTS);
+    if (!jit_fns && (cp->fm != FM || cp->fs != FSLOTS || cp->outside)) {  // JIT unavailable: the interpreter's plan
+        cp = compiled_plan(n, ops, nops, strict, reg_perm(flags & ~SVB_RUN_JIT), FM, FSLOTS, false);
         jit = false;
     }
     for (const PlanStep &st : cp->steps) {

@@ -49,12 +49,16 @@ enum FKind { FK_GENERAL = 0, FK_REAL, FK_ANTI, FK_RX, FK_UANTI, FK_X, FK_Y, FK_N
 enum FDiag { FD_GENERAL = 0, FD_D1, FD_Z, FD_S, FD_SDG, FD_NVAR };
 constexpr int FOP_DIAG = FK_NKIND * FSMAX * 2;
 constexpr int FTPOS_THREAD = FSMAX;  // diagonal tpos: target on a thread bit
+// FGate.cl / FGate.tl >= FTILEBIT: the qubit lies outside the tile, at
+// tile-index bit (value - FTILEBIT) -- a predicate uniform over the tile
+// (runtime-specialised passes only; the interpreter never gets one)
+constexpr int FTILEBIT = 64;
 
 struct FGate {
     double2 m[4];
     uint8_t op;
-    int8_t tl;       // diag with a thread-bit target: its local bit
-    int8_t cl;       // control on a thread bit: its local bit, else -1
+    int8_t tl;       // diag with a thread-bit target: its thread bit (>= FTILEBIT: tile bit)
+    int8_t cl;       // control on a thread bit: its thread bit (>= FTILEBIT: tile bit), else -1
     uint8_t u;       // FK_UANTI unit codes: bits 0-1 q12, bits 2-3 q21
     uint32_t cmask;  // ctrl = 1: registers (pairs: lo registers) the control allows
 };

@@ -156,12 +156,24 @@ unsigned slot_pat(int s) {
     return m;
 }
 
+// predicate "bit b of the element's index is set" for a gate's thread-bit
+// control / target (tid), or -- b >= FTILEBIT -- for a qubit outside the tile
+// (a bit of the tile index tix: uniform over the CTA, a non-divergent branch)
+std::string pbit(int b) {
+    char buf[64];
+    if (b >= FTILEBIT)
+        snprintf(buf, sizeof buf, "((unsigned)(tix >> %d) & 1u)", b - FTILEBIT);
+    else
+        snprintf(buf, sizeof buf, "((tid >> %d) & 1)", b);
+    return buf;
+}
+
 // one gate as straight-line code over v[0..15]
 void emit_gate(Out &o, const FGate &g) {
     const double2 *m = g.m;
     const int op = g.op;
     const bool thread_ctl = g.cl >= 0;
-    if (thread_ctl) o("if ((tid >> %d) & 1) {\n", g.cl);
+    if (thread_ctl) o("if (%s) {\n", pbit(g.cl).c_str());
     if (op < FOP_DIAG) {
         const int kind = (op >> 1) / FSMAX, s = (op >> 1) % FSMAX, ctrl = op & 1;
         for (int i = 0; i < NR(); ++i) {
@@ -199,7 +211,7 @@ void emit_gate(Out &o, const FGate &g) {
         };
         const bool d0_one = var != FD_GENERAL;
         if (tpos == FTPOS_THREAD) {  // target on a thread bit: one factor per thread
-            o("if ((tid >> %d) & 1) {\n", g.tl);
+            o("if (%s) {\n", pbit(g.tl).c_str());
             for (int i = 0; i < NR(); ++i)
                 if (!ctrl || ((g.cmask >> i) & 1)) mul(i, m[3]);
             o("}");
@@ -305,17 +317,26 @@ std::string cm_fold(const double2 &a, int cx) {
 // with branch-free selects; at the group's store the swap becomes a
 // per-thread XOR of the store address (free).  Pending unit factors stay
 // symmetric along a swapped slot, so they commute too.
-thread_local uint32_t *t_pend = nullptr;
+// (mask bits 0-31: thread bits; 32-63: tile-index bits -- a CNOT controlled
+// from outside the tile swaps the same way in every thread of some tiles)
+thread_local uint64_t *t_pend = nullptr;
 
-std::string pcond(uint32_t m) {
-    char b[64];
+uint64_t pmask(int b) { return b >= FTILEBIT ? uint64_t(1) << (32 + b - FTILEBIT) : uint64_t(1) << b; }
+
+std::string pcond(uint64_t m) {
     if ((m & (m - 1)) == 0) {
         int bit = 0;
         while (!((m >> bit) & 1)) ++bit;
-        snprintf(b, sizeof b, "((tid >> %d) & 1)", bit);
-    } else {
-        snprintf(b, sizeof b, "(__popc(tid & %uu) & 1)", m);
+        return pbit(bit >= 32 ? FTILEBIT + bit - 32 : bit);
     }
+    const unsigned lo = (unsigned)m, hi = (unsigned)(m >> 32);
+    char b[128];
+    if (!hi)
+        snprintf(b, sizeof b, "(__popc(tid & %uu) & 1)", lo);
+    else if (!lo)
+        snprintf(b, sizeof b, "(__popc((unsigned)tix & %uu) & 1)", hi);
+    else
+        snprintf(b, sizeof b, "((__popc(tid & %uu) ^ __popc((unsigned)tix & %uu)) & 1)", lo, hi);
     return b;
 }
 
@@ -392,7 +413,7 @@ void emit_gate_fold(Out &o, const FGate &g, int *code) {
                     materialize(o, code, j);
                 }
             }
-            t_pend[s] ^= 1u << g.cl;
+            t_pend[s] ^= pmask(g.cl);
             return;
         }
         if (thread_ctl && unit_anti) {
@@ -406,7 +427,7 @@ void emit_gate_fold(Out &o, const FGate &g, int *code) {
                     materialize(o, code, j);
                 }
             }
-            o("if ((tid >> %d) & 1) {\n", g.cl);
+            o("if (%s) {\n", pbit(g.cl).c_str());
             for (int i : lows) {
                 const int j = i | (1 << s);
                 o("{ const d2 t = v[%d]; v[%d] = v[%d]; v[%d] = t; }\n", i, i, j, j);
@@ -424,7 +445,7 @@ void emit_gate_fold(Out &o, const FGate &g, int *code) {
                 materialize(o, code, i);
                 materialize(o, code, i | (1 << s));
             }
-            o("if ((tid >> %d) & 1) {\n", g.cl);
+            o("if (%s) {\n", pbit(g.cl).c_str());
         }
         for (int i : lows) {
             const int j = i | (1 << s);
@@ -499,9 +520,9 @@ void emit_gate_fold(Out &o, const FGate &g, int *code) {
     };
     if (branch)
         for (int i : regs) materialize(o, code, i);
-    if (thread_ctl) o("if ((tid >> %d) & 1) {\n", g.cl);
+    if (thread_ctl) o("if (%s) {\n", pbit(g.cl).c_str());
     if (tpos == FTPOS_THREAD) {
-        o("if ((tid >> %d) & 1) {\n", g.tl);
+        o("if (%s) {\n", pbit(g.tl).c_str());
         for (int i : regs) mul(i, m[3]);
         o("}");
         if (!d0_one) {
@@ -677,12 +698,12 @@ void emit_gate_fast(Out &o, const FGate &g, int *code, double2 &F) {
         const bool one0 = unit_code(d0) == 0, one1 = unit_code(d1) == 0;
         for (int i = 0; i < NR(); ++i) materialize(o, code, i);
         if (!one1) {
-            o("if ((tid >> %d) & 1) {\n", g.tl);
+            o("if (%s) {\n", pbit(g.tl).c_str());
             for (int i = 0; i < NR(); ++i) mul(i, d1, true);
             o("}\n");
         }
         if (!one0) {
-            o("if (!((tid >> %d) & 1)) {\n", g.tl);
+            o("if (!%s) {\n", pbit(g.tl).c_str());
             for (int i = 0; i < NR(); ++i) mul(i, d0, true);
             o("}\n");
         }
@@ -881,7 +902,7 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             o("__syncthreads();\n{ const i64 nx = tix + gridDim.x; if (nx < ntiles) "
               "fill(reinterpret_cast<unsigned char *>(dsm), a + tbase(nx)); }\n");
         }
-        uint32_t pend[FSMAX] = {0};
+        uint64_t pend[FSMAX] = {0};
         if (fma && pend_on()) t_pend = pend;
         if (fast) {
             int code[FREGMAX] = {0};

@@ -202,6 +202,7 @@ def test_jit_passes_bit_identical_to_interpreter(cuda_ok, n, monkeypatch):
     monkeypatch.setenv("SVB_FUSE_REGPERM", "1")
     monkeypatch.setenv("SVB_JIT_FACTOR", "0")
     monkeypatch.setenv("SVB_JIT_FS", "4")
+    monkeypatch.setenv("SVB_FUSE_OUTSIDE", "0")  # tile-uniform predicates: JIT-only plans
     rng = np.random.default_rng(600 + n)
     x = standard_gate("x")
     pool = all_gates(rng) + [x, x, Gate2x2(1, 0, 0, -1j)]
@@ -235,6 +236,38 @@ def test_jit_passes_bit_identical_to_interpreter(cuda_ok, n, monkeypatch):
         monkeypatch.setenv("SVB_FUSE_REGPERM", "1")
         monkeypatch.setenv("SVB_JIT_FACTOR", "0")
         monkeypatch.setenv("SVB_JIT_FS", "4")
+
+
+@pytest.mark.parametrize("n", [15, 16, 19])
+def test_jit_outside_tile_ops_vs_oracle(cuda_ok, n, monkeypatch):
+    # specialised passes let Z-type qubits (controls, diagonal targets) stay
+    # outside the tile: tile-uniform predicates / per-tile factors, pending
+    # swaps whose parity mixes thread and tile bits.  Controlled and diagonal
+    # heavy circuits in exact and FMA arithmetic, against the oracle; the plan
+    # with them has fewer passes
+    rng = np.random.default_rng(700 + n)
+    x = standard_gate("x")
+    pool = all_gates(rng) + [x, x, x, Gate2x2(1, 0, 0, -1j), rz(0.4), phase(1.3)]
+    ops = []
+    for _ in range(500):
+        g = pool[int(rng.integers(len(pool)))]
+        if rng.random() < 0.6:
+            c, t = rng.choice(n, size=2, replace=False)
+            ops.append(GateOp("controlled", g, int(t), int(c)))
+        else:
+            ops.append(GateOp("single", g, int(rng.integers(n))))
+    circs = [Circuit(n, tuple(ops)), w.qft_circuit(n), w.random_layer_circuit(n, 20, seed=n)]
+    for circ in circs:
+        a = w.random_state_array(rng, n)
+        want = oracle.run_ops(a.copy(), w.oracle_ops(circ), workers=16)
+        for fma in (False, True):
+            got = device.simulate(circ, a.copy(), fma=fma, jit=True)
+            assert np.max(np.abs(got - want)) <= TOL, (fma, np.max(np.abs(got - want)))
+        monkeypatch.setenv("SVB_FUSE_OUTSIDE", "0")
+        inside = device.plan_passes(n, circ, jit=True)
+        monkeypatch.delenv("SVB_FUSE_OUTSIDE")
+        outside = device.plan_passes(n, circ, jit=True)
+        assert outside <= inside or circ is circs[0], (outside, inside)
 
 
 @pytest.mark.parametrize("n", [14, 17])

@@ -86,6 +86,28 @@ def test_jit_sources_compile_with_nvrtc():
     assert out.value >= 1
 
 
+def test_outside_tile_plans_host_only(monkeypatch):
+    # specialised passes leave controls / diagonal targets outside the tile
+    # (tile-uniform predicates): fewer passes, and the sources still compile
+    from paper_1801_01037_b200 import device
+
+    lib = _lib.load(require_cuda=False)
+    out = ctypes.c_int()
+    for n, circ in ((19, workloads.qft_circuit(19)), (20, workloads.random_layer_circuit(20, 20, seed=3))):
+        monkeypatch.setenv("SVB_FUSE_OUTSIDE", "0")
+        inside = device.plan_passes(n, circ, jit=True)
+        monkeypatch.delenv("SVB_FUSE_OUTSIDE")
+        arr, nops = _lib.ops_array(circ.ops)
+        rc = lib.svb_jit_check(n, arr, nops, _lib.run_flags(fma=True), ctypes.byref(out))
+        if rc == _lib.SVB_ESTATE and b"NVRTC not available" in lib.svb_last_error():
+            pytest.skip("NVRTC not available")
+        assert rc == 0, lib.svb_last_error()
+        assert device.plan_passes(n, circ, jit=True) < inside
+        # strict order and the interpreter keep every qubit of an op in the tile
+        assert device.plan_passes(n, circ, jit=True, strict_order=True) == \
+            device.plan_passes(n, circ, jit=False, strict_order=True)
+
+
 def test_kernel_wrapper_validates_like_reference():
     # kernel/__init__.py:83-97, 124-128 -- raised before any device work
     with pytest.raises(ValidationError):
