@@ -1676,7 +1676,7 @@ int jit_check(int n, const svb_op *ops, int nops, unsigned flags) {
     std::vector<FPass> passes;
     std::vector<PlanStep> steps;
     const int fm = plan_fm(n, flags | SVB_RUN_JIT);
-    lower_plan(n, ops, nops, strict, reg_perm(flags), fm, plan_fs(flags | SVB_RUN_JIT),
+    lower_plan(n, ops, nops, strict, reg_perm(flags | SVB_RUN_JIT), fm, plan_fs(flags | SVB_RUN_JIT),
                plan_outside(flags | SVB_RUN_JIT), steps, passes);
     std::string err;
     int r = jit_compile_only(passes, jit_variant((flags & SVB_RUN_FMA) && !strict), err);

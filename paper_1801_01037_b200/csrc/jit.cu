@@ -650,9 +650,64 @@ double2 pick_factor(const double2 *m, bool diag) {
     return best;
 }
 
+// Per-thread phase (fast mode).  A diagonal gate whose target and control
+// (if any) are thread or tile bits multiplies ALL registers of a thread by
+// one scalar; such scalars commute with every in-register gate, so the
+// generator multiplies them into a per-thread `ph` (a few scalar
+// instructions per gate instead of a predicated multiply of every register)
+// and applies ph once, at the end of the group, fused with the global
+// factor when that is due.  SVB_JIT_PHASE=0 turns it off (measurement).
+// (Found with it: the last-pass flag was shadowed by the last-group flag, so
+// F was applied at the end of every pass -- exact, but one multiply of every
+// register per pass; now only the circuit's last pass applies it.)
+thread_local bool t_phase = false;  // the current group's ph is not 1
+
+int phase_mode() {  // bits: 1 thread targets, 2 tile targets, 4 controlled (0: off)
+    const char *e = getenv("SVB_JIT_PHASE");
+    return e ? atoi(e) : 7;
+}
+
+// ph *= (target bit ? d1 : d0), under the (thread / tile) control if any
+void emit_phase(Out &o, const FGate &g) {
+    const double2 d0 = g.m[0], d1 = g.m[3];
+    const bool one0 = unit_code(d0) == 0;
+    o("{ const bool b = %s;\n", pbit(g.tl).c_str());
+    if (g.cl >= 0) o("if (%s) {\n", pbit(g.cl).c_str());
+    // branch-free (a predicated update of ph is miscompiled by ptxas -O1+ in
+    // some long passes -- found by tools/jit_emu.py agreeing with the oracle
+    // while the device did not, and ptxas -O0 agreeing)
+    if (one0)
+        o("ph = cm(b ? %s : 1.0, b ? %s : 0.0, ph);\n", lit(d1.x).c_str(), lit(d1.y).c_str());
+    else
+        o("ph = cm(b ? %s : %s, b ? %s : %s, ph);\n", lit(d1.x).c_str(), lit(d0.x).c_str(), lit(d1.y).c_str(),
+          lit(d0.y).c_str());
+    if (g.cl >= 0) o("}\n");
+    o("}\n");
+    t_phase = true;
+}
+
+// ph * (i^c X) for register X holding a pending unit factor c
+std::string cm_ph(int c) {
+    double k1 = 1.0, k2 = 1.0;
+    const char *m1 = phys(c, 0, k1), *m2 = phys(c, 1, k2);
+    auto sg = [](double k) { return k < 0 ? "-" : ""; };
+    char b[256];
+    snprintf(b, sizeof b, "mk(__fma_rn(ph.x, %sX.%s, %s__dmul_rn(ph.y, X.%s)), __fma_rn(ph.x, %sX.%s, %s__dmul_rn(ph.y, X.%s)))",
+             sg(k1), m1, sg(-k2), m2, sg(k2), m2, sg(k1), m1);
+    return b;
+}
+
 void emit_gate_fast(Out &o, const FGate &g, int *code, double2 &F) {
     const int op = g.op;
     pend_conflicts(o, g);
+    if (op >= FOP_DIAG && phase_mode()) {
+        const int c = op - FOP_DIAG, pm = phase_mode();
+        const bool ok = ((g.tl >= FTILEBIT) ? (pm & 2) : (pm & 1)) && (g.cl < 0 || (pm & 4));
+        if (ok && !(c & 1) && (c >> 1) % (FSMAX + 1) == FTPOS_THREAD) {  // scalar per thread
+            emit_phase(o, g);
+            return;
+        }
+    }
     const bool uncontrolled = g.cl < 0 && !(op & 1);
     if (!uncontrolled) {  // a controlled gate scales only part of the state
         emit_gate_fold(o, g, code);
@@ -777,6 +832,34 @@ size_t jit_dyn_smem(const FPass &P) {
 // the tile loop and kept live (or spilled) across the gate arithmetic.
 const char *kOpaqueTid = "unsigned tg = tid; asm volatile(\"\" : \"+r\"(tg));\n";
 
+// Overlap between a group's shared-memory stores and other threads' loads
+// of the same group: 0 none (each thread rewrites only chunks it read), 1
+// within warps only, 2 across warps.  Pending swaps only exchange a thread's
+// own store slots, so the per-thread store set is the one computed here.
+int store_hazard(const FGroup &G, int threads, int tbits) {
+    const int nr = NR();
+    std::unordered_map<unsigned, int> owner;
+    owner.reserve(size_t(threads) * nr);
+    for (int t = 0; t < threads; ++t) {
+        unsigned a = G.ld_b;
+        for (int j = 0; j < tbits; ++j)
+            if ((t >> j) & 1) a ^= G.ld_t[j];
+        for (int r = 0; r < nr; ++r) owner[a ^ xcombo_h(G.ld_s, r)] = t;
+    }
+    int hz = 0;
+    for (int t = 0; t < threads && hz < 2; ++t) {
+        unsigned b = G.st_b;
+        for (int j = 0; j < tbits; ++j)
+            if ((t >> j) & 1) b ^= G.st_t[j];
+        for (int r = 0; r < nr; ++r) {
+            auto it = owner.find(b ^ xcombo_h(G.st_s, r));
+            if (it == owner.end() || it->second == t) continue;
+            hz = std::max(hz, it->second / 32 == t / 32 ? 1 : 2);
+        }
+    }
+    return hz;
+}
+
 // variant: 0 exact, 1 FMA, 2 FMA + factor extraction (F: the global factor
 // carried in and out; last: the circuit's last fused pass, which applies F)
 std::string jit_body(const FPass &P, int variant, double2 &F, bool last);
@@ -882,7 +965,7 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
     o("d2 v[%d];\n", NR());
     for (int gi = 0; gi < P.ngroups; ++gi) {
         const FGroup &G = P.groups[gi];
-        const bool last = gi == P.ngroups - 1;
+        const bool last_group = gi == P.ngroups - 1;
         o("{ // group %d\n", gi);
         if (gi == 0 && direct_first) {
             o("%s g0 = %s;\n", OFF, offl(P.gl_b).c_str());
@@ -897,7 +980,7 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             for (int i = 0; i < NR(); ++i)
                 o("v[%d] = *reinterpret_cast<const d2 *>(sb + (a0 ^ %uu));\n", i, xcombo_h(G.ld_s, i));
         }
-        if (last && mode == 2) {
+        if (last_group && mode == 2) {
             // every thread has its registers: refill the buffer with the next tile
             o("__syncthreads();\n{ const i64 nx = tix + gridDim.x; if (nx < ntiles) "
               "fill(reinterpret_cast<unsigned char *>(dsm), a + tbase(nx)); }\n");
@@ -906,10 +989,22 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
         if (fma && pend_on()) t_pend = pend;
         if (fast) {
             int code[FREGMAX] = {0};
+            t_phase = false;
+            o("d2 ph = mk(1.0, 0.0);\n");
             for (int q = G.first; q < G.first + G.count; ++q) emit_gate_fast(o, P.gates[q], code, F);
             const double mag = cabsh(F);
-            if (gi == P.ngroups - 1 && (last || mag < 0x1p-200 || mag > 0x1p200) &&
-                !(F.x == 1.0 && F.y == 0.0)) {
+            const bool applyF = gi == P.ngroups - 1 && (last || mag < 0x1p-200 || mag > 0x1p200) &&
+                                !(F.x == 1.0 && F.y == 0.0);
+            if (t_phase) {  // ph (times F when due) on every register
+                if (applyF) {
+                    o("ph = cm(%s, %s, ph);\n", lit(F.x).c_str(), lit(F.y).c_str());
+                    F = make_double2(1.0, 0.0);
+                }
+                for (int i = 0; i < NR(); ++i) {
+                    o("{ const d2 X = v[%d]; v[%d] = %s; }\n", i, i, cm_ph(code[i]).c_str());
+                    code[i] = 0;
+                }
+            } else if (applyF) {
                 for (int i = 0; i < NR(); ++i) {  // stored * F = true amplitude
                     o("{ const d2 X = v[%d]; v[%d] = %s; }\n", i, i, cm_fold(F, code[i]).c_str());
                     code[i] = 0;
@@ -925,7 +1020,7 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             for (int q = G.first; q < G.first + G.count; ++q) emit_gate(o, P.gates[q]);
         }
         t_pend = nullptr;
-        if (last && P.direct_last) {
+        if (last_group && P.direct_last) {
             if (G.perm && gi == 0 && direct_first) o("__syncthreads();\n");
             o("%s s0 = %s;\n", OFF, offl(P.gs_b).c_str());
             o("{\n%s", kOpaqueTid);
@@ -936,7 +1031,16 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             for (int i = 0; i < NR(); ++i)
                 o("stcs(pa + (s0 ^ %s), v[%d]);\n", offl(xcombo_g(P.gs_s, i)).c_str(), i);
         } else {
-            if (G.perm) o("__syncthreads();\n");
+            // the store overwrites chunks other threads may not have loaded
+            // yet (the swizzle changes per transition): order them with the
+            // narrowest barrier that covers every overlap
+            const int hz = (gi == 0 && direct_first) ? 0 : store_hazard(G, FTHREADS, FTBITS);
+            if (G.perm)
+                o("__syncthreads();\n");
+            else if (hz == 2)
+                o("__syncthreads();  // cross-warp store hazard\n");
+            else if (hz == 1)
+                o("__syncwarp();\n");
             o("unsigned b0 = %uu;\n", (unsigned)G.st_b);
             o("{\n%s", kOpaqueTid);
             for (int j = 0; j < FTBITS; ++j) o("if ((tg >> %d) & 1) b0 ^= %uu;\n", j, (unsigned)G.st_t[j]);
