@@ -133,6 +133,9 @@ __device__ __forceinline__ int swz(int l) { return l ^ ((l >> 3) ^ (l >> 6) ^ (l
 __device__ __forceinline__ double ng(double x) {  // -x as a sign-bit flip (integer pipe)
     return __longlong_as_double(__double_as_longlong(x) ^ (long long)0x8000000000000000ull);
 }
+__device__ __forceinline__ double cneg(double x, unsigned m) {  // -x where m = 0x80000000 (one LOP3)
+    return __hiloint2double(__double2hiint(x) ^ (int)m, __double2loint(x));
+}
 )";
 
 int swz_h(int l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9) ^ (l >> 12)) & 7); }
@@ -340,8 +343,21 @@ std::string pcond(uint64_t m) {
     return b;
 }
 
+// pending unit factors of the group's registers (fast / fold modes): a flush
+// swaps data, not codes, so a pair's codes must agree first (gates passed
+// through a pending swap may leave them different)
+thread_local int *t_code = nullptr;
+
 void pend_flush(Out &o, int s) {
     if (!t_pend || !t_pend[s]) return;
+    if (t_code)
+        for (int i = 0; i < NR(); ++i) {
+            const int j = i | (1 << s);
+            if (!(i & (1 << s)) && t_code[i] != t_code[j]) {
+                materialize(o, t_code, i);
+                materialize(o, t_code, j);
+            }
+        }
     o("{ const bool p = %s;\n", pcond(t_pend[s]).c_str());
     for (int i = 0; i < NR(); ++i) {
         if (i & (1 << s)) continue;
@@ -543,6 +559,113 @@ void emit_gate_fold(Out &o, const FGate &g, int *code) {
 }
 
 // ---------------------------------------------------------------------------
+// Gates through a pending swap (fast mode).  A pending swap X^p on slot s
+// (p: a per-thread / per-tile parity, see t_pend) need not be flushed before
+// an uncontrolled gate G on s when X G X is G up to Pauli Z's and a sign:
+// the registers then get G' = X^p G X^p and X^p stays pending --
+//   X, Rx, unit anti-diagonal with q12 = q21 (X G X = G): nothing;
+//   Y-like, q12 = -q21 (X G X = -G): ph *= (-1)^p;
+//   Ry-like, q11 = q22, q12 = -q21 (X G X = Z G Z): Z^p before and after;
+//   H-like, q11 = q12 = q21 = -q22 (H X = Z H): G, then Z^p, and the swap
+//     is consumed;
+//   diagonal (d0, d1): ph *= p ? d1 : d0, hi registers *= p ? d0/d1 : d1/d0.
+// Z^p is a sign-bit XOR of the slot's hi registers; all of it costs a few
+// integer ops instead of a select per register.  SVB_JIT_PENDTHRU=0: off.
+int pend_thru_mode() {  // bits: 1 X-type, 2 Y-like, 4 Ry-like, 8 H-like, 16 diagonal
+    const char *e = getenv("SVB_JIT_PENDTHRU");
+    return e ? atoi(e) : 31;
+}
+bool ceq(double2 a, double2 b) { return a.x == b.x && a.y == b.y; }
+double2 cdivh(double2 a, double2 b);
+double2 cnegh(double2 a) { return make_double2(-a.x, -a.y); }
+
+void emit_phase(Out &o, const FGate &g);
+extern thread_local bool t_phase;
+void emit_gate_fast(Out &o, const FGate &g, int *code, double2 &F);
+
+// sign flip of the hi registers of slot s where the mask's parity is odd
+void emit_zp(Out &o, int s, uint64_t mask) {
+    o("{ const unsigned pm = %s ? 0x80000000u : 0u;\n", pcond(mask).c_str());
+    for (int i = 0; i < NR(); ++i)
+        if ((i >> s) & 1) o("v[%d] = mk(cneg(v[%d].x, pm), cneg(v[%d].y, pm));\n", i, i, i);
+    o("}\n");
+}
+void emit_phase_sign(Out &o, uint64_t mask) {  // ph *= (-1)^p
+    o("{ const unsigned pm = %s ? 0x80000000u : 0u; ph = mk(cneg(ph.x, pm), cneg(ph.y, pm)); }\n",
+      pcond(mask).c_str());
+    t_phase = true;
+}
+
+bool pend_through(Out &o, const FGate &g, int *code, double2 &F) {
+    const int pt = pend_thru_mode();
+    if (!t_pend || !pt || g.cl >= 0 || (g.op & 1)) return false;
+    const double2 *m = g.m;
+    if (g.op < FOP_DIAG) {
+        const int s = (g.op >> 1) % FSMAX;
+        const uint64_t mask = t_pend[s];
+        if (!mask) return false;
+        const bool xtype = ceq(m[0], m[3]) && ceq(m[1], m[2]);
+        const bool ylike = m[0].x == 0 && m[0].y == 0 && m[3].x == 0 && m[3].y == 0 && ceq(m[1], cnegh(m[2])) &&
+                           unit_code(m[1]) >= 0;
+        const bool rylike = ceq(m[0], m[3]) && ceq(m[1], cnegh(m[2])) && !ylike;
+        const bool hlike = ceq(m[0], m[1]) && ceq(m[0], m[2]) && ceq(m[0], cnegh(m[3]));
+        if (!((xtype && (pt & 1)) || (ylike && (pt & 2)) || (rylike && (pt & 4)) || (hlike && (pt & 8))))
+            return false;
+        t_pend[s] = 0;  // emit G itself without flushing s
+        if (rylike) emit_zp(o, s, mask);
+        emit_gate_fast(o, g, code, F);
+        if (rylike) emit_zp(o, s, mask);
+        if (hlike) {
+            emit_zp(o, s, mask);
+            return true;  // consumed
+        }
+        if (ylike) emit_phase_sign(o, mask);
+        t_pend[s] = mask;
+        return true;
+    }
+    const int c = g.op - FOP_DIAG;
+    const int tpos = (c >> 1) % (FSMAX + 1);
+    if (tpos >= FTPOS_THREAD || !t_pend[tpos] || !(pt & 16)) return false;
+    const int s = tpos;
+    const uint64_t mask = t_pend[s];
+    const double2 d0 = m[0], d1 = m[3];
+    if ((d0.x == 0 && d0.y == 0) || (d1.x == 0 && d1.y == 0)) return false;
+    const double2 r = cdivh(d1, d0), ri = cdivh(d0, d1);
+    // ph *= p ? d1 : d0
+    o("{ const bool p = %s;\n", pcond(mask).c_str());
+    o("ph = cm(p ? %s : %s, p ? %s : %s, ph);\n", lit(d1.x).c_str(), lit(d0.x).c_str(), lit(d1.y).c_str(),
+      lit(d0.y).c_str());
+    t_phase = true;
+    const int ur = unit_code(r), uri = unit_code(ri);
+    if (ur >= 0 && uri >= 0) {
+        // r = i^u, 1/r = i^-u = i^u (-1)^[u odd]: a code plus a conditional sign
+        const bool odd = ur & 1;
+        for (int i = 0; i < NR(); ++i)
+            if ((i >> s) & 1) code[i] = (code[i] + ur) & 3;
+        if (odd) {
+            o("const unsigned pm = p ? 0x80000000u : 0u;\n");
+            for (int i = 0; i < NR(); ++i)
+                if ((i >> s) & 1) o("v[%d] = mk(cneg(v[%d].x, pm), cneg(v[%d].y, pm));\n", i, i, i);
+        }
+    } else {
+        o("const double cx = p ? %s : %s, cy = p ? %s : %s;\n", lit(ri.x).c_str(), lit(r.x).c_str(),
+          lit(ri.y).c_str(), lit(r.y).c_str());
+        for (int i = 0; i < NR(); ++i) {
+            if (!((i >> s) & 1)) continue;
+            double k1 = 1.0, k2 = 1.0;
+            const char *m1 = phys(code[i], 0, k1), *m2 = phys(code[i], 1, k2);
+            auto sg = [](double k) { return k < 0 ? "-" : ""; };
+            o("{ const d2 X = v[%d]; v[%d] = mk(__fma_rn(cx, %sX.%s, %s__dmul_rn(cy, X.%s)), "
+              "__fma_rn(cx, %sX.%s, %s__dmul_rn(cy, X.%s))); }\n",
+              i, i, sg(k1), m1, sg(-k2), m2, sg(k2), m2, sg(k1), m1);
+            code[i] = 0;
+        }
+    }
+    o("}\n");
+    return true;
+}
+
+// ---------------------------------------------------------------------------
 // Factor extraction ("fast" FMA mode, SVB_JIT_FACTOR, default on).  An
 // uncontrolled one-qubit gate multiplies EVERY amplitude of the state, so a
 // scalar can be pulled out of it: U = a V with one entry of V equal to 1
@@ -697,8 +820,11 @@ std::string cm_ph(int c) {
     return b;
 }
 
+bool pend_through(Out &o, const FGate &g, int *code, double2 &F);
+
 void emit_gate_fast(Out &o, const FGate &g, int *code, double2 &F) {
     const int op = g.op;
+    if (pend_through(o, g, code, F)) return;
     pend_conflicts(o, g);
     if (op >= FOP_DIAG && phase_mode()) {
         const int c = op - FOP_DIAG, pm = phase_mode();
@@ -989,6 +1115,7 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
         if (fma && pend_on()) t_pend = pend;
         if (fast) {
             int code[FREGMAX] = {0};
+            t_code = code;
             t_phase = false;
             o("d2 ph = mk(1.0, 0.0);\n");
             for (int q = G.first; q < G.first + G.count; ++q) emit_gate_fast(o, P.gates[q], code, F);
@@ -1014,12 +1141,14 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             for (int i = 0; i < NR(); ++i) materialize(o, code, i);
         } else if (fma) {
             int code[FREGMAX] = {0};
+            t_code = code;
             for (int q = G.first; q < G.first + G.count; ++q) emit_gate_fold(o, P.gates[q], code);
             for (int i = 0; i < NR(); ++i) materialize(o, code, i);
         } else {
             for (int q = G.first; q < G.first + G.count; ++q) emit_gate(o, P.gates[q]);
         }
         t_pend = nullptr;
+        t_code = nullptr;
         if (last_group && P.direct_last) {
             if (G.perm && gi == 0 && direct_first) o("__syncthreads();\n");
             o("%s s0 = %s;\n", OFF, offl(P.gs_b).c_str());
