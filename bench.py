@@ -20,8 +20,9 @@ Extra keys on the one JSON line:
   cpu_baseline  the reference's own compiled kernel (oracle/_ref, built
                 from /root/reference by build()) on all host cores, over a
                 bounded prefix of the same circuit;
-  e2e           same metric through the public host-memory call
-                device.simulate (pinned H2D + run + D2H per step);
+  e2e           same metric through the public host-memory batch call
+                device.simulate_batch (pinned H2D + run + D2H per step,
+                neighbouring steps overlapped; `serial`: one call per step);
   local_gate_sweep  BASELINE configs[2]: n=30, one Haar U per target
                 t=0..29 x 10 reps, per-target HBM GB/s (one launch per
                 application, no fusion);
@@ -310,18 +311,28 @@ def run_gpu_arm(args) -> None:
     kernels = {k: {"launches": v[0], "ms": round(v[1], 3), "gbs": round(v[2] / (v[1] / 1e3) / 1e9, 1)}
                for k, v in prof.items()}
 
-    # e2e through the public host-memory call, pinned buffers
+    # e2e through the public host-memory calls, pinned buffers.  Headline:
+    # simulate_batch (svb_host_run_ops_batch) over `steps` input states --
+    # every step copies its 1 GiB state in and its result out, overlapped
+    # with the neighbouring steps' runs; also one simulate call per step
+    # (no overlap) for comparison
     pin_in = torch.zeros(1 << n, dtype=torch.complex128).pin_memory()
     pin_in[0] = 1.0
-    pin_out = torch.empty(1 << n, dtype=torch.complex128).pin_memory()
-    a_in, a_out = pin_in.numpy(), pin_out.numpy()
-    e2e_steps = max(1, min(args.steps, 3))
-    device.simulate(circuit, a_in, fuse=not args.no_fuse, out=a_out, fma=args.fma, jit=args.jit)
+    a_in = pin_in.numpy()
+    e2e_steps = max(3, args.steps)
+    outs = [torch.empty(1 << n, dtype=torch.complex128).pin_memory().numpy() for _ in range(e2e_steps)]
+    kw = dict(fuse=not args.no_fuse, fma=args.fma, jit=args.jit)
+    device.simulate_batch(circuit, [a_in], [outs[0]], **kw)
     t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        device.simulate(circuit, a_in, fuse=not args.no_fuse, out=a_out, fma=args.fma, jit=args.jit)
+    device.simulate_batch(circuit, [a_in] * e2e_steps, outs, **kw)
     e2e_dt = time.perf_counter() - t0
-    e2e_norm = float(np.vdot(a_out, a_out).real)
+    e2e_norm = float(np.vdot(outs[-1], outs[-1]).real)
+    e2e_same = all(np.array_equal(o, outs[0]) for o in outs[1:])
+    serial_steps = max(1, min(args.steps, 3))
+    t0 = time.perf_counter()
+    for k in range(serial_steps):
+        device.simulate(circuit, a_in, out=outs[k], **kw)
+    serial_dt = time.perf_counter() - t0
 
     sweep = None if args.no_sweep else local_gate_sweep(SWEEP_N, SWEEP_REPS, peak)
 
@@ -345,12 +356,15 @@ def run_gpu_arm(args) -> None:
         "gpu_launches": launches,
         "e2e": {"value": round(nops * e2e_steps / e2e_dt, 1), "unit": UNIT,
                 "h2d_bytes_per_step": 16 << n, "d2h_bytes_per_step": 16 << n,
-                "api": "paper_1801_01037_b200.device.simulate (svb_host_run_ops), pinned host buffers",
-                "steps": e2e_steps},
+                "api": "paper_1801_01037_b200.device.simulate_batch (svb_host_run_ops_batch): per step "
+                       "H2D + run + D2H, neighbouring steps overlapped; pinned host buffers",
+                "steps": e2e_steps,
+                "serial": {"value": round(nops * serial_steps / serial_dt, 1), "steps": serial_steps,
+                           "api": "device.simulate (svb_host_run_ops), one synchronous call per step"}},
         "cpu_baseline": cpu,
         "local_gate_sweep": sweep,
         "clocks": clk.summary(),
-        "check": {"norm_after_step": norm_after, "e2e_norm": e2e_norm},
+        "check": {"norm_after_step": norm_after, "e2e_norm": e2e_norm, "e2e_outputs_identical": e2e_same},
         "first_step_s": round(first_step_s, 3),
         "jit_compile_s": round(max(0.0, first_step_s - ms / 1e3 / args.steps), 3) if args.jit else 0.0,
     }

@@ -159,6 +159,16 @@ int svb_host_apply_c1q(double *host_amps, int64_t n_amps, const double q[8], int
  * host_out (may equal host_in).  Synchronous.  The end-to-end public call. */
 int svb_host_run_ops(const double *host_in, double *host_out, int64_t n_amps, const svb_op *ops,
                      int nops, unsigned flags);
+/* The same op list over a batch of host states (serving: many inputs, one
+ * circuit): state k is copied in (host_in[k]), run and copied out
+ * (host_out[k]) exactly as svb_host_run_ops would, but the three stages of
+ * consecutive states overlap -- H2D of k+1 and D2H of k-1 on their own
+ * streams while k runs -- through three device buffers owned by the
+ * library.  Synchronous: returns when every host_out[k] is written.  Pinned
+ * host buffers are needed for the copies to overlap.  host_out[k] may equal
+ * host_in[k]; results equal nbatch calls of svb_host_run_ops bit for bit. */
+int svb_host_run_ops_batch(const double *const *host_in, double *const *host_out, int nbatch,
+                           int64_t n_amps, const svb_op *ops, int nops, unsigned flags);
 
 /* ---- partitioned state over 2^k ranks (engine.py DistState) ------------- */
 

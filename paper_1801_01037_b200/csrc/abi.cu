@@ -479,6 +479,103 @@ int svb_host_run_ops(const double *host_in, double *host_out, int64_t n_amps, co
     return host_unstage(host_out, n_amps, dev);
 }
 
+// three device state buffers + three streams for svb_host_run_ops_batch
+struct BatchStage {
+    std::mutex mu;
+    void *buf[3] = {nullptr, nullptr, nullptr};
+    size_t bytes = 0;
+    int device = -1;
+    cudaStream_t s[3] = {nullptr, nullptr, nullptr};  // H2D, compute, D2H
+    cudaEvent_t in[3], ran[3], out[3];
+};
+static BatchStage g_batch;
+
+static int batch_setup(size_t bytes) {
+    int d;
+    cudaError_t e = cudaGetDevice(&d);
+    if (e != cudaSuccess) return cuda_status(e, "cudaGetDevice");
+    BatchStage &B = g_batch;
+    if (B.device >= 0 && (B.device != d || B.bytes < bytes)) {
+        int cur = d;
+        cudaSetDevice(B.device);
+        for (int i = 0; i < 3; ++i) {
+            cudaFree(B.buf[i]);
+            B.buf[i] = nullptr;
+        }
+        if (B.device != d) {
+            for (int i = 0; i < 3; ++i) {
+                cudaStreamDestroy(B.s[i]);
+                cudaEventDestroy(B.in[i]);
+                cudaEventDestroy(B.ran[i]);
+                cudaEventDestroy(B.out[i]);
+                B.s[i] = nullptr;
+            }
+        }
+        cudaSetDevice(cur);
+        B.bytes = 0;
+    }
+    if (!B.s[0]) {
+        for (int i = 0; i < 3; ++i) {
+            if ((e = cudaStreamCreateWithFlags(&B.s[i], cudaStreamNonBlocking)) != cudaSuccess)
+                return cuda_status(e, "batch stream");
+            cudaEventCreateWithFlags(&B.in[i], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&B.ran[i], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&B.out[i], cudaEventDisableTiming);
+        }
+    }
+    if (!B.buf[0]) {
+        for (int i = 0; i < 3; ++i)
+            if ((e = cudaMalloc(&B.buf[i], bytes)) != cudaSuccess) {
+                for (int j = 0; j < 3; ++j) {
+                    cudaFree(B.buf[j]);
+                    B.buf[j] = nullptr;
+                }
+                return cuda_status(e, "batch cudaMalloc");
+            }
+        B.bytes = bytes;
+    }
+    B.device = d;
+    return SVB_OK;
+}
+
+int svb_host_run_ops_batch(const double *const *host_in, double *const *host_out, int nbatch,
+                           int64_t n_amps, const svb_op *ops, int nops, unsigned flags) {
+    if (nbatch < 0 || (nbatch > 0 && (!host_in || !host_out))) {
+        set_error("batch: nbatch %d, host_in %p, host_out %p", nbatch, (const void *)host_in, (const void *)host_out);
+        return SVB_EINVAL;
+    }
+    int r;
+    for (int k = 0; k < nbatch; ++k) {
+        if ((r = check_amps(host_in[k], n_amps)) != SVB_OK) return r;
+        if ((r = check_amps(host_out[k], n_amps)) != SVB_OK) return r;
+    }
+    if ((r = check_ops(log2_exact(n_amps), ops, nops)) != SVB_OK) return r;
+    if (nbatch == 0) return SVB_OK;
+    std::lock_guard<std::mutex> lk(g_batch.mu);
+    const size_t bytes = size_t(n_amps) * 16;
+    if ((r = batch_setup(bytes)) != SVB_OK) return r;
+    BatchStage &B = g_batch;
+    cudaError_t e;
+    // stage k uses buffer k % 3: H2D(k) waits for D2H(k-3) of that buffer;
+    // the run waits for its H2D; the D2H waits for its run
+    for (int k = 0; k < nbatch; ++k) {
+        const int b = k % 3;
+        if (k >= 3) cudaStreamWaitEvent(B.s[0], B.out[b], 0);
+        if ((e = cudaMemcpyAsync(B.buf[b], host_in[k], bytes, cudaMemcpyHostToDevice, B.s[0])) != cudaSuccess)
+            return cuda_status(e, "batch H2D");
+        cudaEventRecord(B.in[b], B.s[0]);
+        cudaStreamWaitEvent(B.s[1], B.in[b], 0);
+        if ((r = svb_run_ops(B.buf[b], n_amps, ops, nops, flags, B.s[1])) != SVB_OK) return r;
+        cudaEventRecord(B.ran[b], B.s[1]);
+        cudaStreamWaitEvent(B.s[2], B.ran[b], 0);
+        if ((e = cudaMemcpyAsync(host_out[k], B.buf[b], bytes, cudaMemcpyDeviceToHost, B.s[2])) != cudaSuccess)
+            return cuda_status(e, "batch D2H");
+        cudaEventRecord(B.out[b], B.s[2]);
+    }
+    if ((e = cudaStreamSynchronize(B.s[2])) != cudaSuccess) return cuda_status(e, "batch sync");
+    return SVB_OK;
+}
+
 int svb_profile_enable(int on) {
     std::lock_guard<std::mutex> lk(g_prof_mu);
     cudaDeviceSynchronize();

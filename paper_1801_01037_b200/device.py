@@ -210,5 +210,32 @@ def simulate(circuit: Circuit, initial=None, fuse: bool = True, strict_order: bo
     return dst
 
 
+def simulate_batch(circuit: Circuit, inputs, outs=None, fuse: bool = True, strict_order: bool = False,
+                   fma: bool = False, jit: bool = False) -> list:
+    """`simulate` over a batch of host states (one circuit, many inputs):
+    through svb_host_run_ops_batch, which overlaps the H2D copy of the next
+    state and the D2H copy of the previous one with the current run.
+    outs[k] (default: inputs[k], in place) receives state k's result, bit
+    for bit what simulate would return.  Use pinned buffers for overlap."""
+    lib = _lib.load()
+    size = 1 << circuit.n
+    srcs = [_host_c128(x, writable=outs is None) for x in inputs]
+    dsts = srcs if outs is None else list(outs)
+    if len(dsts) != len(srcs):
+        raise ValidationError(f"{len(srcs)} inputs but {len(dsts)} outputs")
+    for x, y in zip(srcs, dsts):
+        if x.shape[0] != size:
+            raise ValidationError(f"initial state has {x.shape[0]} amplitudes, circuit needs 2**{circuit.n}")
+        if not (isinstance(y, np.ndarray) and y.dtype == np.complex128 and y.flags.c_contiguous
+                and y.flags.writeable and y.shape == x.shape):
+            raise ValidationError("outs must be writable contiguous complex128 arrays of the state's size")
+    arr, nops = _lib.ops_array(circuit.ops)
+    flags = _lib.run_flags(fuse, strict_order, fma, jit)
+    pin = (ctypes.c_void_p * max(1, len(srcs)))(*[x.ctypes.data for x in srcs])
+    pout = (ctypes.c_void_p * max(1, len(dsts)))(*[y.ctypes.data for y in dsts])
+    _lib.check(lib.svb_host_run_ops_batch(pin, pout, len(srcs), size, arr, nops, flags), "simulate_batch")
+    return dsts
+
+
 def gate_op(kind: str, gate: Gate2x2, target: int, control: int | None = None) -> GateOp:
     return GateOp(kind, gate, target, control)

@@ -451,3 +451,25 @@ def test_qft_known_answer_partitioned(cuda_ok):
     for y in (0, 1, 77, 4096, 16383):
         assert abs(out[y] - oracle.qft_basis_amplitude(x, y, n)) <= TOL
     assert abs(np.vdot(out, out).real - 1) <= 1e-12
+
+
+def test_simulate_batch_equals_serial(cuda_ok):
+    # svb_host_run_ops_batch (pipelined H2D / run / D2H over three device
+    # buffers) returns exactly what one svb_host_run_ops call per state does
+    import torch
+
+    n = 20
+    circ = w.random_layer_circuit(n, 12, seed=9)
+    rng = np.random.default_rng(90)
+    states = [w.random_state_array(rng, n) for _ in range(5)]
+    serial = [device.simulate(circ, s.copy(), fma=True, jit=True) for s in states]
+    pins = [torch.from_numpy(s.copy()).pin_memory().numpy() for s in states]
+    outs = [torch.empty(1 << n, dtype=torch.complex128).pin_memory().numpy() for _ in states]
+    device.simulate_batch(circ, pins, outs, fma=True, jit=True)
+    for got, want in zip(outs, serial):
+        assert np.array_equal(got, want)
+    inplace = [s.copy() for s in states[:2]]  # pageable, in place, batch smaller than the buffer ring
+    device.simulate_batch(circ, inplace, fma=True, jit=True)
+    for got, want in zip(inplace, serial):
+        assert np.array_equal(got, want)
+    assert device.simulate_batch(circ, [], fma=True, jit=True) == []
