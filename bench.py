@@ -248,7 +248,7 @@ def run_gpu_arm(args) -> None:
     if world > 1 or os.environ.get("SVB_BENCH_DIST") == "1":  # (=1: the N>1 engine at world 1, a smoke test)
         from paper_1801_01037_b200 import dist
 
-        dist.bench_main(args)
+        dist.bench_main(args, clock_cls=ClockSampler, peaks_fn=peaks)
         return
 
     lib = _lib.load()

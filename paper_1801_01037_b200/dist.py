@@ -463,8 +463,12 @@ class DistEngine:
 # bench.py --gpus N (torchrun): weak scaling, 2^26 amplitudes per GPU
 
 
-def bench_main(args) -> None:
+def bench_main(args, clock_cls=None, peaks_fn=None) -> None:
+    """bench.py's N>1 arm (and SVB_BENCH_DIST=1 at world 1).  clock_cls /
+    peaks_fn: bench.py's nvidia-smi sampler and measured-peak reader."""
+    import contextlib
     import json
+    import time
 
     import torch
     import torch.distributed as dist
@@ -496,17 +500,42 @@ def bench_main(args) -> None:
     stats0 = (eng.stats.exchanges, eng.stats.bytes_sent, eng.stats.swaps)
     dist.barrier()
     torch.cuda.synchronize()
+    _lib.profile_enable(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize()
+    sampler = clock_cls(local) if (clock_cls and rank == 0) else contextlib.nullcontext()
+    with sampler as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
     dist.barrier()
+    launches = _lib.launch_count() - launches0
+    prof = _lib.profile_read()
+    _lib.profile_enable(False)
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
     norm = eng.norm2()
+
+    # e2e: every rank copies its slab in from pinned host memory, runs the
+    # circuit, copies the slab back out; max wall time over ranks
+    slab_bytes = eng.slab.numel() * 16
+    host_in = torch.zeros(eng.slab.numel(), dtype=torch.complex128).pin_memory()
+    if rank == 0:
+        host_in[0] = 1.0
+    host_out = torch.empty_like(host_in).pin_memory()
+    e2e_steps = max(1, min(args.steps, 3))
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        eng.slab.copy_(host_in, non_blocking=True)
+        eng.run(circuit)
+        host_out.copy_(eng.slab, non_blocking=True)
+        torch.cuda.synchronize()
+    e2e_dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    dist.all_reduce(e2e_dt, op=dist.ReduceOp.MAX)
+    e2e_dt = float(e2e_dt.item())
     if rank == 0:
         ex = eng.stats.exchanges - stats0[0]
         sent = eng.stats.bytes_sent - stats0[1]
@@ -521,8 +550,23 @@ def bench_main(args) -> None:
             "exchanges_per_step": ex / args.steps,
             "layout_swaps_per_step": (eng.stats.swaps - stats0[2]) / args.steps,
             "nvlink_bytes_sent_per_gpu_per_step": sent / args.steps,
-            "gpu_launches": _lib.launch_count() - launches0,
+            "gpu_launches": launches,
+            "e2e": {"value": round(nops * e2e_steps / e2e_dt, 1), "unit": "gate_apps/s",
+                    "h2d_bytes_per_step": world * slab_bytes, "d2h_bytes_per_step": world * slab_bytes,
+                    "api": "DistEngine.run on each rank's slab, pinned H2D + run + D2H per step",
+                    "steps": e2e_steps},
             "check": {"norm": norm},
         }
+        if prof:
+            name, (cnt, tms, nbytes) = max(prof.items(), key=lambda kv: kv[1][1])
+            peak, peak_src = peaks_fn() if peaks_fn else (6650.0, "fallback")
+            achieved = nbytes / (tms / 1e3) / 1e9
+            line["roofline"] = {"bound": "hbm", "kernel": name, "achieved": round(achieved, 1), "peak": peak,
+                                "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                                "avg_launch_ms": round(tms / cnt, 4), "launches": cnt,
+                                "share_of_step": round(tms / ms, 4), "peak_source": peak_src,
+                                "rank": 0}
+        if clock_cls:
+            line["clocks"] = clk.summary()
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
