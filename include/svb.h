@@ -107,6 +107,20 @@ int svb_norm2(const void *amps, int64_t n_amps, double *out, void *stream);
 /* probs[j] = |a_j|^2 into a device buffer of n_amps doubles. */
 int svb_probs(const void *amps, int64_t n_amps, double *probs, void *stream);
 
+/* ---- dense verifier (oracle.py:81-176), n <= 12 ---------- */
+
+#define SVB_MAX_DENSE_QUBITS 12 /* oracle.py:22 MAX_DENSE_QUBITS */
+/* Write the 2^n x 2^n embedding of gate q on `target` (control = -1: none;
+ * else only where bit `control` is set) into u (row-major complex128):
+ * embed_single / embed_controlled (oracle.py:81-116), the same bits.
+ * n > 12: SVB_ENOMEM (the reference's CapacityError). */
+int svb_dense_embed(void *u, int n_qubits, const double q[8], int control, int target, void *stream);
+/* y[row0 .. row0+nrows) = (U x)[rows], U row-major dim x dim: matvec /
+ * matvec_partitioned's per-rank strip (oracle.py:122-176).  Each row is a
+ * fixed-order sum, so any row partition gives the same bits. */
+int svb_dense_matvec(const void *u, const void *x, void *y, int64_t dim, int64_t row0, int64_t nrows,
+                     void *stream);
+
 /* Own-row exchange update of the paper's single-amplitude protocol for one
  * received chunk (engine.py:241-254 scheme b, 257-272 chunked): for
  * j in [0, count): own[j] = own_is_low ? q11*own[j] + q12*other[j]

@@ -61,6 +61,8 @@ _SIGS = {
     "svb_jit_check": ([_int, ctypes.POINTER(SvbOp), _int, ctypes.c_uint, ctypes.POINTER(_int)], _int),
     "svb_norm2": ([_vp, _i64, _dp, _vp], _int),
     "svb_probs": ([_vp, _i64, _vp, _vp], _int),
+    "svb_dense_embed": ([_vp, _int, _dp, _int, _int, _vp], _int),
+    "svb_dense_matvec": ([_vp, _vp, _vp, _i64, _i64, _i64, _vp], _int),
     "svb_exchange_own_row": ([_vp, _vp, _i64, _dp, _int, _int, _i64, _vp], _int),
     "svb_pair_update": ([_vp, _vp, _i64, _i64, _dp, _int, _vp], _int),
     "svb_pack_ctrl": ([_vp, _vp, _i64, _int, _i64, _vp], _int),
@@ -175,7 +177,7 @@ def ops_array(ops) -> tuple[ctypes.Array, int]:
 
 
 PROFILE_CLASSES = ("k_pair_high", "k_pair_low", "k_diag", "k_tiny", "k_fused", "k_exchange", "k_norm",
-                   "kpass_jit")
+                   "kpass_jit", "k_dense")
 
 
 def profile_enable(on: bool = True) -> None:

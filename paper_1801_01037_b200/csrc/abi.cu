@@ -19,6 +19,9 @@
 namespace svb {
 
 LaunchInfo launch_gate(double2 *a, int64_t n_amps, const Gate &g, int t, int c, cudaStream_t s);
+LaunchInfo launch_dense_embed(double2 *u, int64_t dim, const Gate &g, int t, int c, cudaStream_t s);
+LaunchInfo launch_dense_matvec(const double2 *u, const double2 *x, double2 *y, int64_t dim, int64_t row0,
+                               int64_t nrows, cudaStream_t s);
 int launch_norm2(const double2 *a, int64_t n, double *scratch, cudaStream_t s);
 int norm_scratch_doubles();
 int launch_probs(const double2 *a, int64_t n, double *p, cudaStream_t s);
@@ -279,6 +282,42 @@ int svb_norm2(const void *amps, int64_t n_amps, double *out, void *stream) {
     cudaFreeAsync(scratch, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_status(e, "svb_norm2");
+    return SVB_OK;
+}
+
+int svb_dense_embed(void *u, int n_qubits, const double q[8], int control, int target, void *stream) {
+    if (!u || !q || n_qubits < 1 || n_qubits > SVB_MAX_DENSE_QUBITS) {
+        set_error("dense embed: n_qubits %d outside [1, %d] or NULL buffer", n_qubits, SVB_MAX_DENSE_QUBITS);
+        return n_qubits > SVB_MAX_DENSE_QUBITS ? SVB_ENOMEM : SVB_EINVAL;
+    }
+    if (target < 0 || target >= n_qubits || control >= n_qubits || control == target || control < -1) {
+        set_error("dense embed: control %d / target %d invalid for n=%d", control, target, n_qubits);
+        return SVB_EINVAL;
+    }
+    const int64_t dim = int64_t(1) << n_qubits;
+    prof_begin((cudaStream_t)stream);
+    LaunchInfo li = launch_dense_embed((double2 *)u, dim, make_gate(q), target, control, (cudaStream_t)stream);
+    prof_end((cudaStream_t)stream, li);
+    g_launches += li.kernels;
+    SVB_CHECK_LAUNCH("svb_dense_embed");
+    return SVB_OK;
+}
+
+int svb_dense_matvec(const void *u, const void *x, void *y, int64_t dim, int64_t row0, int64_t nrows,
+                     void *stream) {
+    if (!u || !x || !y || dim < 1 || (dim & (dim - 1)) || dim > (int64_t(1) << SVB_MAX_DENSE_QUBITS) ||
+        row0 < 0 || nrows < 0 || row0 + nrows > dim) {
+        set_error("dense matvec: dim %lld, rows [%lld, %lld) invalid", (long long)dim, (long long)row0,
+                  (long long)(row0 + nrows));
+        return SVB_EINVAL;
+    }
+    if (nrows == 0) return SVB_OK;
+    prof_begin((cudaStream_t)stream);
+    LaunchInfo li = launch_dense_matvec((const double2 *)u, (const double2 *)x, (double2 *)y, dim, row0, nrows,
+                                        (cudaStream_t)stream);
+    prof_end((cudaStream_t)stream, li);
+    g_launches += li.kernels;
+    SVB_CHECK_LAUNCH("svb_dense_matvec");
     return SVB_OK;
 }
 
@@ -599,8 +638,8 @@ int svb_profile_read(int cls, int64_t *launches, double *total_ms, int64_t *alg_
 }
 
 const char *svb_profile_class_name(int cls) {
-    static const char *names[PROF_NCLASSES] = {"k_pair_high", "k_pair_low", "k_diag", "k_tiny",
-                                               "k_fused", "k_exchange", "k_norm", "kpass_jit"};
+    static const char *names[PROF_NCLASSES] = {"k_pair_high", "k_pair_low", "k_diag", "k_tiny", "k_fused",
+                                               "k_exchange", "k_norm", "kpass_jit", "k_dense"};
     return (cls >= 0 && cls < PROF_NCLASSES) ? names[cls] : "";
 }
 

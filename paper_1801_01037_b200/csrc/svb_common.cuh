@@ -169,7 +169,8 @@ enum ProfClass : int {
     PROF_EXCHANGE = 5,   // k_exchange_own_row / k_pair_update
     PROF_NORM = 6,       // norm / probs
     PROF_FUSED_JIT = 7,  // kpass: NVRTC-specialised fused pass (jit.cu)
-    PROF_NCLASSES = 8
+    PROF_DENSE = 8,      // k_dense_embed / k_dense_matvec (dense verifier)
+    PROF_NCLASSES = 9
 };
 struct LaunchInfo {
     int kernels;
