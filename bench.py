@@ -239,6 +239,34 @@ def local_gate_sweep(n: int, reps: int, peak: float) -> dict:
             "norm_after": nrm, "bytes_per_app": bytes_per_app}
 
 
+def qft20_rate(args, reps: int = 20) -> dict:
+    """BASELINE configs[0] on the GPU: QFT n=20 on the seeded Gaussian state
+    (16 MiB, L2-resident), device-resident, the bench's arithmetic mode."""
+    import torch
+
+    from paper_1801_01037_b200 import device, workloads
+
+    n = 20
+    circ = workloads.qft_circuit(n)
+    a = torch.from_numpy(workloads.seeded_state(n, workloads.SEED_STATE)).cuda()
+    st = device.DeviceState(n, a.clone())
+    kw = dict(fuse=not args.no_fuse, fma=args.fma, jit=args.jit)
+    device.run_ops(st, circ, **kw)  # plan + compile
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        st.amps.copy_(a)
+        device.run_ops(st, circ, **kw)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    return {"config": "QFT n=20 on the seeded Gaussian state (configs[0]), state reset + circuit per rep",
+            "ops": len(circ.ops), "ms_per_circuit": round(ms, 4),
+            "gate_apps_per_s": round(len(circ.ops) / (ms / 1e3), 1),
+            "passes": device.plan_passes(n, circ, fuse=not args.no_fuse, jit=args.jit)}
+
+
 def run_gpu_arm(args) -> None:
     import torch
 
@@ -335,6 +363,7 @@ def run_gpu_arm(args) -> None:
     serial_dt = time.perf_counter() - t0
 
     sweep = None if args.no_sweep else local_gate_sweep(SWEEP_N, SWEEP_REPS, peak)
+    qft = None if args.no_sweep else qft20_rate(args)
 
     cores = host_cores()
     cpu = None
@@ -363,6 +392,7 @@ def run_gpu_arm(args) -> None:
                            "api": "device.simulate (svb_host_run_ops), one synchronous call per step"}},
         "cpu_baseline": cpu,
         "local_gate_sweep": sweep,
+        "qft20": qft,
         "clocks": clk.summary(),
         "check": {"norm_after_step": norm_after, "e2e_norm": e2e_norm, "e2e_outputs_identical": e2e_same},
         "first_step_s": round(first_step_s, 3),
