@@ -1757,15 +1757,24 @@ struct CompiledPlan {
     // per variant (exact / FMA / FMA + factors): 0 untried, 1 built, -1 failed
     mutable int jit_state[3] = {0, 0, 0};
     mutable std::vector<void *> jit_fns[3];
+    mutable std::vector<std::shared_ptr<void>> jit_keep[3];  // the loaded modules (unloaded with the plan)
 };
 
-bool jit_build(const std::vector<FPass> &passes, int variant, std::vector<void *> &fns);
+bool jit_build(const std::vector<FPass> &passes, int variant, std::vector<void *> &fns,
+               std::vector<std::shared_ptr<void>> &keep);
 bool jit_launch(void *fn, const FPass &P, double2 *a, int64_t ntiles, cudaStream_t s);
 
 static uint64_t fnv1a(const void *p, size_t len, uint64_t h) {
     const unsigned char *b = static_cast<const unsigned char *>(p);
     for (size_t i = 0; i < len; ++i) h = (h ^ b[i]) * 1099511628211ull;
     return h;
+}
+
+// descriptor bytes the plan cache keeps beyond its 4 most recent plans
+// (SVB_PLAN_CACHE_MB, default 256; read per call)
+static size_t plan_cache_bytes() {
+    const char *e = getenv("SVB_PLAN_CACHE_MB");
+    return (e ? size_t(atoll(e)) : size_t(256)) << 20;
 }
 
 static std::shared_ptr<const CompiledPlan> compiled_plan(int n, const svb_op *ops, int nops, bool strict,
@@ -1810,7 +1819,7 @@ static std::shared_ptr<const CompiledPlan> compiled_plan(int n, const svb_op *op
     size_t bytes = 0, keep = 0;
     for (; keep < cache.size(); ++keep) {
         bytes += cache[keep].second->passes.size() * sizeof(FPass) + cache[keep].second->ops.size() * sizeof(svb_op);
-        if (keep >= 4 && bytes > (size_t(256) << 20)) break;
+        if (keep >= 4 && bytes > plan_cache_bytes()) break;
     }
     cache.resize(std::max<size_t>(keep, 1));
     return cp;
@@ -1847,7 +1856,8 @@ int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsi
         std::lock_guard<std::mutex> lk(cp->jit_mu);
         const int variant = jit_variant(fma);
         int &state = cp->jit_state[variant];
-        if (state == 0) state = jit_build(cp->passes, variant, cp->jit_fns[variant]) ? 1 : -1;
+        if (state == 0)
+            state = jit_build(cp->passes, variant, cp->jit_fns[variant], cp->jit_keep[variant]) ? 1 : -1;
         if (state == 1) jit_fns = &cp->jit_fns[variant];
     }
     if (!jit_fns && (cp->fm != FM || cp->fs != FSLOTS || cp->outside)) {  // JIT unavailable: the interpreter's plan

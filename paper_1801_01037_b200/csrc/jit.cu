@@ -25,6 +25,7 @@
 #include <mutex>
 #include <string>
 #include <thread>
+#include <memory>
 #include <unordered_map>
 #include <vector>
 
@@ -1201,13 +1202,20 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
 // ---------------------------------------------------------------------------
 // compile + cache
 
-struct JitFn {
+// A loaded pass module, shared by every compiled plan that uses its source
+// (plans hold shared_ptrs; the cache only weak ones, so a module is unloaded
+// once the last plan using it leaves the plan cache -- bounded memory for
+// long-running processes that see many circuits).
+struct JitModule {
     cudaLibrary_t lib = nullptr;
     cudaKernel_t fn = nullptr;
+    ~JitModule() {
+        if (lib) cudaLibraryUnload(lib);  // (errors at process teardown are harmless)
+    }
 };
 
 static std::mutex g_jit_mu;
-static std::unordered_map<uint64_t, JitFn> g_jit_cache;
+static std::unordered_map<uint64_t, std::weak_ptr<JitModule>> g_jit_cache;
 static std::string g_jit_err;
 
 static uint64_t hash_str(const std::string &s) {
@@ -1297,8 +1305,10 @@ static bool set_dyn_smem(cudaKernel_t fn, size_t bytes) {
 // `fns` empty on any failure (the caller falls back to k_fused).
 int jit_variant(bool fma) { return fma ? (jit_factor_on() ? 2 : 1) : 0; }
 
-bool jit_build(const std::vector<FPass> &passes, int variant, std::vector<void *> &fns) {
+bool jit_build(const std::vector<FPass> &passes, int variant, std::vector<void *> &fns,
+               std::vector<std::shared_ptr<void>> &keep) {
     fns.assign(passes.size(), nullptr);
+    keep.assign(passes.size(), nullptr);
     std::vector<std::string> srcs(passes.size());
     std::vector<uint64_t> keys(passes.size());
     std::vector<size_t> todo;
@@ -1309,10 +1319,13 @@ bool jit_build(const std::vector<FPass> &passes, int variant, std::vector<void *
             srcs[i] = jit_source(passes[i], variant, F, i + 1 == passes.size());
             keys[i] = hash_str(srcs[i]);
             auto it = g_jit_cache.find(keys[i]);
-            if (it != g_jit_cache.end())
-                fns[i] = it->second.fn;
-            else
+            std::shared_ptr<JitModule> m = it != g_jit_cache.end() ? it->second.lock() : nullptr;
+            if (m) {
+                fns[i] = (void *)m->fn;
+                keep[i] = m;
+            } else {
                 todo.push_back(i);
+            }
         }
     }
     if (!todo.empty()) {
@@ -1337,22 +1350,28 @@ bool jit_build(const std::vector<FPass> &passes, int variant, std::vector<void *
         if (!ok) {
             fprintf(stderr, "svb jit: compile failed, using the interpreter:\n%s\n", g_jit_err.c_str());
             fns.clear();
+            keep.clear();
             return false;
         }
         std::lock_guard<std::mutex> lk(g_jit_mu);
         for (size_t i : todo) {
-            JitFn f;
-            if (cudaLibraryLoadData(&f.lib, cubins[i].data(), nullptr, nullptr, 0, nullptr, nullptr, 0) !=
+            auto m = std::make_shared<JitModule>();
+            if (cudaLibraryLoadData(&m->lib, cubins[i].data(), nullptr, nullptr, 0, nullptr, nullptr, 0) !=
                     cudaSuccess ||
-                cudaLibraryGetKernel(&f.fn, f.lib, "kpass") != cudaSuccess ||
-                (jit_dyn_smem(passes[i]) && !set_dyn_smem(f.fn, jit_dyn_smem(passes[i])))) {
+                cudaLibraryGetKernel(&m->fn, m->lib, "kpass") != cudaSuccess ||
+                (jit_dyn_smem(passes[i]) && !set_dyn_smem(m->fn, jit_dyn_smem(passes[i])))) {
                 cudaGetLastError();
                 fns.clear();
+                keep.clear();
                 return false;
             }
-            g_jit_cache[keys[i]] = f;
-            fns[i] = (void *)f.fn;
+            g_jit_cache[keys[i]] = m;
+            fns[i] = (void *)m->fn;
+            keep[i] = m;
         }
+        if (g_jit_cache.size() > 4096)  // drop entries whose modules are gone
+            for (auto it = g_jit_cache.begin(); it != g_jit_cache.end();)
+                it = it->second.expired() ? g_jit_cache.erase(it) : std::next(it);
     }
     return true;
 }

@@ -473,3 +473,20 @@ def test_simulate_batch_equals_serial(cuda_ok):
     for got, want in zip(inplace, serial):
         assert np.array_equal(got, want)
     assert device.simulate_batch(circ, [], fma=True, jit=True) == []
+
+
+def test_plan_cache_eviction_unloads_and_rebuilds(cuda_ok, monkeypatch):
+    # plans beyond the cache bound are dropped with their JIT modules; a
+    # circuit seen again is re-planned and recompiled, same results
+    monkeypatch.setenv("SVB_PLAN_CACHE_MB", "0")  # keep only the 4 most recent plans
+    n = 16
+    rng = np.random.default_rng(99)
+    a = w.random_state_array(rng, n)
+    circs = [w.random_layer_circuit(n, 3, seed=1000 + i) for i in range(7)]
+    first = device.simulate(circs[0], a.copy(), fma=True, jit=True)
+    for c in circs[1:]:
+        device.simulate(c, a.copy(), fma=True, jit=True)
+    again = device.simulate(circs[0], a.copy(), fma=True, jit=True)
+    assert np.array_equal(again, first)
+    want = oracle.run_ops(a.copy(), w.oracle_ops(circs[0]))
+    assert np.max(np.abs(again - want)) <= TOL
