@@ -183,6 +183,10 @@ int svb_host_run_ops(const double *host_in, double *host_out, int64_t n_amps, co
  * host_in[k]; results equal nbatch calls of svb_host_run_ops bit for bit. */
 int svb_host_run_ops_batch(const double *const *host_in, double *const *host_out, int nbatch,
                            int64_t n_amps, const svb_op *ops, int nops, unsigned flags);
+/* Free the device staging buffers the host-memory calls keep between calls
+ * (one state for svb_host_*, three for the batch call); they are
+ * reallocated on the next call. */
+int svb_release_staging(void);
 
 /* ---- partitioned state over 2^k ranks (engine.py DistState) ------------- */
 

@@ -73,6 +73,7 @@ _SIGS = {
     "svb_host_apply_1q": ([_vp, _i64, _dp, _int], _int),
     "svb_host_apply_c1q": ([_vp, _i64, _dp, _int, _int], _int),
     "svb_host_run_ops": ([_vp, _vp, _i64, ctypes.POINTER(SvbOp), _int, ctypes.c_uint], _int),
+    "svb_release_staging": ([], _int),
     "svb_host_run_ops_batch": ([ctypes.POINTER(_vp), ctypes.POINTER(_vp), _int, _i64, ctypes.POINTER(SvbOp), _int,
                                 ctypes.c_uint], _int),
     "svb_profile_enable": ([_int], _int),

@@ -615,6 +615,34 @@ int svb_host_run_ops_batch(const double *const *host_in, double *const *host_out
     return SVB_OK;
 }
 
+int svb_release_staging(void) {
+    {
+        std::lock_guard<std::mutex> lk(g_stage.mu);
+        if (g_stage.ptr) {
+            int cur = 0;
+            cudaGetDevice(&cur);
+            cudaSetDevice(g_stage.device);
+            cudaFree(g_stage.ptr);
+            cudaSetDevice(cur);
+        }
+        g_stage.ptr = nullptr;
+        g_stage.bytes = 0;
+    }
+    std::lock_guard<std::mutex> lk(g_batch.mu);
+    if (g_batch.device >= 0) {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(g_batch.device);
+        for (int i = 0; i < 3; ++i) {
+            cudaFree(g_batch.buf[i]);
+            g_batch.buf[i] = nullptr;
+        }
+        cudaSetDevice(cur);
+        g_batch.bytes = 0;
+    }
+    return SVB_OK;
+}
+
 int svb_profile_enable(int on) {
     std::lock_guard<std::mutex> lk(g_prof_mu);
     cudaDeviceSynchronize();

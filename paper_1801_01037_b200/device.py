@@ -237,5 +237,10 @@ def simulate_batch(circuit: Circuit, inputs, outs=None, fuse: bool = True, stric
     return dsts
 
 
+def release_staging() -> None:
+    """Free the device buffers simulate / simulate_batch keep between calls."""
+    _lib.check(_lib.load().svb_release_staging(), "release_staging")
+
+
 def gate_op(kind: str, gate: Gate2x2, target: int, control: int | None = None) -> GateOp:
     return GateOp(kind, gate, target, control)

@@ -473,6 +473,11 @@ def test_simulate_batch_equals_serial(cuda_ok):
     for got, want in zip(inplace, serial):
         assert np.array_equal(got, want)
     assert device.simulate_batch(circ, [], fma=True, jit=True) == []
+    device.release_staging()  # buffers come back on the next call
+    again = device.simulate_batch(circ, [states[0].copy()], fma=True, jit=True)[0]
+    assert np.array_equal(again, serial[0])
+    device.release_staging()
+    assert np.array_equal(device.simulate(circ, states[1].copy(), fma=True, jit=True), serial[1])
 
 
 def test_plan_cache_eviction_unloads_and_rebuilds(cuda_ok, monkeypatch):
