@@ -42,7 +42,7 @@ inline int NR() { return 1 << t_fs; }
 
 struct Out {
     std::string s;
-    void operator()(const char *fmt, ...) {
+    __attribute__((format(printf, 2, 3))) void operator()(const char *fmt, ...) {
         char tmp[512];
         va_list ap;
         va_start(ap, fmt);
@@ -349,8 +349,11 @@ std::string pcond(uint64_t m) {
 // through a pending swap may leave them different)
 thread_local int *t_code = nullptr;
 
+void slot_phase_flush(Out &o, int s);
+
 void pend_flush(Out &o, int s) {
     if (!t_pend || !t_pend[s]) return;
+    slot_phase_flush(o, s);  // a data swap along s mixes its lo / hi registers
     if (t_code)
         for (int i = 0; i < NR(); ++i) {
             const int j = i | (1 << s);
@@ -821,10 +824,72 @@ std::string cm_ph(int c) {
     return b;
 }
 
+// Per-slot phases (fast mode).  A diagonal gate whose only slot is s --
+// target s under a thread / tile control with q11 = 1 (controlled phase
+// from a thread or a qubit outside the tile), or control s with a thread /
+// tile target -- multiplies the registers with slot bit s set by one
+// per-thread value.  Those values are multiplied into a per-thread `hs<s>`
+// (scalar work) and applied to the 16 registers once, when a non-diagonal
+// gate targets s, a pending swap along s is flushed, or the group ends:
+// QFT passes carry dozens of such phases per slot.  SVB_JIT_SLOTPH=0: off.
+thread_local unsigned t_hs = 0;  // slots whose hs is not 1
+
+bool slot_phase_on() {
+    const char *e = getenv("SVB_JIT_SLOTPH");
+    return !e || atoi(e) != 0;
+}
+
+void slot_phase_flush(Out &o, int s) {
+    if (!((t_hs >> s) & 1) || !t_code) return;
+    for (int i = 0; i < NR(); ++i) {
+        if (!((i >> s) & 1)) continue;
+        double k1 = 1.0, k2 = 1.0;
+        const char *m1 = phys(t_code[i], 0, k1), *m2 = phys(t_code[i], 1, k2);
+        auto sg = [](double k) { return k < 0 ? "-" : ""; };
+        o("{ const d2 X = v[%d]; v[%d] = mk(__fma_rn(hs%d.x, %sX.%s, %s__dmul_rn(hs%d.y, X.%s)), "
+          "__fma_rn(hs%d.x, %sX.%s, %s__dmul_rn(hs%d.y, X.%s))); }\n",
+          i, i, s, sg(k1), m1, sg(-k2), s, m2, s, sg(k2), m2, sg(k1), s, m1);
+        t_code[i] = 0;
+    }
+    o("hs%d = mk(1.0, 0.0);\n", s);
+    t_hs &= ~(1u << s);
+}
+
+// true if g was taken into a per-slot phase
+bool slot_phase_take(Out &o, const FGate &g) {
+    if (g.op < FOP_DIAG || !slot_phase_on()) return false;
+    const int c = g.op - FOP_DIAG;
+    const int tpos = (c >> 1) % (FSMAX + 1);
+    int s;
+    std::string pred;
+    double2 f1, f0;  // factor when pred holds / not
+    if (tpos < FTPOS_THREAD && !(c & 1) && g.cl >= 0 && unit_code(g.m[0]) == 0) {
+        s = tpos;  // target slot, thread / tile control
+        pred = pbit(g.cl);
+        f1 = g.m[3];
+        f0 = make_double2(1.0, 0.0);
+    } else if (tpos == FTPOS_THREAD && (c & 1) && g.cl < 0) {
+        s = slot_of_mask(g.cmask, -1);  // control slot, thread / tile target
+        if (s < 0) return false;
+        pred = pbit(g.tl);
+        f1 = g.m[3];
+        f0 = g.m[0];
+    } else {
+        return false;
+    }
+    if (t_pend && t_pend[s]) return false;  // (the pending-swap paths handle it)
+    o("{ const bool b = %s; hs%d = cm(b ? %s : %s, b ? %s : %s, hs%d); }\n", pred.c_str(), s, lit(f1.x).c_str(),
+      lit(f0.x).c_str(), lit(f1.y).c_str(), lit(f0.y).c_str(), s);
+    t_hs |= 1u << s;
+    return true;
+}
+
 bool pend_through(Out &o, const FGate &g, int *code, double2 &F);
 
 void emit_gate_fast(Out &o, const FGate &g, int *code, double2 &F) {
     const int op = g.op;
+    if (slot_phase_take(o, g)) return;
+    if (op < FOP_DIAG) slot_phase_flush(o, (op >> 1) % FSMAX);  // a non-diagonal gate on that slot
     if (pend_through(o, g, code, F)) return;
     pend_conflicts(o, g);
     if (op >= FOP_DIAG && phase_mode()) {
@@ -1118,8 +1183,11 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             int code[FREGMAX] = {0};
             t_code = code;
             t_phase = false;
+            t_hs = 0;
             o("d2 ph = mk(1.0, 0.0);\n");
+            for (int k = 0; k < NS(); ++k) o("d2 hs%d = mk(1.0, 0.0);\n", k);
             for (int q = G.first; q < G.first + G.count; ++q) emit_gate_fast(o, P.gates[q], code, F);
+            for (int k = 0; k < NS(); ++k) slot_phase_flush(o, k);
             const double mag = cabsh(F);
             const bool applyF = gi == P.ngroups - 1 && (last || mag < 0x1p-200 || mag > 0x1p200) &&
                                 !(F.x == 1.0 && F.y == 0.0);
