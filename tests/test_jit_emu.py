@@ -39,7 +39,7 @@ def _controlled_heavy(n, rng, count):
 
 @pytest.mark.skipif(shutil.which("g++") is None, reason="g++ not available")
 @pytest.mark.parametrize("case,n,fm", [("layers", 15, 11), ("qft", 15, 11), ("controlled", 15, 11),
-                                       ("layers", 17, 12), ("controlled", 17, 12)])
+                                       ("layers", 17, 12), ("controlled", 17, 12), ("qft", 17, 12)])
 def test_generated_passes_match_oracle(case, n, fm, tmp_path, monkeypatch):
     # fm 11: one shared buffer, 4 CTAs/SM; fm 12: next-tile prefetch (mode 2)
     monkeypatch.setenv("SVB_JIT_FM", str(fm))
