@@ -495,3 +495,31 @@ def test_plan_cache_eviction_unloads_and_rebuilds(cuda_ok, monkeypatch):
     assert np.array_equal(again, first)
     want = oracle.run_ops(a.copy(), w.oracle_ops(circs[0]))
     assert np.max(np.abs(again - want)) <= TOL
+
+
+def test_jit_fast_fuzz_vs_oracle(cuda_ok):
+    # the bench's path (JIT, FMA, factor extraction, outside-tile plans,
+    # per-thread / per-slot phases, pending swaps) on random circuits drawn
+    # from mixed gate pools -- a net for code-generation and compiler
+    # regressions
+    rng = np.random.default_rng(2024)
+    x = standard_gate("x")
+    base = [standard_gate(g) for g in "XYZHST"] + [x, x]
+    for trial in range(12):
+        n = int(rng.integers(15, 21))
+        pool = base + [rx(float(rng.uniform(0, 6.3))), ry(float(rng.uniform(0, 6.3))),
+                       rz(float(rng.uniform(0, 6.3))), phase(float(rng.uniform(0, 6.3))), w.random_unitary2(rng)]
+        p_ctl = float(rng.uniform(0.1, 0.7))
+        ops = []
+        for _ in range(int(rng.integers(100, 600))):
+            g = pool[int(rng.integers(len(pool)))]
+            if rng.random() < p_ctl:
+                c, t = rng.choice(n, size=2, replace=False)
+                ops.append(GateOp("controlled", g, int(t), int(c)))
+            else:
+                ops.append(GateOp("single", g, int(rng.integers(n))))
+        circ = Circuit(n, tuple(ops))
+        a = w.random_state_array(rng, n)
+        want = oracle.run_ops(a.copy(), w.oracle_ops(circ), workers=16)
+        got = device.simulate(circ, a.copy(), fma=True, jit=True)
+        assert np.max(np.abs(got - want)) <= TOL, (trial, n, np.max(np.abs(got - want)))
