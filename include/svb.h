@@ -161,6 +161,21 @@ int svb_exchange_own_row_packed(void *own, const void *other_packed, int64_t cou
 int svb_pair_update(void *lo_slab, void *hi_slab, int64_t begin, int64_t end, const double q[8],
                     int cbit, void *stream);
 
+/* Peer-memory transport of the multi-process engine (DistEngine(peer=True);
+ * replaces the send/recv of engine.py:359-389 and its layout swaps): every
+ * rank exports its slab (svb_ipc_handle, 64 opaque bytes shipped over the
+ * control-plane process group), opens its partners' (svb_ipc_open), and a
+ * global-target gate or a layout swap runs as one kernel per rank that
+ * reads and writes the partner slab in place -- svb_pair_update above, and
+ * svb_peer_swap_half: for j in [begin, end) swap a[ins(j, bit, va)] with
+ * b[ins(j, bit, vb)] (ins: insert the value as bit `bit` of j). */
+int svb_peer_swap_half(void *a, void *b, int64_t begin, int64_t end, int bit, int va, int vb, void *stream);
+/* handle of the allocation holding dev_ptr, and dev_ptr's byte offset in it
+ * (svb_ipc_open returns the allocation's base: add the offset) */
+int svb_ipc_handle(const void *dev_ptr, unsigned char handle[64], int64_t *offset);
+int svb_ipc_open(const unsigned char handle[64], void **dev_ptr);
+int svb_ipc_close(void *dev_ptr);
+
 /* ---- host buffers, synchronous (the svsim kernel-backend contract) ------ */
 
 /* Backend-module contract apply_single(amps, q11, q12, q21, q22, target,

@@ -74,6 +74,10 @@ _SIGS = {
     "svb_host_apply_c1q": ([_vp, _i64, _dp, _int, _int], _int),
     "svb_host_run_ops": ([_vp, _vp, _i64, ctypes.POINTER(SvbOp), _int, ctypes.c_uint], _int),
     "svb_release_staging": ([], _int),
+    "svb_peer_swap_half": ([_vp, _vp, _i64, _i64, _int, _int, _int, _vp], _int),
+    "svb_ipc_handle": ([_vp, ctypes.c_char_p, ctypes.POINTER(_i64)], _int),
+    "svb_ipc_open": ([ctypes.c_char_p, ctypes.POINTER(_vp)], _int),
+    "svb_ipc_close": ([_vp], _int),
     "svb_host_run_ops_batch": ([ctypes.POINTER(_vp), ctypes.POINTER(_vp), _int, _i64, ctypes.POINTER(SvbOp), _int,
                                 ctypes.c_uint], _int),
     "svb_profile_enable": ([_int], _int),

@@ -20,6 +20,8 @@ namespace svb {
 
 LaunchInfo launch_gate(double2 *a, int64_t n_amps, const Gate &g, int t, int c, cudaStream_t s);
 LaunchInfo launch_dense_embed(double2 *u, int64_t dim, const Gate &g, int t, int c, cudaStream_t s);
+LaunchInfo launch_peer_swap_half(double2 *a, double2 *b, int64_t begin, int64_t end, int bit, int va, int vb,
+                                 cudaStream_t s);
 LaunchInfo launch_dense_matvec(const double2 *u, const double2 *x, double2 *y, int64_t dim, int64_t row0,
                                int64_t nrows, cudaStream_t s);
 int launch_norm2(const double2 *a, int64_t n, double *scratch, cudaStream_t s);
@@ -442,6 +444,68 @@ int svb_pair_update(void *lo_slab, void *hi_slab, int64_t begin, int64_t end, co
     prof_end((cudaStream_t)stream, li);
     g_launches += li.kernels;
     SVB_CHECK_LAUNCH("svb_pair_update");
+    return SVB_OK;
+}
+
+int svb_peer_swap_half(void *a, void *b, int64_t begin, int64_t end, int bit, int va, int vb, void *stream) {
+    if (!a || !b || begin < 0 || end < begin || bit < 0 || bit > 62 || (va & ~1) || (vb & ~1)) {
+        set_error("bad arguments to svb_peer_swap_half");
+        return SVB_EINVAL;
+    }
+    prof_begin((cudaStream_t)stream);
+    LaunchInfo li = launch_peer_swap_half((double2 *)a, (double2 *)b, begin, end, bit, va, vb, (cudaStream_t)stream);
+    prof_end((cudaStream_t)stream, li);
+    g_launches += li.kernels;
+    SVB_CHECK_LAUNCH("svb_peer_swap_half");
+    return SVB_OK;
+}
+
+int svb_ipc_handle(const void *dev_ptr, unsigned char handle[64], int64_t *offset) {
+    if (!dev_ptr || !handle || !offset) {
+        set_error("svb_ipc_handle: NULL argument");
+        return SVB_EINVAL;
+    }
+    cudaIpcMemHandle_t h;
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void *>(dev_ptr));
+    if (e != cudaSuccess) return cuda_status(e, "cudaIpcGetMemHandle");
+    memcpy(handle, &h, 64);
+    // the handle names the whole allocation (a caching allocator's segment);
+    // the opener gets its base, so ship the buffer's offset in it
+    typedef int (*range_t)(unsigned long long *, size_t *, unsigned long long);
+    static range_t range = [] {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return (range_t)fn;
+    }();
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (!range || range(&base, &size, (unsigned long long)(uintptr_t)dev_ptr) != 0) {
+        set_error("svb_ipc_handle: cuMemGetAddressRange unavailable or failed");
+        return SVB_ECUDA;
+    }
+    *offset = int64_t((uintptr_t)dev_ptr - base);
+    return SVB_OK;
+}
+
+int svb_ipc_open(const unsigned char handle[64], void **dev_ptr) {
+    if (!handle || !dev_ptr) {
+        set_error("svb_ipc_open: NULL argument");
+        return SVB_EINVAL;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, 64);
+    cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_status(e, "cudaIpcOpenMemHandle");
+    return SVB_OK;
+}
+
+int svb_ipc_close(void *dev_ptr) {
+    cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+    if (e != cudaSuccess) return cuda_status(e, "cudaIpcCloseMemHandle");
     return SVB_OK;
 }
 

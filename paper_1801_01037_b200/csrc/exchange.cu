@@ -192,6 +192,34 @@ LaunchInfo launch_exchange_packed(double2 *own, const double2 *other, int64_t co
     return LaunchInfo{1, PROF_EXCHANGE, count * 48};
 }
 
+// k_peer_swap_half: the rank-bit <-> local-bit swap of the layout engine
+// over peer memory.  Half index j in [begin, end) names position
+// ins(j, bit, va) of slab a and ins(j, bit, vb) of slab b (ins: insert `v`
+// as bit `bit` of j); the two amplitudes trade places.  The two ranks of a
+// pair split the j range, each reading and writing the partner's slab
+// through NVLink -- the pack / send / receive / unpack of the NCCL engine in
+// one kernel, no staging.
+__global__ void __launch_bounds__(kXThreads) k_peer_swap_half(double2 *a, double2 *b, int64_t begin, int64_t end,
+                                                              int bit, int va, int vb) {
+    const int64_t stride = int64_t(gridDim.x) * kXThreads;
+    const int64_t low = (int64_t(1) << bit) - 1;
+    for (int64_t j = begin + int64_t(blockIdx.x) * kXThreads + threadIdx.x; j < end; j += stride) {
+        const int64_t hi = (j >> bit) << (bit + 1), lo = j & low;
+        const int64_t ia = hi | (int64_t(va) << bit) | lo, ib = hi | (int64_t(vb) << bit) | lo;
+        const double2 x = a[ia], y = b[ib];
+        a[ia] = y;
+        b[ib] = x;
+    }
+}
+
+LaunchInfo launch_peer_swap_half(double2 *a, double2 *b, int64_t begin, int64_t end, int bit, int va, int vb,
+                                 cudaStream_t s) {
+    if (end <= begin) return LaunchInfo{0, PROF_EXCHANGE, 0};
+    const int64_t blocks = std::min<int64_t>((end - begin + kXThreads - 1) / kXThreads, 148 * 8);
+    k_peer_swap_half<<<(unsigned)blocks, kXThreads, 0, s>>>(a, b, begin, end, bit, va, vb);
+    return LaunchInfo{1, PROF_EXCHANGE, (end - begin) * 64};
+}
+
 LaunchInfo launch_pair_update(double2 *lo_slab, double2 *hi_slab, int64_t begin, int64_t end,
                               const Gate &g, int cbit, cudaStream_t s) {
     if (end <= begin) return LaunchInfo{0, PROF_EXCHANGE, 0};

@@ -104,6 +104,33 @@ class CudaCompute:
                 ctypes.c_void_p(own.data_ptr()), ctypes.c_void_p(other.data_ptr()), count, q,
                 int(own_is_low), cbit, offset, self._sp()), "exchange")
 
+    # -- peer-memory transport (DistEngine(peer=True)) --------------------
+
+    def ipc_handle(self, slab) -> tuple[bytes, int]:
+        """(handle of the allocation holding slab, slab's byte offset in it)"""
+        h = ctypes.create_string_buffer(64)
+        off = ctypes.c_int64()
+        self._lib.check(self.lib.svb_ipc_handle(ctypes.c_void_p(slab.data_ptr()), h, ctypes.byref(off)),
+                        "ipc_handle")
+        return h.raw, off.value
+
+    def ipc_open(self, handle: tuple[bytes, int]) -> tuple[int, int]:
+        """(mapped allocation base, slab pointer)"""
+        p = ctypes.c_void_p()
+        self._lib.check(self.lib.svb_ipc_open(ctypes.c_char_p(handle[0]), ctypes.byref(p)), "ipc_open")
+        return p.value, p.value + handle[1]
+
+    def ipc_close(self, ptr: int) -> None:
+        self._lib.check(self.lib.svb_ipc_close(ctypes.c_void_p(ptr)), "ipc_close")
+
+    def pair_update(self, lo_ptr: int, hi_ptr: int, begin: int, end: int, gate: Gate2x2, cbit: int) -> None:
+        self._lib.check(self.lib.svb_pair_update(ctypes.c_void_p(lo_ptr), ctypes.c_void_p(hi_ptr), begin, end,
+                                                 self._lib.gate_array(gate), cbit, self._sp()), "pair_update")
+
+    def peer_swap_half(self, a_ptr: int, b_ptr: int, begin: int, end: int, bit: int, va: int, vb: int) -> None:
+        self._lib.check(self.lib.svb_peer_swap_half(ctypes.c_void_p(a_ptr), ctypes.c_void_p(b_ptr), begin, end,
+                                                    bit, va, vb, self._sp()), "peer_swap_half")
+
     def norm2(self, slab) -> float:
         out = ctypes.c_double()
         self._lib.check(self.lib.svb_norm2(ctypes.c_void_p(slab.data_ptr()), slab.shape[0],
@@ -133,7 +160,7 @@ class DistEngine:
 
     def __init__(self, n: int, compute=None, group=None, initial=None, chunk: int = DEFAULT_CHUNK,
                  fuse: bool = True, elide_diagonal: bool = True, fma: bool = False, jit: bool = False,
-                 layout: bool = False):
+                 layout: bool = False, peer: bool = False):
         import torch.distributed as dist
 
         self.dist = dist
@@ -170,6 +197,44 @@ class DistEngine:
         self._pending_key = None  # the cached tuple _pending was copied from, if any
         self._scheds: dict = {}
         self._bufs = None
+        # peer: exchanges and swaps read / write the partner's slab in place
+        # (CUDA IPC; NVLink P2P between GPUs) -- one kernel per rank between
+        # two barriers of the process group, which only carries control
+        self.peer = peer
+        self._peers: dict[int, int] = {}
+        self._maps: list[int] = []
+        if peer:
+            handles = [None] * self.world
+            dist.all_gather_object(handles, self.compute.ipc_handle(self.slab), group=self.group)
+            err = None
+            try:
+                for r, h in enumerate(handles):
+                    if r != self.rank:
+                        base, ptr = self.compute.ipc_open(h)
+                        self._maps.append(base)
+                        self._peers[r] = ptr
+            except Exception as e:  # e.g. no peer access between these GPUs
+                err = str(e)
+            errs = [None] * self.world
+            dist.all_gather_object(errs, err, group=self.group)
+            if any(errs):  # every rank falls back together to the send/recv transport
+                for base in self._maps:
+                    self.compute.ipc_close(base)
+                self._peers, self._maps, self.peer = {}, [], False
+                if self.rank == 0:
+                    import sys
+
+                    print(f"DistEngine: peer transport unavailable ({next(e for e in errs if e)}); "
+                          "using send/recv", file=sys.stderr)
+
+    def close(self) -> None:
+        """Unmap the partners' slabs (peer mode); the engine is unusable after."""
+        self.compute.synchronize()
+        if self.peer:
+            self.dist.barrier(group=self.group)
+            for base in self._maps:
+                self.compute.ipc_close(base)
+            self._peers, self._maps = {}, []
 
     # -- helpers ------------------------------------------------------------
 
@@ -200,7 +265,36 @@ class DistEngine:
         else:
             self._pending.append(GateOp("controlled", d, 1 if cbit == 0 else 0, cbit))
 
+    def _peer_sync(self) -> None:
+        self.compute.synchronize()
+        self.dist.barrier(group=self.group)
+
+    def _exchange_peer(self, g: Gate2x2 | None, t: int, cbit: int | None) -> None:
+        """Global-target gate over peer memory: the pair (mine[j], partner[j])
+        is updated in place -- the lower rank for j < L/2, the upper for
+        j >= L/2 (k_pair_update; 8*L bytes each way over the link instead of
+        16*L).  g None: this rank does not act (regime iii) but joins the
+        barriers, which every rank passes twice per global gate."""
+        self._flush()
+        self._peer_sync()
+        if g is not None:
+            partner = self.rank ^ (1 << (t - self.boundary))
+            low = self.rank < partner
+            mine, theirs = self.slab.data_ptr(), self._peers[partner]
+            lo, hi = (mine, theirs) if low else (theirs, mine)
+            half = self.L // 2
+            begin, end = (0, half) if low else (half, self.L)
+            self.compute.pair_update(lo, hi, begin, end, g, -1 if cbit is None else cbit)
+            count = self.L if cbit is None else self.L // 2
+            self.stats.exchanges += 1
+            self.stats.messages += 1
+            self.stats.bytes_sent += 8 * count
+            self.stats.bytes_recv += 8 * count
+        self._peer_sync()
+
     def _exchange(self, g: Gate2x2, t: int, cbit: int | None) -> None:
+        if self.peer:
+            return self._exchange_peer(g, t, cbit)
         self._flush()
         dist = self.dist
         partner = self.rank ^ (1 << (t - self.boundary))
@@ -245,6 +339,8 @@ class DistEngine:
         """Swap rank bit (physical qubit) g with local bit l: each rank sends
         the half of its slab whose bit l differs from its own bit g to the
         partner and unpacks the partner's half into the same positions."""
+        if self.peer:
+            return self._swap_peer(g, l)
         self._flush()
         dist = self.dist
         partner = self.rank ^ (1 << (g - self.boundary))
@@ -277,6 +373,23 @@ class DistEngine:
         self.stats.messages += nchunks
         self.stats.bytes_sent += 16 * count
         self.stats.bytes_recv += 16 * count
+
+    def _swap_peer(self, g: int, l: int) -> None:
+        """Layout swap over peer memory: the half of my slab whose bit l is v
+        trades places with the partner's half whose bit l is 1 - v, in place
+        (k_peer_swap_half); the pair's two ranks split the L/2 positions."""
+        self._flush()
+        self._peer_sync()
+        partner = self.rank ^ (1 << (g - self.boundary))
+        v = 1 - ((self.rank >> (g - self.boundary)) & 1)  # the half that leaves
+        quarter = self.L // 4
+        begin, end = (0, quarter) if self.rank < partner else (quarter, self.L // 2)
+        self.compute.peer_swap_half(self.slab.data_ptr(), self._peers[partner], begin, end, l, v, 1 - v)
+        self.stats.swaps += 1
+        self.stats.messages += 1
+        self.stats.bytes_sent += 8 * self.L // 2
+        self.stats.bytes_recv += 8 * self.L // 2
+        self._peer_sync()
 
     def _schedule_layout(self, ops: tuple) -> tuple[list, int]:
         """Action list with dynamic global<->local qubit swaps.
@@ -362,7 +475,11 @@ class DistEngine:
         b = self.boundary
         if c is not None and c >= b:
             if not (self.rank >> (c - b)) & 1:
-                return  # regime (iii): this rank's control bit is clear
+                # regime (iii): this rank's control bit is clear; over peer
+                # memory it still joins the exchange's barriers
+                if self.peer and t >= b and not (self.elide_diagonal and _is_diag(g)):
+                    self._exchange(None, t, None)
+                return
             c = None  # acts as an uncontrolled gate on participating ranks
         if t < b:
             self._pending.append(GateOp("single", g, t) if c is None else GateOp("controlled", g, t, c))
@@ -485,7 +602,8 @@ def bench_main(args, clock_cls=None, peaks_fn=None) -> None:
     circuit = workloads.random_layer_circuit(n, layers)
     nops = len(circuit.ops)
     eng = DistEngine(n, fma=getattr(args, "fma", True), jit=getattr(args, "jit", True),
-                     layout=os.environ.get("SVB_DIST_LAYOUT", "1") != "0")
+                     layout=os.environ.get("SVB_DIST_LAYOUT", "1") != "0",
+                     peer=os.environ.get("SVB_DIST_PEER", "1") != "0" and world > 1)
     stream = torch.cuda.current_stream()
 
     def step():
@@ -547,6 +665,8 @@ def bench_main(args, clock_cls=None, peaks_fn=None) -> None:
             "config": {"workload": f"random layer circuit n={n} ({layers} layers) over {world} GPUs, "
                                    f"2^26 amplitudes per GPU, {k} global qubits",
                        "n_qubits": n, "global_qubits": k, "parallelism": f"state partition x{world}"},
+            "transport": "peer memory (CUDA IPC, one kernel per rank per exchange / swap)" if eng.peer
+                         else "NCCL send/recv, chunk-pipelined",
             "exchanges_per_step": ex / args.steps,
             "layout_swaps_per_step": (eng.stats.swaps - stats0[2]) / args.steps,
             "nvlink_bytes_sent_per_gpu_per_step": sent / args.steps,
