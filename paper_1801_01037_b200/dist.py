@@ -592,9 +592,17 @@ def bench_main(args, clock_cls=None, peaks_fn=None) -> None:
 
     from . import _lib, workloads
 
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one GPU per rank; SVB_DIST_BACKEND=gloo (control plane on the host,
+    # ranks may share a GPU) is a functional smoke of this path on one GPU
+    # with the peer transport -- its timings are not a multi-GPU measurement
+    backend = os.environ.get("SVB_DIST_BACKEND", "nccl")
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+    red_dev = "cuda" if backend == "nccl" else "cpu"
     rank, world = dist.get_rank(), dist.get_world_size()
     k = world.bit_length() - 1
     n = 26 + k
@@ -631,7 +639,7 @@ def bench_main(args, clock_cls=None, peaks_fn=None) -> None:
     launches = _lib.launch_count() - launches0
     prof = _lib.profile_read()
     _lib.profile_enable(False)
-    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=red_dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
     norm = eng.norm2()
@@ -651,7 +659,7 @@ def bench_main(args, clock_cls=None, peaks_fn=None) -> None:
         eng.run(circuit)
         host_out.copy_(eng.slab, non_blocking=True)
         torch.cuda.synchronize()
-    e2e_dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    e2e_dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=red_dev)
     dist.all_reduce(e2e_dt, op=dist.ReduceOp.MAX)
     e2e_dt = float(e2e_dt.item())
     if rank == 0:
