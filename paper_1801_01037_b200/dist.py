@@ -637,6 +637,7 @@ def bench_main(args, clock_cls=None, peaks_fn=None) -> None:
         torch.cuda.synchronize()
     dist.barrier()
     launches = _lib.launch_count() - launches0
+    stats1 = (eng.stats.exchanges, eng.stats.bytes_sent, eng.stats.swaps)  # the timed steps only
     prof = _lib.profile_read()
     _lib.profile_enable(False)
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=red_dev)
@@ -663,8 +664,8 @@ def bench_main(args, clock_cls=None, peaks_fn=None) -> None:
     dist.all_reduce(e2e_dt, op=dist.ReduceOp.MAX)
     e2e_dt = float(e2e_dt.item())
     if rank == 0:
-        ex = eng.stats.exchanges - stats0[0]
-        sent = eng.stats.bytes_sent - stats0[1]
+        ex = stats1[0] - stats0[0]
+        sent = stats1[1] - stats0[1]
         line = {
             "metric": "gate applications/s", "value": round(nops * args.steps / (ms / 1e3), 1),
             "unit": "gate_apps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -676,7 +677,7 @@ def bench_main(args, clock_cls=None, peaks_fn=None) -> None:
             "transport": "peer memory (CUDA IPC, one kernel per rank per exchange / swap)" if eng.peer
                          else "NCCL send/recv, chunk-pipelined",
             "exchanges_per_step": ex / args.steps,
-            "layout_swaps_per_step": (eng.stats.swaps - stats0[2]) / args.steps,
+            "layout_swaps_per_step": (stats1[2] - stats0[2]) / args.steps,
             "nvlink_bytes_sent_per_gpu_per_step": sent / args.steps,
             "gpu_launches": launches,
             "e2e": {"value": round(nops * e2e_steps / e2e_dt, 1), "unit": "gate_apps/s",
