@@ -10,9 +10,10 @@
 // k_pair_update: both rows of pairs (lo_slab[j], hi_slab[j]).  With peer
 //   access one GPU reads the partner slab over NVLink and writes both
 //   amplitudes back: the lower rank of a pair covers j < L/2, the upper rank
-//   j >= L/2, so each direction of the link carries 8*L bytes instead of a
-//   full 16*L slab exchange (the work split of scheme a, engine.py:206-238,
-//   without the staging buffer or the send-back).
+//   j >= L/2: each direction of the link carries 16*L bytes (a rank's reads
+//   and writes of the partner's half, plus the partner's of its own) -- the
+//   bytes of a slab exchange, but with no staging buffer, no send-back and
+//   no separate update pass (the work split of scheme a, engine.py:206-238).
 #include "svb_common.cuh"
 
 namespace svb {

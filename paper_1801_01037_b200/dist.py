@@ -272,8 +272,8 @@ class DistEngine:
     def _exchange_peer(self, g: Gate2x2 | None, t: int, cbit: int | None) -> None:
         """Global-target gate over peer memory: the pair (mine[j], partner[j])
         is updated in place -- the lower rank for j < L/2, the upper for
-        j >= L/2 (k_pair_update; 8*L bytes each way over the link instead of
-        16*L).  g None: this rank does not act (regime iii) but joins the
+        j >= L/2 (k_pair_update: 16*L bytes each way over the link, like a
+        slab exchange, but no staging buffers and no separate update pass).  g None: this rank does not act (regime iii) but joins the
         barriers, which every rank passes twice per global gate."""
         self._flush()
         self._peer_sync()
@@ -288,8 +288,11 @@ class DistEngine:
             count = self.L if cbit is None else self.L // 2
             self.stats.exchanges += 1
             self.stats.messages += 1
-            self.stats.bytes_sent += 8 * count
-            self.stats.bytes_recv += 8 * count
+            # link bytes each way: my writes into the partner's half plus the
+            # partner's reads of mine (the same 16 B per pair as send/recv,
+            # without the staging copies)
+            self.stats.bytes_sent += 16 * count
+            self.stats.bytes_recv += 16 * count
         self._peer_sync()
 
     def _exchange(self, g: Gate2x2, t: int, cbit: int | None) -> None:
@@ -387,8 +390,8 @@ class DistEngine:
         self.compute.peer_swap_half(self.slab.data_ptr(), self._peers[partner], begin, end, l, v, 1 - v)
         self.stats.swaps += 1
         self.stats.messages += 1
-        self.stats.bytes_sent += 8 * self.L // 2
-        self.stats.bytes_recv += 8 * self.L // 2
+        self.stats.bytes_sent += 16 * (self.L // 2)
+        self.stats.bytes_recv += 16 * (self.L // 2)
         self._peer_sync()
 
     def _schedule_layout(self, ops: tuple) -> tuple[list, int]:
