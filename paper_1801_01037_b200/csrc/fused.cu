@@ -898,6 +898,11 @@ static bool group_lookahead() {
 // its last group then stores every register through the extra bit
 // permutation.  Gates name logical qubits; everything on the device is
 // physical.
+static bool defer_diag() {
+    const char *e = getenv("SVB_FUSE_DEFERDIAG");
+    return !e || atoi(e) != 0;
+}
+
 static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, bool strict, bool regperm,
                        int fm, const int8_t *phys = nullptr, const int8_t *phys_next = nullptr,
                        int fs = FSLOTS) {
@@ -1132,6 +1137,58 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
                 // (nothing fit the chosen set -- cannot happen, but never loop)
                 fill_group(*g, placed, left, first, 0);
             }
+        }
+    }
+    // Move diagonal gates to the latest group they commute into (no
+    // non-diagonal gate or load / store permutation on their local bits in
+    // between): diagonals on thread or tile bits become per-thread phases
+    // that cost one multiply of every register per group that has any, so
+    // gathering them into fewer groups saves those multiplies.
+    // SVB_FUSE_DEFERDIAG=0 keeps them where the scan put them.
+    if (!strict && gps.size() > 1 && defer_diag()) {
+        const int G = (int)gps.size();
+        std::vector<uint64_t> in_perm(G, 0), out_perm(G, 0);  // local bits the load / store maps touch
+        for (int c = 0; c < G; ++c) {
+            const GroupPlan &g = gps[c];
+            uint64_t ti = g.qb, to = g.mb | g.permq;
+            for (int j = 0; j < fm; ++j) {
+                if (g.qcol[j] != (1 << j)) ti |= uint64_t(g.qcol[j] ^ (1 << j)) | (uint64_t(1) << j);
+                if (g.mcol[j] != (1 << j)) to |= uint64_t(g.mcol[j] ^ (1 << j)) | (uint64_t(1) << j);
+            }
+            in_perm[c] = ti;
+            out_perm[c] = to;
+        }
+        for (int c = 0; c + 1 < G; ++c) {
+            std::vector<int> keep;
+            const std::vector<int> gates = gps[c].gates;
+            for (size_t k = 0; k < gates.size(); ++k) {
+                const int q = gates[k];
+                const GateMeta &m = meta[q];
+                if (!m.diag) {
+                    keep.push_back(q);
+                    continue;
+                }
+                const uint64_t bits = gbits(m);
+                bool later_conflict = false;  // a non-diagonal gate after it in this group
+                for (size_t k2 = k + 1; k2 < gates.size() && !later_conflict; ++k2)
+                    later_conflict = !meta[gates[k2]].diag && (gbits(meta[gates[k2]]) & bits);
+                int dest = c;
+                if (!later_conflict && !(out_perm[c] & bits)) {
+                    for (int d = c + 1; d < G; ++d) {
+                        if (in_perm[d] & bits) break;
+                        dest = d;
+                        bool blocked = (out_perm[d] & bits) != 0;
+                        for (int q2 : gps[d].gates)
+                            if (!meta[q2].diag && (gbits(meta[q2]) & bits)) blocked = true;
+                        if (blocked) break;  // it goes first in d, before the conflict
+                    }
+                }
+                if (dest == c)
+                    keep.push_back(q);
+                else
+                    gps[dest].gates.insert(gps[dest].gates.begin(), q);
+            }
+            gps[c].gates = keep;
         }
     }
     if (gps.empty()) new_group();  // a pure layout pass (no gates)
