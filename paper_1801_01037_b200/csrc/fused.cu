@@ -1171,15 +1171,16 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
                 const uint64_t bits = gbits(m);
                 bool later_conflict = false;  // a non-diagonal gate after it in this group
                 for (size_t k2 = k + 1; k2 < gates.size() && !later_conflict; ++k2)
-                    later_conflict = !meta[gates[k2]].diag && (gbits(meta[gates[k2]]) & bits);
+                    later_conflict = !meta[gates[k2]].diag && meta[gates[k2]].tl >= 0 &&
+                                     ((bits >> meta[gates[k2]].tl) & 1);
                 int dest = c;
                 if (!later_conflict && !(out_perm[c] & bits)) {
                     for (int d = c + 1; d < G; ++d) {
                         if (in_perm[d] & bits) break;
                         dest = d;
                         bool blocked = (out_perm[d] & bits) != 0;
-                        for (int q2 : gps[d].gates)
-                            if (!meta[q2].diag && (gbits(meta[q2]) & bits)) blocked = true;
+                        for (int q2 : gps[d].gates)  // (controls are diagonal: they commute)
+                            if (!meta[q2].diag && meta[q2].tl >= 0 && ((bits >> meta[q2].tl) & 1)) blocked = true;
                         if (blocked) break;  // it goes first in d, before the conflict
                     }
                 }
