@@ -10,9 +10,15 @@
 //
 // The generated kernel has exactly the structure of k_fused (same tile,
 // register groups, load/store maps, direct HBM groups, swizzle) and the same
-// arithmetic (exact or FMA), so its results equal the interpreter's bit for
-// bit.  NVRTC compiles all passes of a plan in parallel host threads; modules
-// are cached in memory by source hash.
+// arithmetic (exact or FMA), so on the same plan its results equal the
+// interpreter's bit for bit.  The fast variant (FMA + factor extraction, the
+// bench default) adds what only generated code can do: tile-uniform
+// predicates for qubits outside the tile, per-thread and per-slot phases,
+// pending conditional swaps that gates pass through, a global factor applied
+// by the circuit's last pass.  NVRTC compiles all passes of a plan in
+// parallel host threads; loaded modules are shared by source hash and
+// unloaded with the last plan using them.  tools/jit_emu.py runs the
+// generated code on the host against the oracle (tests/test_jit_emu.py).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
