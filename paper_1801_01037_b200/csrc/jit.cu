@@ -392,7 +392,11 @@ void pend_conflicts(Out &o, const FGate &g) {
     const int op = g.op;
     if (op < FOP_DIAG) {
         const int t = (op >> 1) % FSMAX, ctrl = op & 1;
-        pend_flush(o, t);
+        // a gate of the form a I + b X on its target (X, CNOT, Rx, their
+        // controlled forms) commutes with a pending swap on that slot
+        const bool xtype = g.m[0].x == g.m[3].x && g.m[0].y == g.m[3].y && g.m[1].x == g.m[2].x &&
+                           g.m[1].y == g.m[2].y;
+        if (!xtype) pend_flush(o, t);
         if (ctrl) {
             const int k = slot_of_mask(g.cmask, t);
             if (k < 0)
@@ -418,7 +422,26 @@ void emit_gate_fold(Out &o, const FGate &g, int *code) {
     const double2 *m = g.m;
     const int op = g.op;
     const bool thread_ctl = g.cl >= 0;
+    // CNOT from slot k to slot s while k has a pending swap X_k^p: since
+    // X_k CNOT X_k = CNOT X_s, the registers get the plain CNOT (a rename)
+    // and X_s^p joins the pending swaps -- no flush (exact data moves only)
+    uint64_t carry = 0;
+    int carry_to = -1;
+    if (t_pend && op < FOP_DIAG && (op & 1) && !thread_ctl && m[0].x == 0 && m[0].y == 0 && m[3].x == 0 &&
+        m[3].y == 0 && unit_code(m[1]) == 0 && unit_code(m[2]) == 0) {
+        const int s = (op >> 1) % FSMAX;
+        const int k = slot_of_mask(g.cmask, s);
+        if (k >= 0 && t_pend[k]) {
+            carry = t_pend[k];
+            carry_to = s;
+            t_pend[k] = 0;  // (kept out of pend_conflicts' flush)
+        }
+    }
     pend_conflicts(o, g);
+    if (carry_to >= 0) {
+        const int k = slot_of_mask(g.cmask, carry_to);
+        t_pend[k] = carry;
+    }
     if (op < FOP_DIAG) {
         const int kind = (op >> 1) / FSMAX, s = (op >> 1) % FSMAX, ctrl = op & 1;
         const int u12 = unit_code(m[1]), u21 = unit_code(m[2]);
@@ -522,6 +545,7 @@ void emit_gate_fold(Out &o, const FGate &g, int *code) {
             code[i] = code[j] = 0;
         }
         if (thread_ctl) o("}\n");
+        if (carry_to >= 0) t_pend[carry_to] ^= carry;
         return;
     }
     const int code_ = op - FOP_DIAG;
@@ -897,7 +921,6 @@ void emit_gate_fast(Out &o, const FGate &g, int *code, double2 &F) {
     if (slot_phase_take(o, g)) return;
     if (op < FOP_DIAG) slot_phase_flush(o, (op >> 1) % FSMAX);  // a non-diagonal gate on that slot
     if (pend_through(o, g, code, F)) return;
-    pend_conflicts(o, g);
     if (op >= FOP_DIAG && phase_mode()) {
         const int c = op - FOP_DIAG, pm = phase_mode();
         const bool ok = ((g.tl >= FTILEBIT) ? (pm & 2) : (pm & 1)) && (g.cl < 0 || (pm & 4));
@@ -908,9 +931,10 @@ void emit_gate_fast(Out &o, const FGate &g, int *code, double2 &F) {
     }
     const bool uncontrolled = g.cl < 0 && !(op & 1);
     if (!uncontrolled) {  // a controlled gate scales only part of the state
-        emit_gate_fold(o, g, code);
+        emit_gate_fold(o, g, code);  // (handles the pending swaps itself)
         return;
     }
+    pend_conflicts(o, g);
     if (op < FOP_DIAG) {
         const int s = (op >> 1) % FSMAX;
         const int u12 = unit_code(g.m[1]), u21 = unit_code(g.m[2]);
