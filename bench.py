@@ -126,45 +126,85 @@ class ClockSampler:
 # CPU reference (oracle/ is the checker and the CPU baseline; never the product)
 
 
-def cpu_reference_rate(circuit, budget_s: float, cores: int) -> dict:
-    """The reference's compiled kernel (oracle/_ref, else the C port) on the
-    host over a bounded prefix of `circuit`, mode parallel_collapsed."""
-    sys.path.insert(0, os.path.join(REPO, "oracle"))
-    import oracle
+def workload_config(n: int = N_QUBITS, layers: int = LAYERS) -> dict:
+    """The workload keys both arms print (the driver compares the dicts);
+    implementation details go in each arm's `impl` key."""
+    return {"workload": f"random layer circuit n={n}, {layers} layers x ({n} 1q + {n // 2} CNOT) "
+                        f"= {layers * (n + n // 2)} ops (BASELINE configs[1])",
+            "n_qubits": n, "layers": layers, "ops_per_circuit": layers * (n + n // 2),
+            "initial_state": "|0...0>", "state_bytes": 16 << n,
+            "l2": "state 1 GiB > 126 MB L2; no flush needed"}
 
-    ref = oracle.ref_module()
-    kind = "reference" if ref is not None else "port"
-    amps = np.zeros(1 << circuit.n, np.complex128)
-    amps[0] = 1.0
 
-    def one(op):
-        g = op.gate
-        if ref is not None:
+class CpuReference:
+    """The reference's compiled stride kernel (oracle/_ref: svsim's own
+    _stride_cy built from /root/reference; else the C port) applying a
+    circuit op by op on host memory -- the paper's CPU path
+    (kernel/__init__.py:107-134 -> _stride_cy.pyx:24-90)."""
+
+    MODES = {"sequential": 0, "parallel_collapsed": 3}
+
+    def __init__(self, n: int, cores: int):
+        sys.path.insert(0, os.path.join(REPO, "oracle"))
+        import oracle
+
+        self.oracle = oracle
+        self.ref = oracle.ref_module()
+        self.kind = "reference" if self.ref is not None else "port"
+        self.cores = cores
+        self.amps = np.zeros(1 << n, np.complex128)
+        self.reset()
+
+    def reset(self) -> None:
+        self.amps[:] = 0
+        self.amps[0] = 1.0
+
+    def apply(self, op, mode: str = "parallel_collapsed") -> None:
+        g, a = op.gate, self.amps
+        workers = 1 if mode == "sequential" else self.cores
+        if self.ref is not None:
+            m = self.MODES[mode]
             if op.control is None:
-                ref.apply_single(amps, g.q11, g.q12, g.q21, g.q22, op.target, 3, cores)
+                self.ref.apply_single(a, g.q11, g.q12, g.q21, g.q22, op.target, m, workers)
             else:
-                ref.apply_controlled(amps, g.q11, g.q12, g.q21, g.q22, op.control, op.target, 3, cores)
+                self.ref.apply_controlled(a, g.q11, g.q12, g.q21, g.q22, op.control, op.target, m, workers)
+        elif op.control is None:
+            self.oracle.apply_single(a, g, op.target, workers)
         else:
-            if op.control is None:
-                oracle.apply_single(amps, g, op.target, cores)
-            else:
-                oracle.apply_controlled(amps, g, op.control, op.target, cores)
+            self.oracle.apply_controlled(a, g, op.control, op.target, workers)
 
+    def label(self, mode: str) -> str:
+        src = "svsim _stride_cy (oracle/_ref)" if self.ref is not None else "oracle C port"
+        threads = 1 if mode == "sequential" else self.cores
+        return f"{src} mode {mode} x{threads}"
+
+
+def cpu_reference_rate(circuit, budget_s: float, cores: int, mode: str = "parallel_collapsed") -> dict:
+    """Bounded sample: the first ops of `circuit` from |0...0> for about
+    budget_s seconds (the GPU arm's cpu_baseline; `sequential` is the
+    paper's own mode)."""
+    cpu = CpuReference(circuit.n, cores)
     done = 0
     t0 = time.perf_counter()
     for op in circuit.ops:
-        one(op)
+        cpu.apply(op, mode)
         done += 1
         if time.perf_counter() - t0 >= budget_s:
             break
     dt = time.perf_counter() - t0
-    return {"value": done / dt, "unit": UNIT, "cores": cores, "kind": kind,
-            "sample": f"first {done} of {len(circuit.ops)} ops of the n={circuit.n} random layer "
-                      f"circuit (configs[1]), {'svsim _stride_cy' if ref else 'oracle C port'} "
-                      f"mode parallel_collapsed x{cores}, {dt:.1f} s"}
+    return {"value": done / dt, "unit": UNIT, "cores": 1 if mode == "sequential" else cores, "kind": cpu.kind,
+            "sample": f"first {done} of {len(circuit.ops)} ops of the n={circuit.n} random layer circuit "
+                      f"(configs[1]) from |0...0>, {cpu.label(mode)}, {dt:.1f} s"}
 
 
 def run_reference_arm(args) -> None:
+    """--impl reference: the reference's CPU path on the whole configs[1]
+    circuit.  The circuit's 7,800 ops are split into K contiguous slices;
+    timed step i applies slice i, so the K timed steps apply the complete
+    circuit once, from |0...0>, on every host core (mode parallel_collapsed,
+    the reference's fastest).  Warm-up steps apply the first W slices to a
+    scratch run that is then reset.  value = 7,800 ops / total timed time.
+    Also a bounded sample of the paper's own `sequential` mode."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -172,27 +212,44 @@ def run_reference_arm(args) -> None:
 
     n = N_QUBITS
     circuit = workloads.random_layer_circuit(n, LAYERS)
+    ops = circuit.ops
     cores = host_cores()
     steps, warm = max(args.steps, 1), max(args.warmup, 0)
-    per_step = max(2.0, min(20.0, 150.0 / (steps + warm)))
-    for _ in range(warm):
-        cpu_reference_rate(circuit, per_step / 4, cores)
-    rates, samples = [], []
-    for _ in range(steps):
-        r = cpu_reference_rate(circuit, per_step, cores)
-        rates.append(r["value"])
-        samples.append(r)
-    value = float(np.mean(rates))
+    bounds = [len(ops) * i // steps for i in range(steps + 1)]
+    cpu = CpuReference(n, cores)
+    t0 = time.perf_counter()
+    for i in range(warm):
+        for op in ops[bounds[i % steps]:bounds[i % steps + 1]]:
+            cpu.apply(op)
+    warm_s = time.perf_counter() - t0
+    cpu.reset()
+    per_step = []
+    for i in range(steps):
+        t0 = time.perf_counter()
+        for op in ops[bounds[i]:bounds[i + 1]]:
+            cpu.apply(op)
+        per_step.append(time.perf_counter() - t0)
+    total = sum(per_step)
+    norm = float(np.vdot(cpu.amps, cpu.amps).real)
+    value = len(ops) / total
+    seq = None if args.no_sequential else cpu_reference_rate(circuit, args.seq_budget, cores, "sequential")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": steps, "warmup": warm,
-        "ms_per_step": 1e3 * len(circuit.ops) / value,
+        "ms_per_step": 1e3 * total / steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "c128", "data": "synthetic (seeded, BASELINE configs[1])",
-        "config": {"workload": f"random layer circuit n={n}, {LAYERS} layers, 7800 ops (configs[1])",
-                   "n_qubits": n, "layers": LAYERS},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": samples[-1]["kind"],
-                         "sample": samples[-1]["sample"]},
+        "dtype": "c128", "data": "synthetic (seeded numpy PCG64 circuit, |0...0> start)",
+        "config": workload_config(n, LAYERS),
+        "impl_detail": {"engine": cpu.label("parallel_collapsed"),
+                        "step": f"1/{steps} of the circuit: timed step i applies ops "
+                                f"[{len(ops)}*i/{steps}, {len(ops)}*(i+1)/{steps}); the {steps} timed steps "
+                                f"apply all {len(ops)} ops once, from |0...0>",
+                        "ops_per_step": len(ops) / steps, "timed_s": round(total, 3),
+                        "warmup_s": round(warm_s, 3), "norm_after_circuit": norm},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": cpu.kind,
+                         "sample": f"the whole {len(ops)}-op circuit from |0...0> over the {steps} timed "
+                                   f"steps, {cpu.label('parallel_collapsed')}, {total:.1f} s"},
+        "sequential": seq,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -217,14 +274,17 @@ def local_gate_sweep(n: int, reps: int, peak: float) -> dict:
     per_t = []
     for t in range(n):
         q = _lib.gate_array(circ.ops[t * reps].gate)
-        lib.svb_apply_1q(st.ptr, 1 << n, q, t, sp)  # warm
+        # repetition 1 warms the launch path untimed; 2..reps are timed, so the
+        # final state is exactly the 300 configs[2] applications
+        # (tests/test_gpu_large.py compares it with the oracle)
+        _lib.check(lib.svb_apply_1q(st.ptr, 1 << n, q, t, sp))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(reps):
+        for _ in range(reps - 1):
             _lib.check(lib.svb_apply_1q(st.ptr, 1 << n, q, t, sp))
         e1.record(stream)
         e1.synchronize()
-        ms = e0.elapsed_time(e1) / reps
+        ms = e0.elapsed_time(e1) / (reps - 1)
         per_t.append(bytes_per_app / ms / 1e6)
     nrm = device.norm2(st)
     del st
@@ -375,11 +435,10 @@ def run_gpu_arm(args) -> None:
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
         "data": "synthetic (seeded numpy PCG64 circuit, |0...0> start)",
-        "config": {"workload": f"random layer circuit n={n}, {LAYERS} layers x ({n} 1q + {n // 2} CNOT) "
-                               f"= {nops} ops (BASELINE configs[1])",
-                   "n_qubits": n, "layers": LAYERS, "ops_per_step": nops, "fused": not args.no_fuse, "fma": args.fma, "jit": args.jit,
-                   "hbm_passes_per_step": passes, "state_bytes": 16 << n,
-                   "l2": "state 1 GiB > 126 MB L2; no flush needed", "parallelism": "single GPU"},
+        "config": workload_config(n, LAYERS),
+        "impl_detail": {"engine": "libsvb svb_run_ops (include/svb.h)", "fused": not args.no_fuse,
+                        "fma": args.fma, "jit": args.jit, "hbm_passes_per_step": passes,
+                        "ops_per_step": nops, "parallelism": "single GPU"},
         "roofline": roofline,
         "kernels": kernels,
         "gpu_launches": launches,
@@ -417,6 +476,9 @@ def main(argv=None):
     ap.add_argument("--no-sweep", action="store_true", help="skip the configs[2] n=30 sweep")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU reference work")
+    ap.add_argument("--seq-budget", type=float, default=8.0,
+                    help="--impl reference: seconds of the paper's sequential mode (bounded sample)")
+    ap.add_argument("--no-sequential", action="store_true", help="--impl reference: skip the sequential sample")
     args = ap.parse_args(argv)
     if args.impl == "reference":
         run_reference_arm(args)

@@ -54,6 +54,7 @@ def lib():
         i64, c_int = ctypes.c_int64, ctypes.c_int
         L.or_apply_single.argtypes = [_dptr, i64, _dptr, c_int, c_int]
         L.or_apply_controlled.argtypes = [_dptr, i64, _dptr, c_int, c_int, c_int]
+        L.or_apply_single_reps.argtypes = [_dptr, i64, _dptr, c_int, c_int, c_int]
         L.or_exchange_own_row.argtypes = [_dptr, _dptr, i64, _dptr, c_int, c_int]
         L.or_norm2.argtypes = [_dptr, i64]
         L.or_norm2.restype = ctypes.c_double
@@ -96,6 +97,14 @@ def gate_q(g) -> np.ndarray:
 def apply_single(amps: np.ndarray, g, t: int, workers: int = 1) -> np.ndarray:
     q = gate_q(g)
     lib().or_apply_single(_p(amps), amps.shape[0], _p(q), int(t), int(workers))
+    return amps
+
+
+def apply_single_reps(amps: np.ndarray, g, t: int, reps: int, workers: int = 1) -> np.ndarray:
+    """`reps` applications of g on t; bit-identical to calling apply_single
+    `reps` times (each pair's update depends on that pair only)."""
+    q = gate_q(g)
+    lib().or_apply_single_reps(_p(amps), amps.shape[0], _p(q), int(t), int(reps), int(workers))
     return amps
 
 

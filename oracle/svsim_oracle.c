@@ -71,6 +71,26 @@ void or_apply_single(double *amps, int64_t n_amps, const double *q, int t, int w
     }
 }
 
+/* `reps` consecutive applications of the same single-qubit gate on target t
+ * (BASELINE configs[2]: 10 repetitions per target).  Each application
+ * updates every pair (base, base+2^t) from that pair's own two amplitudes
+ * only, so applying all `reps` to one pair before moving to the next pair is
+ * bit-identical to `reps` full sweeps of or_apply_single -- it only keeps
+ * the pair in registers (a checker speed-up; same arithmetic, same order per
+ * amplitude). */
+void or_apply_single_reps(double *amps, int64_t n_amps, const double *q, int t, int reps, int workers)
+{
+    dc *a = (dc *)amps;
+    dc q11 = load_q(q, 0), q12 = load_q(q, 1), q21 = load_q(q, 2), q22 = load_q(q, 3);
+    int64_t stride = (int64_t)1 << t;
+    int64_t npairs = n_amps >> 1;
+#pragma omp parallel for schedule(static) num_threads(workers > 0 ? workers : 1)
+    for (int64_t qq = 0; qq < npairs; ++qq) {
+        int64_t base = ((qq >> t) << (t + 1)) | (qq & (stride - 1));
+        for (int r = 0; r < reps; ++r) pair(a, base, stride, q11, q12, q21, q22);
+    }
+}
+
 /* Controlled gate: pair (base, base+2^t) updated only where bit c of base is
  * set (_stride_cy.pyx:57-90). */
 void or_apply_controlled(double *amps, int64_t n_amps, const double *q, int c, int t, int workers)

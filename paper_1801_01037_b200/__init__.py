@@ -61,7 +61,7 @@ _LAZY = {
     "DistState": "engine", "GateStats": "engine", "dist_init": "engine", "gather": "engine",
     "dist_apply_local": "engine", "dist_apply_scheme_a": "engine", "dist_apply_scheme_b": "engine",
     "dist_apply_chunked": "engine", "dist_apply_controlled": "engine", "run_circuit": "engine",
-    "time_ratio": "engine", "dist_norm2": "engine",
+    "time_ratio": "engine", "dist_norm2": "engine", "PeerTransport": "engine", "InMemoryTransport": "engine",
 }
 
 

@@ -41,6 +41,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -1816,6 +1817,23 @@ struct CompiledPlan {
     mutable int jit_state[3] = {0, 0, 0};
     mutable std::vector<void *> jit_fns[3];
     mutable std::vector<std::shared_ptr<void>> jit_keep[3];  // the loaded modules (unloaded with the plan)
+    // devices this plan's JIT kernels were launched on: before the modules are
+    // released (and unloaded), those devices are drained, so no launch of a
+    // module can still be queued when cudaLibraryUnload runs
+    mutable std::atomic<uint64_t> jit_devices{0};
+    ~CompiledPlan() {
+        const uint64_t m = jit_devices.load();
+        if (!m) return;
+        int cur = 0;
+        if (cudaGetDevice(&cur) != cudaSuccess) return;
+        for (int d = 0; d < 64; ++d)
+            if ((m >> d) & 1) {
+                cudaSetDevice(d);
+                cudaDeviceSynchronize();
+            }
+        cudaSetDevice(cur);
+        cudaGetLastError();
+    }
 };
 
 bool jit_build(const std::vector<FPass> &passes, int variant, std::vector<void *> &fns,
@@ -1897,11 +1915,16 @@ int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsi
         for (int i = 0; i < nops; ++i) single(ops[i]);
         return SVB_OK;
     }
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(k_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem());
-        cudaFuncSetAttribute(k_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem());
-        attr_set = true;
+    {  // the dynamic shared-memory opt-in is per device: set it for each device used
+        static std::atomic<uint64_t> attr_set{0};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const uint64_t bit = dev < 64 ? uint64_t(1) << dev : 0;
+        if (!(attr_set.load() & bit)) {
+            cudaFuncSetAttribute(k_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem());
+            cudaFuncSetAttribute(k_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem());
+            attr_set.fetch_or(bit);
+        }
     }
     const bool strict = flags & SVB_RUN_STRICT_ORDER;
     const bool fma = (flags & SVB_RUN_FMA) && !strict;
@@ -1916,7 +1939,12 @@ int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsi
         int &state = cp->jit_state[variant];
         if (state == 0)
             state = jit_build(cp->passes, variant, cp->jit_fns[variant], cp->jit_keep[variant]) ? 1 : -1;
-        if (state == 1) jit_fns = &cp->jit_fns[variant];
+        if (state == 1) {
+            jit_fns = &cp->jit_fns[variant];
+            int dev = 0;
+            cudaGetDevice(&dev);
+            if (dev < 64) cp->jit_devices.fetch_or(uint64_t(1) << dev);
+        }
     }
     if (!jit_fns && (cp->fm != FM || cp->fs != FSLOTS || cp->outside)) {  // JIT unavailable: the interpreter's plan
         cp = compiled_plan(n, ops, nops, strict, reg_perm(flags & ~SVB_RUN_JIT), FM, FSLOTS, false);

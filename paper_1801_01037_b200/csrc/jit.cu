@@ -1307,6 +1307,9 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
 struct JitModule {
     cudaLibrary_t lib = nullptr;
     cudaKernel_t fn = nullptr;
+    // (the plan holding the last reference drains every device it launched on
+    // before releasing it -- ~CompiledPlan in fused.cu -- so no queued launch
+    // of this module is outstanding here)
     ~JitModule() {
         if (lib) cudaLibraryUnload(lib);  // (errors at process teardown are harmless)
     }
@@ -1392,11 +1395,28 @@ static bool nvrtc_compile(const std::string &src, std::vector<char> &cubin, std:
     return true;
 }
 
-static bool set_dyn_smem(cudaKernel_t fn, size_t bytes) {
-    int d = 0;
-    cudaGetDevice(&d);
+// The >48 KiB dynamic shared-memory opt-in is a per-device attribute of a
+// library kernel: it is set for the device a launch runs on, the first time a
+// (kernel, device) pair is seen -- a plan loaded while cuda:0 was current
+// still launches on cuda:1.
+static bool set_dyn_smem(cudaKernel_t fn, size_t bytes, int d) {
     return cudaKernelSetAttributeForDevice(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes, d) ==
            cudaSuccess;
+}
+
+static bool ensure_dyn_smem(cudaKernel_t fn, size_t bytes) {
+    if (!bytes) return true;
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess) return false;
+    static std::mutex mu;
+    static std::unordered_map<const void *, uint64_t> done;  // kernel -> devices with the attribute
+    std::lock_guard<std::mutex> lk(mu);
+    uint64_t &mask = done[(const void *)fn];
+    const uint64_t bit = d < 64 ? uint64_t(1) << d : 0;
+    if (bit && (mask & bit)) return true;
+    if (!set_dyn_smem(fn, bytes, d)) return false;
+    mask |= bit;
+    return true;
 }
 
 // Compile (or fetch) one kernel per pass.  Returns false and leaves
@@ -1456,8 +1476,7 @@ bool jit_build(const std::vector<FPass> &passes, int variant, std::vector<void *
             auto m = std::make_shared<JitModule>();
             if (cudaLibraryLoadData(&m->lib, cubins[i].data(), nullptr, nullptr, 0, nullptr, nullptr, 0) !=
                     cudaSuccess ||
-                cudaLibraryGetKernel(&m->fn, m->lib, "kpass") != cudaSuccess ||
-                (jit_dyn_smem(passes[i]) && !set_dyn_smem(m->fn, jit_dyn_smem(passes[i])))) {
+                cudaLibraryGetKernel(&m->fn, m->lib, "kpass") != cudaSuccess) {
                 cudaGetLastError();
                 fns.clear();
                 keep.clear();
@@ -1507,6 +1526,7 @@ bool jit_launch(void *fn, const FPass &P, double2 *a, int64_t ntiles, cudaStream
         return v;
     }();
     const int grid = (int)std::min<int64_t>(ntiles, int64_t(sms) * jit_ctas_per_sm(P));
+    if (!ensure_dyn_smem((cudaKernel_t)fn, jit_dyn_smem(P))) return false;
     long long nt = ntiles;
     void *args[] = {&a, &nt};
     return cudaLaunchKernel((const void *)fn, dim3(grid), dim3(jit_threads(P)), args, jit_dyn_smem(P), s) ==

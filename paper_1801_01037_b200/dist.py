@@ -204,17 +204,28 @@ class DistEngine:
         self._peers: dict[int, int] = {}
         self._maps: list[int] = []
         if peer:
-            handles = [None] * self.world
-            dist.all_gather_object(handles, self.compute.ipc_handle(self.slab), group=self.group)
-            err = None
+            # export (may fail, e.g. VMM-backed slabs under expandable_segments)
+            # and import both report through the collectives below, so every
+            # rank sees every failure and all fall back together -- none is
+            # left waiting in a collective the others skipped
+            mine, err = None, None
             try:
-                for r, h in enumerate(handles):
-                    if r != self.rank:
-                        base, ptr = self.compute.ipc_open(h)
-                        self._maps.append(base)
-                        self._peers[r] = ptr
-            except Exception as e:  # e.g. no peer access between these GPUs
-                err = str(e)
+                mine = self.compute.ipc_handle(self.slab)
+            except Exception as e:
+                err = f"rank {self.rank}: export: {e}"
+            handles = [None] * self.world
+            dist.all_gather_object(handles, mine, group=self.group)
+            if err is None and any(h is None for h in handles):
+                err = "a partner could not export its slab"
+            if err is None:
+                try:
+                    for r, h in enumerate(handles):
+                        if r != self.rank:
+                            base, ptr = self.compute.ipc_open(h)
+                            self._maps.append(base)
+                            self._peers[r] = ptr
+                except Exception as e:  # e.g. no peer access between these GPUs
+                    err = f"rank {self.rank}: import: {e}"
             errs = [None] * self.world
             dist.all_gather_object(errs, err, group=self.group)
             if any(errs):  # every rank falls back together to the send/recv transport

@@ -35,7 +35,7 @@ import numpy as np
 
 from . import _lib
 from .core import Circuit, Gate2x2, StateVector
-from .errors import ContractViolation, ValidationError
+from .errors import CapacityError, ContractViolation, ValidationError
 from .partition import (
     SCHEME_A,
     SCHEME_B,
@@ -60,14 +60,52 @@ class GateStats:
     wall_time: float
 
 
+class PeerTransport:
+    """Accounting face of the transport (engine.py:57-120's counters).
+
+    The reference's InMemoryTransport moves every message through Python
+    FIFOs; here amplitudes move GPU to GPU through peer memory inside the
+    pair kernels, so the object keeps only what callers read from it: the
+    rank count and the per-sender message / byte counters of the reference
+    protocol (exact formulas, partition.protocol_accounting).  Exported as
+    ``InMemoryTransport`` too, so reference code that builds one and passes
+    it to dist_init / run_circuit keeps working."""
+
+    def __init__(self, nranks: int, record_log: bool = False):
+        if nranks < 1:
+            raise ValidationError(f"need at least one rank, got {nranks}")
+        self.nranks = int(nranks)
+        self.messages_sent = [0] * self.nranks
+        self.bytes_sent = [0] * self.nranks
+        self.log: list[tuple[int, int, int]] | None = [] if record_log else None
+
+    def count(self, src: int, dst: int, messages: int, nbytes: int) -> None:
+        self.messages_sent[src] += messages
+        self.bytes_sent[src] += nbytes
+        if self.log is not None and messages:
+            self.log.append((src, dst, nbytes))
+
+
+InMemoryTransport = PeerTransport
+
+
 class DistState:
     """2^k slabs plus the native handle that drives them (engine.py:132-140)."""
 
-    def __init__(self, plan: PartitionPlan, scheme: CommScheme | None, slabs, devices):
+    def __init__(self, plan: PartitionPlan, scheme: CommScheme | None, slabs, devices,
+                 transport: PeerTransport | None = None, buffer_amps: int | None = None,
+                 execution: str = "cooperative", strat=None, kernel_backend: str | None = None):
         self.plan = plan
         self.scheme = scheme
         self.slabs = slabs
         self.devices = list(devices)
+        self.transport = transport if transport is not None else PeerTransport(plan.p)
+        # per-rank protocol scratch the reference would allocate (engine.py:179):
+        # exchanges whose scheme needs more raise CapacityError like the reference
+        self.buffer_amps = plan.local_len if buffer_amps is None else buffer_amps
+        self.execution = execution
+        self.strat = strat
+        self.kernel_backend = kernel_backend
         lib = _lib.load()
         p = plan.p
         dev_arr = (ctypes.c_int * p)(*self.devices)
@@ -78,8 +116,14 @@ class DistState:
         torch.cuda.synchronize()
         _lib.check(lib.svb_dist_create(plan.n, plan.k, dev_arr, slab_arr, ctypes.byref(h)), "dist_init")
         self._h = h
-        self.messages_sent = [0] * p
-        self.bytes_sent = [0] * p
+
+    @property
+    def messages_sent(self) -> list[int]:
+        return self.transport.messages_sent
+
+    @property
+    def bytes_sent(self) -> list[int]:
+        return self.transport.bytes_sent
 
     @property
     def handle(self) -> ctypes.c_void_p:
@@ -108,21 +152,31 @@ class DistState:
             pass
 
 
-def dist_init(plan: PartitionPlan, scheme: CommScheme | None = None, devices=None,
-              initial=None) -> DistState:
+def dist_init(plan: PartitionPlan, transport: PeerTransport | None = None, scheme: CommScheme | None = None,
+              execution: str = "cooperative", strat=None, kernel_backend: str | None = None, *,
+              devices=None, initial=None) -> DistState:
     """|0...0> (or `initial`, host array / StateVector) across the plan's ranks
-    (engine.py:157-185).  devices: list of CUDA ordinals per rank, default all
-    ranks on the current device."""
+    (engine.py:157-185; same positional order -- plan, transport, scheme,
+    execution, strat, kernel_backend).  With a scheme, each rank's protocol
+    scratch is that scheme's requirement (exchanges of a scheme needing more
+    raise CapacityError); without one, a full slab.  Keyword-only extras:
+    devices (CUDA ordinal per rank, default all on the current device) and
+    initial."""
     import torch
 
     _lib.load()
+    if execution not in ("cooperative", "threads"):
+        raise ValidationError(f"unknown execution mode {execution!r}")
+    if transport is None:
+        transport = PeerTransport(plan.p)
+    elif transport.nranks != plan.p:
+        raise ValidationError(f"transport has {transport.nranks} ranks, plan needs {plan.p}")
     if devices is None:
         devices = [torch.cuda.current_device()] * plan.p
     devices = list(devices)
     if len(devices) != plan.p:
         raise ValidationError(f"need {plan.p} device ordinals, got {len(devices)}")
-    if scheme is not None:
-        scheme.buffer_amps(plan)  # reference validation (chunk size <= slab)
+    buf_amps = plan.local_len if scheme is None else max(scheme.buffer_amps(plan), 1)
     L = plan.local_len
     slabs = []
     if initial is not None:
@@ -137,7 +191,7 @@ def dist_init(plan: PartitionPlan, scheme: CommScheme | None = None, devices=Non
             if r == 0:
                 s[0] = 1.0
             slabs.append(s)
-    return DistState(plan, scheme, slabs, devices)
+    return DistState(plan, scheme, slabs, devices, transport, buf_amps, execution, strat, kernel_backend)
 
 
 def gather(ds: DistState) -> StateVector:
@@ -154,8 +208,7 @@ def _account(ds: DistState, scheme: CommScheme, t: int, cbit: int | None, partic
             continue
         q = r ^ (1 << gb)
         m, b = protocol_accounting(plan, scheme, r < q, cbit)
-        ds.messages_sent[r] += m
-        ds.bytes_sent[r] += b
+        ds.transport.count(r, q, m, b)
 
 
 def protocol_stats(circuit: Circuit, plan: PartitionPlan, scheme: CommScheme | None) -> list[tuple[int, int]]:
@@ -190,6 +243,13 @@ def protocol_stats(circuit: Circuit, plan: PartitionPlan, scheme: CommScheme | N
     return out
 
 
+def _check_capacity(ds: DistState, scheme: CommScheme) -> None:
+    """engine.py:372-377."""
+    need = scheme.buffer_amps(ds.plan)
+    if need > ds.buffer_amps:
+        raise CapacityError(f"rank buffers hold {ds.buffer_amps} amplitudes, scheme needs {need}")
+
+
 def dist_apply_local(ds: DistState, g: Gate2x2, i: int, strat=None) -> None:
     """engine.py:348-356."""
     if needs_comm(ds.plan, i):
@@ -201,6 +261,7 @@ def _exchange(ds: DistState, g: Gate2x2, i: int, scheme: CommScheme) -> None:
     plan = ds.plan
     if not needs_comm(plan, i):
         raise ContractViolation(f"qubit {i} is rank-local for n={plan.n}, k={plan.k}; use dist_apply_local")
+    _check_capacity(ds, scheme)
     _lib.check(_lib.load().svb_dist_apply_1q(ds.handle, _lib.gate_array(g), int(i)), "exchange")
     _account(ds, scheme, i, None, None)
 
@@ -228,8 +289,10 @@ def dist_apply_controlled(ds: DistState, g: Gate2x2, c: int, t: int,
         raise ValidationError("control and target must differ")
     scheme = scheme if scheme is not None else ds.scheme
     boundary = plan.n - plan.k
-    if t >= boundary and scheme is None:
-        raise ValidationError("communicating target requires a scheme")
+    if t >= boundary:
+        if scheme is None:
+            raise ValidationError("communicating target requires a scheme")
+        _check_capacity(ds, scheme)
     _lib.check(_lib.load().svb_dist_apply_c1q(ds.handle, _lib.gate_array(g), int(c), int(t)),
                "dist_apply_controlled")
     if t >= boundary:
@@ -247,16 +310,19 @@ def dist_norm2(ds: DistState) -> float:
 
 
 def run_circuit(circuit: Circuit, plan: PartitionPlan, scheme: CommScheme | None = None,
-                strat=None, perm=None, norm_tol: float | None = None, devices=None,
-                initial=None) -> tuple[DistState, list[GateStats]]:
-    """engine.py:457-512 on the device.  Gate-by-gate with a device sync per
-    gate so GateStats.wall_time means what it does in the reference; use
-    device.run_ops / simulate for fused full-speed execution."""
+                strat=None, transport: PeerTransport | None = None, execution: str = "cooperative",
+                perm=None, kernel_backend: str | None = None, norm_tol: float | None = None, *,
+                devices=None, initial=None) -> tuple[DistState, list[GateStats]]:
+    """engine.py:457-512 on the device, same positional order (circuit, plan,
+    scheme, strat, transport, execution, perm, kernel_backend, norm_tol).
+    Gate-by-gate with a device sync per gate so GateStats.wall_time means
+    what it does in the reference; use device.run_ops / simulate for fused
+    full-speed execution."""
     if circuit.n != plan.n:
         raise ValidationError(f"circuit has {circuit.n} qubits, plan has {plan.n}")
     if perm is not None and perm.n != plan.n:
         raise ValidationError(f"layout is over {perm.n} qubits, plan has {plan.n}")
-    ds = dist_init(plan, scheme, devices=devices, initial=initial)
+    ds = dist_init(plan, transport, scheme, execution, strat, kernel_backend, devices=devices, initial=initial)
     l2p = perm.logical_to_phys if perm is not None else tuple(range(plan.n))
     boundary = plan.n - plan.k
     stats: list[GateStats] = []

@@ -102,3 +102,56 @@ def test_dist_engine_matches_oracle(world, n, chunk, elide, layout):
     assert exchanges > 0
     if not elide:
         assert elided == 0
+
+
+def _worker_peer_fallback(rank, world, port, n, queue):
+    # peer transport requested, but one rank cannot export its slab (e.g. a
+    # VMM-backed allocation): every rank must fall back to send/recv together
+    # (no rank left waiting in a collective), and the run must still be exact
+    sys.path.insert(0, HERE)
+    sys.path.insert(0, os.path.dirname(HERE))
+    sys.path.insert(0, os.path.join(os.path.dirname(HERE), "oracle"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from cpu_compute import CpuCompute
+        from paper_1801_01037_b200 import workloads as w
+        from paper_1801_01037_b200.dist import DistEngine
+
+        class NoExport(CpuCompute):
+            def ipc_handle(self, slab):
+                if rank == world - 1:
+                    raise RuntimeError("cudaIpcGetMemHandle: invalid argument")
+                return b"handle"
+
+            def ipc_open(self, h):  # never reached: the failure is seen first
+                raise AssertionError("ipc_open after a failed export")
+
+        k = world.bit_length() - 1
+        a0 = w.seeded_state(n, 6)
+        circ = _circuit(n, k, seed=77)
+        eng = DistEngine(n, compute=NoExport(), initial=a0, chunk=16, peer=True)
+        assert not eng.peer
+        eng.run(circ)
+        full = eng.gather()
+        if rank == 0:
+            import oracle
+
+            want = oracle.run_ops(a0.copy(), w.oracle_ops(circ))
+            queue.put(bool(np.array_equal(full, want)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_dist_engine_peer_export_failure_falls_back_together(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_peer_fallback, args=(r, world, port, 9, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    assert q.get(timeout=5)

@@ -148,12 +148,18 @@ def test_fused_fma_within_tolerance(cuda_ok, n):
         assert np.max(np.abs(st.to_host().amps - want)) <= TOL
 
 
-def test_bench_path_deep_circuit_vs_oracle(cuda_ok):
+@pytest.mark.parametrize("geom", [None, ("12", "5")])
+def test_bench_path_deep_circuit_vs_oracle(cuda_ok, geom, monkeypatch):
     # the bench's default path (fused + FMA + JIT: in-register perms, unit
     # folding, scalar extraction with the global factor applied at the end)
     # on the full configs[1] depth -- 200 layers, 7800 ops -- at n = 20, where
     # the oracle finishes in seconds; also the same circuit in two halves
-    # (each run_ops applies its own factor)
+    # (each run_ops applies its own factor).  geom (12, 5): the bench's own
+    # geometry at n = 26 (12-qubit tiles, 5 slot bits; n = 20 alone would get
+    # 11-qubit tiles); test_gpu_large.py runs n = 26 itself
+    if geom is not None:
+        monkeypatch.setenv("SVB_JIT_FM", geom[0])
+        monkeypatch.setenv("SVB_JIT_FS", geom[1])
     n = 20
     circ = w.random_layer_circuit(n, 200)
     rng = np.random.default_rng(77)
@@ -427,13 +433,13 @@ def test_engine_partitioned_equals_single_rank(cuda_ok, k):
 
 def test_engine_known_answers(cuda_ok):
     # test_engine.py:87-95: X on the top qubit at n=3, k=2 swaps the halves
-    ds = engine.dist_init(PartitionPlan(3, 2), SCHEME_B,
+    ds = engine.dist_init(PartitionPlan(3, 2), scheme=SCHEME_B,
                           initial=np.arange(8, dtype=np.complex128))
     engine.dist_apply_scheme_b(ds, standard_gate("x"), 2)
     assert np.array_equal(engine.gather(ds).amps, np.array([4, 5, 6, 7, 0, 1, 2, 3], np.complex128))
     ds.close()
     # test_engine.py:98-109 scheme a pairing
-    ds = engine.dist_init(PartitionPlan(4, 2), SCHEME_A, initial=np.arange(16, dtype=np.complex128))
+    ds = engine.dist_init(PartitionPlan(4, 2), scheme=SCHEME_A, initial=np.arange(16, dtype=np.complex128))
     engine.dist_apply_scheme_a(ds, standard_gate("x"), 3)
     want = np.array([8, 9, 10, 11, 12, 13, 14, 15, 0, 1, 2, 3, 4, 5, 6, 7], np.complex128)
     assert np.array_equal(engine.gather(ds).amps, want)
@@ -523,3 +529,79 @@ def test_jit_fast_fuzz_vs_oracle(cuda_ok):
         want = oracle.run_ops(a.copy(), w.oracle_ops(circ), workers=16)
         got = device.simulate(circ, a.copy(), fma=True, jit=True)
         assert np.max(np.abs(got - want)) <= TOL, (trial, n, np.max(np.abs(got - want)))
+
+
+@pytest.mark.parametrize("n", [14, 18, 22])
+def test_jit_cnot_chains_carry_pending_swaps(cuda_ok, n):
+    # CNOT chains a->b->c->... between arithmetic gates: a CNOT from a
+    # thread bit onto a slot becomes a pending swap X_k^p; a following CNOT
+    # controlled by that slot carries it (X_k CNOT_{k->s} X_k = CNOT_{k->s}
+    # X_s), and H / Ry / T on the slots consume or pass through it.  Bench
+    # path (FMA + JIT) against the oracle, several seeds and geometries
+    x = standard_gate("x")
+    for seed in range(6):
+        rng = np.random.default_rng(4000 + 10 * n + seed)
+        ops = []
+        for _ in range(40):
+            chain = rng.permutation(n)[: int(rng.integers(3, 8))]
+            for a, b in zip(chain[:-1], chain[1:]):
+                ops.append(GateOp("controlled", x, int(b), int(a)))
+            for q in rng.choice(n, size=int(rng.integers(1, 5)), replace=False):
+                g = (standard_gate("h"), ry(float(rng.uniform(0, 6.3))), standard_gate("t"),
+                     rx(float(rng.uniform(0, 6.3))), x)[int(rng.integers(5))]
+                ops.append(GateOp("single", g, int(q)))
+        circ = Circuit(n, tuple(ops))
+        a0 = w.random_state_array(rng, n)
+        want = oracle.run_ops(a0.copy(), w.oracle_ops(circ), workers=16)
+        got = device.simulate(circ, a0.copy(), fma=True, jit=True)
+        assert np.max(np.abs(got - want)) <= TOL, (seed, np.max(np.abs(got - want)))
+
+
+def test_engine_undersized_buffer_is_capacity_error(cuda_ok):
+    # test_engine.py:284-288: a scheme-b state has one-amplitude scratch, so a
+    # scheme-a exchange (L/2 amplitudes) is refused before any data moves
+    from paper_1801_01037_b200 import CapacityError
+
+    plan = PartitionPlan(5, 1)
+    ds = engine.dist_init(plan, scheme=SCHEME_B)
+    with pytest.raises(CapacityError):
+        engine.dist_apply_scheme_a(ds, standard_gate("h"), 4)
+    with pytest.raises(CapacityError):
+        engine.dist_apply_controlled(ds, standard_gate("x"), 0, 4, scheme=SCHEME_A)
+    engine.dist_apply_scheme_b(ds, standard_gate("h"), 4)  # fits
+    ds.close()
+    ds = engine.dist_init(plan)  # no scheme: full-slab scratch, every protocol runs
+    engine.dist_apply_scheme_a(ds, standard_gate("h"), 4)
+    ds.close()
+
+
+def test_engine_reference_positional_order(cuda_ok):
+    # dist_init(plan, transport, scheme, execution, strat, kernel_backend) and
+    # run_circuit(circuit, plan, scheme, strat, transport, execution, perm,
+    # kernel_backend, norm_tol) as engine.py:157-164, 457-467
+    from paper_1801_01037_b200 import InMemoryTransport, SEQUENTIAL, ValidationError
+
+    plan = PartitionPlan(6, 1)
+    t = InMemoryTransport(2)
+    ds = engine.dist_init(plan, t, SCHEME_B, "cooperative", SEQUENTIAL, None)
+    assert ds.transport is t and ds.scheme is SCHEME_B
+    engine.dist_apply_scheme_b(ds, standard_gate("x"), 5)
+    assert t.messages_sent == [32, 32] and t.bytes_sent == [512, 512]
+    ds.close()
+    with pytest.raises(ValidationError):
+        engine.dist_init(plan, InMemoryTransport(4))
+    with pytest.raises(ValidationError):
+        engine.dist_init(plan, None, SCHEME_B, "bogus")
+    circ = w.random_layer_circuit(6, 2, seed=5)
+    t2 = InMemoryTransport(2)
+    ds, stats = engine.run_circuit(circ, plan, SCHEME_B, SEQUENTIAL, t2, "cooperative", None, None, 1e-10)
+    assert sum(t2.messages_sent) == 2 * sum(s.messages_sent_per_rank for s in stats)
+    want = oracle.run_ops(_basis0(6), w.oracle_ops(circ))
+    assert np.max(np.abs(engine.gather(ds).amps - want)) <= TOL
+    ds.close()
+
+
+def _basis0(n):
+    e = np.zeros(1 << n, np.complex128)
+    e[0] = 1
+    return e

@@ -81,7 +81,7 @@ def main():
 
     # partitioned engine, 2^k emulated ranks on this GPU, then the inverse
     plan = PartitionPlan(n, k)
-    ds = engine.dist_init(plan, SCHEME_B)
+    ds = engine.dist_init(plan, scheme=SCHEME_B)
     L = plan.local_len
     for s in ds.slabs:
         s.zero_()
