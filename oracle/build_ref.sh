@@ -25,3 +25,6 @@ INC="$($PY -c 'import sysconfig; print(sysconfig.get_paths()["include"])')"
 /usr/bin/gcc -O3 -fopenmp -ffp-contract=off -fPIC -shared -I"$INC" \
     "$OUT/_stride_cy.c" -o "$OUT/_stride_cy$EXT"
 echo "build_ref: built $OUT/_stride_cy$EXT"
+# the reference's pure-Python package + kernel tests, with INTEGRATION.md's
+# cuda-backend registration applied (tests/test_gpu_plug.py runs them)
+"$PY" "$HERE/stage_ref_pkg.py" "${SVSIM_REF:-/root/reference}"

@@ -70,3 +70,51 @@ def test_format_matches_reference_and_round_trips():
         assert rows(back) == rows(c)
     c = w.random_layer_circuit(6, 3, seed=1)
     assert rows(parse_circuit(format_circuit(c))) == rows(c)
+
+
+def test_cli_verify_bad_gate_exit_2(tmp_path):
+    from paper_1801_01037_b200.__main__ import main
+
+    p = tmp_path / "bad.circ"
+    p.write_text("qubits 1\nu 0 1 0 0 0 0 0 0 2\n")  # non-unitary (ref test_cli.py:221-226)
+    assert main(["verify", str(p)]) == 2
+
+
+@pytest.mark.gpu
+def test_cli_verify(cuda_ok, tmp_path, capsys):
+    from paper_1801_01037_b200.__main__ import main
+
+    p = tmp_path / "r.circ"
+    p.write_text(format_circuit(w.random_layer_circuit(8, 6, seed=62)))
+    for extra in (["--ranks", "8", "--scheme", "a"], ["--ranks", "8", "--scheme", "b"],
+                  ["--ranks", "8", "--scheme", "chunked:4"], ["--fused"]):
+        capsys.readouterr()
+        assert main(["verify", str(p)] + extra) == 0, extra
+        out = capsys.readouterr().out
+        assert out.startswith("max deviation = ")
+        assert float(out.split("=")[1]) <= 1e-10
+    i = tmp_path / "i.circ"
+    i.write_text("qubits 1\ni 0\n")
+    capsys.readouterr()
+    assert main(["verify", str(i)]) == 0
+    assert float(capsys.readouterr().out.split("=")[1]) == 0.0
+
+
+@pytest.mark.gpu
+def test_cli_bench_format(cuda_ok, capsys):
+    from paper_1801_01037_b200.__main__ import main
+
+    assert main(["bench", "--qubits", "4", "--ranks", "1", "--repeat", "2"]) == 0
+    out = capsys.readouterr().out
+    assert "c = no communication" in out and "T = n/a" in out
+    rows = [ln.split(",") for ln in out[out.index("gate_index,"):].strip().splitlines()[1:]]
+    assert len(rows) == 8
+    assert all(r[3] == "false" and r[4] == "0" and r[5] == "0" for r in rows)
+    assert main(["bench", "--qubits", "12", "--ranks", "4", "--scheme", "b", "--repeat", "3"]) == 0
+    out = capsys.readouterr().out
+    assert "c = 5.00" in out
+    t = [ln for ln in out.splitlines() if ln.startswith("T = ")][0]
+    assert float(t.split("=")[1]) > 0.0
+    rows = [ln.split(",") for ln in out[out.index("gate_index,"):].strip().splitlines()[1:]]
+    comm = [r for r in rows if r[3] == "true"]
+    assert len(comm) == 2 * 3 and all(int(r[5]) == 16 * (1 << 10) for r in comm)  # 16*L bytes (scheme b)
