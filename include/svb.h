@@ -55,6 +55,12 @@ typedef struct svb_op {
 #define SVB_RUN_JIT 8u          /* compile each fused pass to straight-line code (NVRTC,
                                    cached per op list): 12-qubit tiles, X/CNOT as register
                                    renames; falls back to the interpreter without NVRTC */
+#define SVB_RUN_JIT_ASYNC 16u   /* with SVB_RUN_JIT: a plan whose passes are not compiled
+                                   yet runs on the interpreter while NVRTC compiles them on
+                                   a background thread; later calls switch over.  Compiled
+                                   cubins are also kept on disk (SVB_JIT_CACHE, default
+                                   $XDG_CACHE_HOME/svb-jit or ~/.cache/svb-jit; "0" = off),
+                                   keyed by source, options and NVRTC version */
 
 int svb_abi_version(void);
 const char *svb_last_error(void);
@@ -99,6 +105,11 @@ int svb_plan_passes(int n_qubits, const svb_op *ops, int nops, unsigned flags, i
  * compiled; SVB_ESTATE (message in svb_last_error) when NVRTC is missing or a
  * pass fails to compile. */
 int svb_jit_check(int n_qubits, const svb_op *ops, int nops, unsigned flags, int *compiled);
+/* Runtime-specialised pass counters since load: cubins read from the on-disk
+ * cache, and NVRTC compiles. */
+void svb_jit_counters(long *disk_hits, long *compiles);
+/* Block until the background compiles SVB_RUN_JIT_ASYNC started have finished. */
+void svb_jit_wait(void);
 
 /* sum |a_j|^2 -> *out (host).  Synchronises `stream`.  Replaces norm2
  * (core.py:171-174) / _dist_norm2 for one slab (engine.py:453-454). */
@@ -175,6 +186,23 @@ int svb_peer_swap_half(void *a, void *b, int64_t begin, int64_t end, int bit, in
 int svb_ipc_handle(const void *dev_ptr, unsigned char handle[64], int64_t *offset);
 int svb_ipc_open(const unsigned char handle[64], void **dev_ptr);
 int svb_ipc_close(void *dev_ptr);
+/* Stream-ordered pairwise rank synchronisation for the peer transport (no
+ * host barrier): svb_stream_signal stores `value` into a (peer) device word
+ * with system-scope release after every earlier kernel of `stream`;
+ * svb_stream_wait makes `stream` wait until the local word is >= value
+ * (cuStreamWaitValue32, no SM occupied).  Each rank of a pair signals its
+ * partner's word and waits on its own, before and after the pair kernel.
+ * Replaces the per-gate synchronize + process-group barrier around
+ * engine.py:359-389's exchange. */
+int svb_stream_signal(void *flag, uint32_t value, void *stream);
+int svb_stream_wait(void *flag, uint32_t value, void *stream);
+/* SM-driven copy dst[i] = src[i] (n_amps x 16 B; either side may be peer
+ * memory): the link-ceiling probe of the multi-GPU bench. */
+int svb_peer_copy(void *dst, const void *src, int64_t n_amps, void *stream);
+/* cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault): the copy-engine leg
+ * of the same probe (cudaMemcpyPeerAsync when the two sides sit on
+ * different GPUs). */
+int svb_copy_async(void *dst, const void *src, int64_t bytes, void *stream);
 
 /* ---- host buffers, synchronous (the svsim kernel-backend contract) ------ */
 

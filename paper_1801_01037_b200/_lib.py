@@ -29,11 +29,15 @@ RUN_FUSE = 1
 RUN_STRICT_ORDER = 2
 RUN_FMA = 4
 RUN_JIT = 8
+RUN_JIT_ASYNC = 16
 
 
-def run_flags(fuse: bool = True, strict_order: bool = False, fma: bool = False, jit: bool = False) -> int:
+def run_flags(fuse: bool = True, strict_order: bool = False, fma: bool = False, jit=False) -> int:
+    """jit: False, True (compile on first use, synchronously) or "async"
+    (interpreter until the background compile finishes)."""
     return ((RUN_FUSE if fuse else 0) | (RUN_STRICT_ORDER if strict_order else 0)
-            | (RUN_FMA if fma else 0) | (RUN_JIT if jit else 0))
+            | (RUN_FMA if fma else 0) | (RUN_JIT if jit else 0)
+            | (RUN_JIT_ASYNC if jit == "async" else 0))
 
 _dp = ctypes.POINTER(ctypes.c_double)
 _i64 = ctypes.c_int64
@@ -59,6 +63,12 @@ _SIGS = {
     "svb_plan_passes": ([_int, ctypes.POINTER(SvbOp), _int, ctypes.c_uint, ctypes.POINTER(_int),
                          ctypes.POINTER(_int)], _int),
     "svb_jit_check": ([_int, ctypes.POINTER(SvbOp), _int, ctypes.c_uint, ctypes.POINTER(_int)], _int),
+    "svb_jit_counters": ([ctypes.POINTER(ctypes.c_long), ctypes.POINTER(ctypes.c_long)], None),
+    "svb_jit_wait": ([], None),
+    "svb_stream_signal": ([_vp, ctypes.c_uint32, _vp], _int),
+    "svb_stream_wait": ([_vp, ctypes.c_uint32, _vp], _int),
+    "svb_peer_copy": ([_vp, _vp, _i64, _vp], _int),
+    "svb_copy_async": ([_vp, _vp, _i64, _vp], _int),
     "svb_norm2": ([_vp, _i64, _dp, _vp], _int),
     "svb_probs": ([_vp, _i64, _vp, _vp], _int),
     "svb_dense_embed": ([_vp, _int, _dp, _int, _int, _vp], _int),
@@ -203,3 +213,15 @@ def profile_read() -> dict:
 
 def launch_count() -> int:
     return int(load(require_cuda=False).svb_launch_count())
+
+
+def jit_counters() -> tuple[int, int]:
+    """(cubins read from the on-disk JIT cache, NVRTC compiles) since load."""
+    hits, comps = ctypes.c_long(), ctypes.c_long()
+    load(require_cuda=False).svb_jit_counters(ctypes.byref(hits), ctypes.byref(comps))
+    return hits.value, comps.value
+
+
+def jit_wait() -> None:
+    """Wait for background pass compiles (run_flags(jit="async"))."""
+    load(require_cuda=False).svb_jit_wait()

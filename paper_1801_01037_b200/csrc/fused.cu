@@ -37,12 +37,15 @@
 
 #include <algorithm>
 #include <array>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <atomic>
+#include <functional>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -712,11 +715,13 @@ static std::vector<PlanPass> plan_beam(int n, const svb_op *ops, int nops, int f
         static const int wa = getenv("SVB_BEAM_W") ? atoi(getenv("SVB_BEAM_W")) : 2;
         static const int depth = getenv("SVB_BEAM_D") ? atoi(getenv("SVB_BEAM_D")) : 3;
         std::vector<uint64_t> cands = candidates(d0, first, p0, ncand);
-        uint64_t best_m = 0;
-        long best_score = -1;
-        for (uint64_t m : cands) {
+        // candidates are scored independently (each on its own copy of
+        // `done`), on up to 16 host threads; the first best in candidate
+        // order wins, so the plan does not depend on the thread count
+        std::vector<long> scores(cands.size(), -1);
+        auto score_one = [&](size_t c) {
             std::vector<char> d1 = done;
-            PlanPass a = greedy(d1, first, m);
+            PlanPass a = greedy(d1, first, cands[c]);
             long score = wa * (long)a.ops.size();
             int f1 = first;
             for (int k = 1; k < depth; ++k) {
@@ -724,11 +729,29 @@ static std::vector<PlanPass> plan_beam(int n, const svb_op *ops, int nops, int f
                 if (f1 >= nops) break;
                 score += (long)greedy(d1, f1, 0).ops.size();
             }
-            if (score > best_score) {
-                best_score = score;
-                best_m = m;
-            }
+            scores[c] = score;
+        };
+        const unsigned nthr = std::min<unsigned>((unsigned)cands.size(),
+                                                 std::min(16u, std::max(1u, std::thread::hardware_concurrency())));
+        if (nthr > 1 && nops - first > 256) {
+            std::atomic<size_t> next{0};
+            std::vector<std::thread> pool;
+            for (unsigned t = 1; t < nthr; ++t)
+                pool.emplace_back([&] {
+                    for (size_t c; (c = next++) < cands.size();) score_one(c);
+                });
+            for (size_t c; (c = next++) < cands.size();) score_one(c);
+            for (auto &t : pool) t.join();
+        } else {
+            for (size_t c = 0; c < cands.size(); ++c) score_one(c);
         }
+        uint64_t best_m = 0;
+        long best_score = -1;
+        for (size_t c = 0; c < cands.size(); ++c)
+            if (scores[c] > best_score) {
+                best_score = scores[c];
+                best_m = cands[c];
+            }
         PlanPass p = greedy(done, first, best_m);
         if (p.ops.empty()) {  // guard: the first pending op always fits
             p.ops.push_back(first);
@@ -746,9 +769,10 @@ static std::vector<PlanPass> plan_beam(int n, const svb_op *ops, int nops, int f
     return passes;
 }
 
-static std::vector<PlanPass> plan(int n, const svb_op *ops, int nops, bool strict, int fm, bool outside) {
-    if (!strict && planner_kind() == 3) return plan_beam(n, ops, nops, fm, outside);
-    if (!strict && planner_kind() == 2) return plan_lookahead(n, ops, nops, fm);
+static std::vector<PlanPass> plan(int n, const svb_op *ops, int nops, bool strict, int fm, bool outside,
+                                  int kind) {
+    if (!strict && kind == 3) return plan_beam(n, ops, nops, fm, outside);
+    if (!strict && kind == 2) return plan_lookahead(n, ops, nops, fm);
     std::vector<PlanPass> passes;
     const uint64_t low = (uint64_t(1) << flow_bits()) - 1;
     const uint64_t all = n >= 64 ? ~uint64_t(0) : ((uint64_t(1) << n) - 1);
@@ -1559,11 +1583,16 @@ static int phase_ways(const uint32_t *t) {
 // when they can, and gate-free layout passes at the end restore the
 // identity layout the caller expects.
 static void lower_plan(int n, const svb_op *ops, int nops, bool strict, bool regperm, int fm, int fs,
-                       bool outside, std::vector<PlanStep> &steps, std::vector<FPass> &passes) {
-    outside = outside && !strict && planner_kind() == 3;
-    const std::vector<PlanPass> plans = plan(n, ops, nops, strict, fm, outside);
+                       bool outside, std::vector<PlanStep> &steps, std::vector<FPass> &passes,
+                       int kind = planner_kind()) {
+    outside = outside && !strict && kind == 3;
+    const auto t_plan0 = std::chrono::steady_clock::now();
+    const std::vector<PlanPass> plans = plan(n, ops, nops, strict, fm, outside, kind);
+    if (getenv("SVB_PLAN_DEBUG"))
+        fprintf(stderr, "plan: op grouping %.3f s\n",
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - t_plan0).count());
     const int nlow = flow_bits();
-    const bool rotate = !strict && rotate_low() && planner_kind() == 3;
+    const bool rotate = !strict && rotate_low() && kind == 3;
     std::vector<int8_t> phys(64), nxt(64);
     for (int q = 0; q < 64; ++q) phys[q] = (int8_t)q;
     auto single = [&](int oi) {
@@ -1614,13 +1643,16 @@ static void lower_plan(int n, const svb_op *ops, int nops, bool strict, bool reg
                     for (int c = b + 1; c < np && choices.size() < 24; ++c)
                         if (nlow == 3) choices.push_back({pool[a], pool[b], pool[c]});
             if (choices.empty()) choices.push_back(std::vector<int>(pool.begin(), pool.begin() + std::min(np, nlow)));
-            bool built = false;
-            FPass best;
-            std::vector<int8_t> best_next;
-            int best_score = 1 << 20;
-            for (size_t ci = 0; ci < choices.size(); ++ci) {
+            // every choice is lowered (build_pass: register groups, swizzle
+            // search) independently on up to 16 host threads; the lowest
+            // score wins, the first in choice order on ties
+            const size_t nc = choices.size();
+            std::vector<FPass> cand(nc);
+            std::vector<std::vector<int8_t>> cand_next(nc);
+            std::vector<int> cand_score(nc, 1 << 20);
+            auto lower_one = [&](size_t ci) {
             const std::vector<int> &lowq = choices[ci];
-            nxt = phys;
+            std::vector<int8_t> nx = phys;
             uint64_t T = 0;  // the tile's physical bits
             for (int q = 0; q < n; ++q)
                 if ((pp.S >> q) & 1) T |= uint64_t(1) << phys[q];
@@ -1632,13 +1664,13 @@ static void lower_plan(int n, const svb_op *ops, int nops, bool strict, bool reg
                 if (phys[q] >= nlow) {
                     int b = 0;
                     while ((taken >> b) & 1) ++b;
-                    nxt[q] = (int8_t)b;
+                    nx[q] = (int8_t)b;
                     taken |= uint64_t(1) << b;
                 }
             for (int q = 0; q < n; ++q) {
                 if (!((pp.S >> q) & 1) || std::find(lowq.begin(), lowq.end(), q) != lowq.end()) continue;
                 if (q >= nlow && ((T >> q) & 1) && !((taken >> q) & 1)) {
-                    nxt[q] = (int8_t)q;  // home
+                    nx[q] = (int8_t)q;  // home
                     taken |= uint64_t(1) << q;
                 } else {
                     rest.push_back(q);
@@ -1647,11 +1679,11 @@ static void lower_plan(int n, const svb_op *ops, int nops, bool strict, bool reg
             for (int q : rest) {
                 int b = 0;
                 while (!((T >> b) & 1) || ((taken >> b) & 1)) ++b;
-                nxt[q] = (int8_t)b;
+                nx[q] = (int8_t)b;
                 taken |= uint64_t(1) << b;
             }
-            FPass P;
-            if (!build_pass(n, ops, pp, P, strict, regperm, fm, phys.data(), nxt.data(), fs)) continue;
+            FPass &P = cand[ci];
+            if (!build_pass(n, ops, pp, P, strict, regperm, fm, phys.data(), nx.data(), fs)) return;
             // score: uncoalesced last-group HBM store (2) + shared-memory
             // conflicts of the last group's loads and the groups' stores
             const FGroup &GL = P.groups[P.ngroups - 1];
@@ -1662,12 +1694,35 @@ static void lower_plan(int n, const svb_op *ops, int nops, bool strict, bool reg
             int score = 4 * P.ngroups + (coal ? 0 : 2);
             score += phase_ways(GL.ld_t) - 1;
             for (int gi = 0; gi + 1 < P.ngroups; ++gi) score += phase_ways(P.groups[gi].st_t) - 1;
-            if (score < best_score) {
-                best_score = score;
-                best = P;
-                best_next = nxt;
-                built = true;
+            cand_score[ci] = score;
+            cand_next[ci] = std::move(nx);
+            };
+            const unsigned nthr = std::min<unsigned>((unsigned)nc,
+                                                     std::min(16u, std::max(1u, std::thread::hardware_concurrency())));
+            if (nthr > 1) {
+                std::atomic<size_t> nextc{0};
+                std::vector<std::thread> pool;
+                for (unsigned t = 1; t < nthr; ++t)
+                    pool.emplace_back([&] {
+                        for (size_t c; (c = nextc++) < nc;) lower_one(c);
+                    });
+                for (size_t c; (c = nextc++) < nc;) lower_one(c);
+                for (auto &t : pool) t.join();
+            } else {
+                for (size_t c = 0; c < nc; ++c) lower_one(c);
             }
+            bool built = false;
+            size_t bi = 0;
+            for (size_t ci = 0; ci < nc; ++ci)
+                if (cand_score[ci] < (built ? cand_score[bi] : (1 << 20))) {
+                    bi = ci;
+                    built = true;
+                }
+            FPass best;
+            std::vector<int8_t> best_next;
+            if (built) {
+                best = cand[bi];
+                best_next = cand_next[bi];
             }
             if (built) {
                 PlanStep st;
@@ -1806,7 +1861,7 @@ int plan_passes(int n, const svb_op *ops, int nops, unsigned flags, int *groups)
 // sweeps) is planned and lowered to kernel descriptors once.
 
 struct CompiledPlan {
-    int n, fm, fs;
+    int n, fm, fs, kind;
     bool strict, regperm, outside;
     std::vector<svb_op> ops;  // exact key
     std::vector<PlanStep> steps;
@@ -1838,6 +1893,7 @@ struct CompiledPlan {
 
 bool jit_build(const std::vector<FPass> &passes, int variant, std::vector<void *> &fns,
                std::vector<std::shared_ptr<void>> &keep);
+void jit_async(std::function<void()> fn);
 bool jit_launch(void *fn, const FPass &P, double2 *a, int64_t ntiles, cudaStream_t s);
 
 static uint64_t fnv1a(const void *p, size_t len, uint64_t h) {
@@ -1854,7 +1910,8 @@ static size_t plan_cache_bytes() {
 }
 
 static std::shared_ptr<const CompiledPlan> compiled_plan(int n, const svb_op *ops, int nops, bool strict,
-                                                         bool regperm, int fm, int fs, bool outside) {
+                                                         bool regperm, int fm, int fs, bool outside,
+                                                         int kind = planner_kind(), bool peek = false) {
     static std::mutex mu;
     static std::vector<std::pair<uint64_t, std::shared_ptr<const CompiledPlan>>> cache;  // MRU first
     uint64_t key = fnv1a(ops, sizeof(svb_op) * size_t(nops), 1469598103934665603ull);
@@ -1864,12 +1921,13 @@ static std::shared_ptr<const CompiledPlan> compiled_plan(int n, const svb_op *op
     key = fnv1a(&fm, sizeof fm, key);
     key = fnv1a(&fs, sizeof fs, key);
     key = fnv1a(&outside, sizeof outside, key);
+    key = fnv1a(&kind, sizeof kind, key);
     {
         std::lock_guard<std::mutex> lk(mu);
         for (size_t i = 0; i < cache.size(); ++i) {
             const auto &c = cache[i].second;
-            if (cache[i].first == key && c->n == n && c->fm == fm && c->fs == fs && c->outside == outside && c->strict == strict && c->regperm == regperm &&
-                (int)c->ops.size() == nops &&
+            if (cache[i].first == key && c->n == n && c->fm == fm && c->fs == fs && c->outside == outside &&
+                c->strict == strict && c->regperm == regperm && c->kind == kind && (int)c->ops.size() == nops &&
                 std::memcmp(c->ops.data(), ops, sizeof(svb_op) * size_t(nops)) == 0) {
                 auto hit = cache[i];
                 cache.erase(cache.begin() + i);
@@ -1878,15 +1936,17 @@ static std::shared_ptr<const CompiledPlan> compiled_plan(int n, const svb_op *op
             }
         }
     }
+    if (peek) return nullptr;
     auto cp = std::make_shared<CompiledPlan>();
     cp->n = n;
     cp->fm = fm;
     cp->fs = fs;
+    cp->kind = kind;
     cp->strict = strict;
     cp->regperm = regperm;
     cp->outside = outside;
     cp->ops.assign(ops, ops + nops);
-    lower_plan(n, ops, nops, strict, regperm, fm, fs, outside, cp->steps, cp->passes);
+    lower_plan(n, ops, nops, strict, regperm, fm, fs, outside, cp->steps, cp->passes, kind);
     // Bounded by descriptor bytes (~27 KiB per pass), not by count: the
     // multi-process engine runs one op segment per exchange interval, so a
     // circuit step may cycle through hundreds of small plans.
@@ -1899,6 +1959,41 @@ static std::shared_ptr<const CompiledPlan> compiled_plan(int n, const svb_op *op
     }
     cache.resize(std::max<size_t>(keep, 1));
     return cp;
+}
+
+// SVB_RUN_JIT_ASYNC: plan + compile the specialised passes of an op list on
+// a background thread (once per op list: in-flight keys are remembered).
+// The plan lands in the plan cache with its kernels already built, so a later
+// call finds it through compiled_plan(..., peek) with jit_state 1.
+static bool start_async_jit(int n, const svb_op *ops, int nops, bool strict, bool regperm, int fm, int fs,
+                            bool outside, int variant) {
+    static std::mutex mu;
+    static std::vector<uint64_t> inflight;
+    uint64_t key = fnv1a(ops, sizeof(svb_op) * size_t(nops), 0x2545f4914f6cdd1dull);
+    key = fnv1a(&n, sizeof n, key);
+    key = fnv1a(&variant, sizeof variant, key);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (std::find(inflight.begin(), inflight.end(), key) != inflight.end()) return false;
+        inflight.push_back(key);
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::vector<svb_op> copy(ops, ops + nops);
+    jit_async([copy = std::move(copy), n, strict, regperm, fm, fs, outside, variant, dev, key] {
+        cudaSetDevice(dev);
+        std::shared_ptr<const CompiledPlan> cp =
+            compiled_plan(n, copy.data(), (int)copy.size(), strict, regperm, fm, fs, outside);
+        {
+            std::lock_guard<std::mutex> lk2(cp->jit_mu);
+            if (cp->jit_state[variant] == 0)
+                cp->jit_state[variant] =
+                    jit_build(cp->passes, variant, cp->jit_fns[variant], cp->jit_keep[variant]) ? 1 : -1;
+        }
+        std::lock_guard<std::mutex> lk(mu);
+        inflight.erase(std::find(inflight.begin(), inflight.end(), key));
+    });
+    return true;
 }
 
 int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsigned flags,
@@ -1928,14 +2023,37 @@ int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsi
     }
     const bool strict = flags & SVB_RUN_STRICT_ORDER;
     const bool fma = (flags & SVB_RUN_FMA) && !strict;
-    std::shared_ptr<const CompiledPlan> cp =
-        compiled_plan(n, ops, nops, strict, reg_perm(flags), plan_fm(n, flags), plan_fs(flags), plan_outside(flags));
+    const int variant = jit_variant(fma);
+    std::shared_ptr<const CompiledPlan> cp;
+    if ((flags & SVB_RUN_JIT) && (flags & SVB_RUN_JIT_ASYNC) && jit_available()) {
+        // use the specialised plan only once its kernels are built; until
+        // then a quickly planned interpreter run (lookahead planner: ~0.07 s
+        // for configs[1] instead of ~1 s) while a background thread plans and
+        // compiles the specialised one
+        cp = compiled_plan(n, ops, nops, strict, reg_perm(flags), plan_fm(n, flags), plan_fs(flags),
+                           plan_outside(flags), planner_kind(), true);
+        int state = 0;
+        if (cp) {
+            std::lock_guard<std::mutex> lk(cp->jit_mu);
+            state = cp->jit_state[variant];
+        }
+        if (state != 1) {
+            if (state == 0)
+                start_async_jit(n, ops, nops, strict, reg_perm(flags), plan_fm(n, flags), plan_fs(flags),
+                                plan_outside(flags), variant);
+            cp = compiled_plan(n, ops, nops, strict, reg_perm(flags & ~SVB_RUN_JIT), FM, FSLOTS, false,
+                               strict ? planner_kind() : 2);
+            flags &= ~(SVB_RUN_JIT | SVB_RUN_JIT_ASYNC);
+        }
+    }
+    if (!cp)
+        cp = compiled_plan(n, ops, nops, strict, reg_perm(flags), plan_fm(n, flags), plan_fs(flags),
+                           plan_outside(flags));
     size_t next_pass = 0;
     bool jit = (flags & SVB_RUN_JIT) && !cp->passes.empty();
     const std::vector<void *> *jit_fns = nullptr;
     if (jit) {
         std::lock_guard<std::mutex> lk(cp->jit_mu);
-        const int variant = jit_variant(fma);
         int &state = cp->jit_state[variant];
         if (state == 0)
             state = jit_build(cp->passes, variant, cp->jit_fns[variant], cp->jit_keep[variant]) ? 1 : -1;

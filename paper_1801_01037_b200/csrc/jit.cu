@@ -21,6 +21,8 @@
 // generated code on the host against the oracle (tests/test_jit_emu.py).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cmath>
@@ -28,6 +30,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -1334,11 +1337,13 @@ struct Nvrtc {
     typedef int (*size_t_)(void *, size_t *);
     typedef int (*get_t)(void *, char *);
     typedef int (*destroy_t)(void **);
+    typedef int (*version_t)(int *, int *);
     create_t create = nullptr;
     compile_t compile = nullptr;
     size_t_ log_size = nullptr, cubin_size = nullptr;
     get_t log = nullptr, cubin = nullptr;
     destroy_t destroy = nullptr;
+    int major = 0, minor = 0;
     bool ok = false;
 };
 
@@ -1357,6 +1362,7 @@ static const Nvrtc &nvrtc() {
         r.cubin_size = (Nvrtc::size_t_)dlsym(h, "nvrtcGetCUBINSize");
         r.cubin = (Nvrtc::get_t)dlsym(h, "nvrtcGetCUBIN");
         r.destroy = (Nvrtc::destroy_t)dlsym(h, "nvrtcDestroyProgram");
+        if (auto v = (Nvrtc::version_t)dlsym(h, "nvrtcVersion")) v(&r.major, &r.minor);
         r.ok = r.create && r.compile && r.log_size && r.log && r.cubin_size && r.cubin && r.destroy;
         return r;
     }();
@@ -1365,7 +1371,16 @@ static const Nvrtc &nvrtc() {
 
 bool jit_available() { return nvrtc().ok; }
 
-static bool nvrtc_compile(const std::string &src, std::vector<char> &cubin, std::string &log) {
+static const std::vector<const char *> &nvrtc_opts() {
+    static const std::vector<const char *> opts = [] {
+        std::vector<const char *> o = {"-arch=sm_100a", "-std=c++17", "-default-device", "-fmad=false"};
+        if (getenv("SVB_JIT_LINEINFO")) o.push_back("-lineinfo");  // for ncu source pages
+        return o;
+    }();
+    return opts;
+}
+
+static bool nvrtc_compile_now(const std::string &src, std::vector<char> &cubin, std::string &log) {
     const Nvrtc &nv = nvrtc();
     if (!nv.ok) {
         log = "NVRTC not available";
@@ -1376,9 +1391,7 @@ static bool nvrtc_compile(const std::string &src, std::vector<char> &cubin, std:
         log = "nvrtcCreateProgram failed";
         return false;
     }
-    std::vector<const char *> opts = {"-arch=sm_100a", "-std=c++17", "-default-device", "-fmad=false"};
-    if (getenv("SVB_JIT_LINEINFO")) opts.push_back("-lineinfo");  // for ncu source pages
-    if (const char *x = getenv("SVB_JIT_OPT")) opts.push_back(x);   // one extra option (measurement)
+    const std::vector<const char *> &opts = nvrtc_opts();
     if (nv.compile(prog, (int)opts.size(), opts.data()) != 0) {
         size_t n = 0;
         nv.log_size(prog, &n);
@@ -1392,6 +1405,169 @@ static bool nvrtc_compile(const std::string &src, std::vector<char> &cubin, std:
     cubin.resize(n);
     nv.cubin(prog, cubin.data());
     nv.destroy(&prog);
+    return true;
+}
+
+// On-disk cubin cache: a circuit compiled once is not recompiled by the next
+// process.  Directory: SVB_JIT_CACHE ("0" or "" disables), else
+// $XDG_CACHE_HOME/svb-jit, else $HOME/.cache/svb-jit.  Entry name = two
+// independent 64-bit hashes of (source, options, NVRTC version); the file
+// carries a magic and the source length and hash, re-checked on read, and is
+// written to a temporary name and renamed (concurrent writers are harmless).
+static const std::string &jit_cache_dir() {
+    static const std::string dir = [] {
+        std::string d;
+        if (const char *e = getenv("SVB_JIT_CACHE")) {
+            d = e;
+            if (d == "0") d.clear();
+        } else if (const char *x = getenv("XDG_CACHE_HOME")) {
+            if (*x) d = std::string(x) + "/svb-jit";
+        } else if (const char *h = getenv("HOME")) {
+            if (*h) d = std::string(h) + "/.cache/svb-jit";
+        }
+        if (!d.empty()) {  // mkdir -p
+            for (size_t i = 1; i <= d.size(); ++i)
+                if (i == d.size() || d[i] == '/') mkdir(d.substr(0, i).c_str(), 0755);
+            struct stat st;
+            if (stat(d.c_str(), &st) != 0 || !S_ISDIR(st.st_mode)) d.clear();
+        }
+        return d;
+    }();
+    return dir;
+}
+
+static uint64_t fnv64(const void *p, size_t n, uint64_t h) {
+    const unsigned char *b = static_cast<const unsigned char *>(p);
+    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+    return h;
+}
+
+struct CubinKey {
+    uint64_t a, b;
+};
+
+static CubinKey cubin_key(const std::string &src) {
+    std::string k = src;
+    for (const char *o : nvrtc_opts()) (k += '\0') += o;
+    k += "\0nvrtc " + std::to_string(nvrtc().major) + "." + std::to_string(nvrtc().minor);
+    // second hash: different offset basis and the bytes fed in reverse
+    std::string r(k.rbegin(), k.rend());
+    return {fnv64(k.data(), k.size(), 1469598103934665603ull), fnv64(r.data(), r.size(), 0x9e3779b97f4a7c15ull)};
+}
+
+static const uint64_t kCubinMagic = 0x31304a4954425653ull;  // "SVBTIJ01"
+
+static std::string cubin_path(const CubinKey &key) {
+    char name[48];
+    snprintf(name, sizeof name, "/%016llx%016llx.cubin", (unsigned long long)key.a, (unsigned long long)key.b);
+    return jit_cache_dir() + name;
+}
+
+static bool cubin_load(const std::string &src, const CubinKey &key, std::vector<char> &cubin) {
+    FILE *f = fopen(cubin_path(key).c_str(), "rb");
+    if (!f) return false;
+    uint64_t hdr[3] = {0, 0, 0};
+    bool ok = fread(hdr, sizeof hdr, 1, f) == 1 && hdr[0] == kCubinMagic && hdr[1] == src.size() &&
+              hdr[2] == fnv64(src.data(), src.size(), 14695981039346656037ull ^ 0x5a5a);
+    if (ok) {
+        fseek(f, 0, SEEK_END);
+        long end = ftell(f);
+        ok = end > long(sizeof hdr);
+        if (ok) {
+            cubin.resize(size_t(end) - sizeof hdr);
+            fseek(f, long(sizeof hdr), SEEK_SET);
+            ok = fread(cubin.data(), 1, cubin.size(), f) == cubin.size();
+        }
+    }
+    fclose(f);
+    return ok;
+}
+
+static void cubin_store(const std::string &src, const CubinKey &key, const std::vector<char> &cubin) {
+    const std::string path = cubin_path(key);
+    char tmp_sfx[64];
+    snprintf(tmp_sfx, sizeof tmp_sfx, ".tmp.%d.%zx", (int)getpid(),
+             std::hash<std::thread::id>()(std::this_thread::get_id()));
+    const std::string tmp = path + tmp_sfx;
+    FILE *f = fopen(tmp.c_str(), "wb");
+    if (!f) return;
+    const uint64_t hdr[3] = {kCubinMagic, src.size(), fnv64(src.data(), src.size(), 14695981039346656037ull ^ 0x5a5a)};
+    bool ok = fwrite(hdr, sizeof hdr, 1, f) == 1 && fwrite(cubin.data(), 1, cubin.size(), f) == cubin.size();
+    ok = (fclose(f) == 0) && ok;
+    if (!ok || rename(tmp.c_str(), path.c_str()) != 0) unlink(tmp.c_str());
+}
+
+static std::atomic<long> g_disk_hits{0}, g_compiles{0};
+
+// Background compiles (SVB_RUN_JIT_ASYNC).  Outstanding threads are joined
+// before this file's statics (the module cache they fill) are destroyed:
+// the joiner is defined after them, so it is destroyed first.
+struct AsyncJoiner {
+    struct Job {
+        std::thread t;
+        std::shared_ptr<std::atomic<bool>> done;
+    };
+    std::mutex mu;
+    std::vector<Job> jobs;
+    ~AsyncJoiner() {
+        std::vector<Job> j;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            j.swap(jobs);
+        }
+        for (auto &x : j)
+            if (x.t.joinable()) x.t.join();
+    }
+};
+static AsyncJoiner g_async;
+
+void jit_async(std::function<void()> fn) {
+    std::lock_guard<std::mutex> lk(g_async.mu);
+    for (auto it = g_async.jobs.begin(); it != g_async.jobs.end();) {  // reap finished compiles
+        if (it->done->load()) {
+            it->t.join();
+            it = g_async.jobs.erase(it);
+        } else {
+            ++it;
+        }
+    }
+    auto done = std::make_shared<std::atomic<bool>>(false);
+    g_async.jobs.push_back({std::thread([fn = std::move(fn), done] {
+                                fn();
+                                done->store(true);
+                            }),
+                            done});
+}
+
+// Block until every background compile started so far has finished.
+extern "C" void svb_jit_wait(void) {
+    std::vector<AsyncJoiner::Job> j;
+    {
+        std::lock_guard<std::mutex> lk(g_async.mu);
+        j.swap(g_async.jobs);
+    }
+    for (auto &x : j)
+        if (x.t.joinable()) x.t.join();
+}
+
+extern "C" void svb_jit_counters(long *disk_hits, long *compiles) {
+    if (disk_hits) *disk_hits = g_disk_hits.load();
+    if (compiles) *compiles = g_compiles.load();
+}
+
+static bool nvrtc_compile(const std::string &src, std::vector<char> &cubin, std::string &log) {
+    const bool disk = !jit_cache_dir().empty();
+    CubinKey key{0, 0};
+    if (disk) {
+        key = cubin_key(src);
+        if (cubin_load(src, key, cubin)) {
+            ++g_disk_hits;
+            return true;
+        }
+    }
+    if (!nvrtc_compile_now(src, cubin, log)) return false;
+    ++g_compiles;
+    if (disk) cubin_store(src, key, cubin);
     return true;
 }
 
