@@ -20,6 +20,8 @@ namespace svb {
 
 LaunchInfo launch_gate(double2 *a, int64_t n_amps, const Gate &g, int t, int c, cudaStream_t s);
 LaunchInfo launch_dense_embed(double2 *u, int64_t dim, const Gate &g, int t, int c, cudaStream_t s);
+LaunchInfo launch_signal(unsigned *flag, unsigned value, cudaStream_t s);
+LaunchInfo launch_peer_copy(double2 *dst, const double2 *src, int64_t count, cudaStream_t s);
 LaunchInfo launch_peer_swap_half(double2 *a, double2 *b, int64_t begin, int64_t end, int bit, int va, int vb,
                                  cudaStream_t s);
 LaunchInfo launch_dense_matvec(const double2 *u, const double2 *x, double2 *y, int64_t dim, int64_t row0,
@@ -460,6 +462,69 @@ int svb_peer_swap_half(void *a, void *b, int64_t begin, int64_t end, int bit, in
     return SVB_OK;
 }
 
+int svb_stream_signal(void *flag, uint32_t value, void *stream) {
+    if (!flag || (uintptr_t(flag) & 3)) {
+        set_error("svb_stream_signal: flag must be a 4-byte aligned device address");
+        return SVB_EINVAL;
+    }
+    prof_begin((cudaStream_t)stream);
+    LaunchInfo li = launch_signal((unsigned *)flag, value, (cudaStream_t)stream);
+    prof_end((cudaStream_t)stream, li);
+    g_launches += li.kernels;
+    SVB_CHECK_LAUNCH("svb_stream_signal");
+    return SVB_OK;
+}
+
+int svb_stream_wait(void *flag, uint32_t value, void *stream) {
+    if (!flag || (uintptr_t(flag) & 3)) {
+        set_error("svb_stream_wait: flag must be a 4-byte aligned device address");
+        return SVB_EINVAL;
+    }
+    // cuStreamWaitValue32(stream, addr, value, CU_STREAM_WAIT_VALUE_GEQ)
+    typedef int (*wait_t)(void *, unsigned long long, unsigned, unsigned);
+    static wait_t wait = [] {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return (wait_t)fn;
+    }();
+    if (!wait) {
+        set_error("svb_stream_wait: cuStreamWaitValue32 unavailable");
+        return SVB_ECUDA;
+    }
+    const int r = wait(stream, (unsigned long long)(uintptr_t)flag, value, 0u /* GEQ */);
+    if (r != 0) {
+        set_error("svb_stream_wait: cuStreamWaitValue32 failed (CUresult %d)", r);
+        return SVB_ECUDA;
+    }
+    return SVB_OK;
+}
+
+int svb_copy_async(void *dst, const void *src, int64_t bytes, void *stream) {
+    if (!dst || !src || bytes < 0) {
+        set_error("bad arguments to svb_copy_async");
+        return SVB_EINVAL;
+    }
+    cudaError_t e = cudaMemcpyAsync(dst, src, size_t(bytes), cudaMemcpyDefault, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_status(e, "svb_copy_async");
+    return SVB_OK;
+}
+
+int svb_peer_copy(void *dst, const void *src, int64_t n_amps, void *stream) {
+    if (!dst || !src || n_amps < 0) {
+        set_error("bad arguments to svb_peer_copy");
+        return SVB_EINVAL;
+    }
+    prof_begin((cudaStream_t)stream);
+    LaunchInfo li = launch_peer_copy((double2 *)dst, (const double2 *)src, n_amps, (cudaStream_t)stream);
+    prof_end((cudaStream_t)stream, li);
+    g_launches += li.kernels;
+    SVB_CHECK_LAUNCH("svb_peer_copy");
+    return SVB_OK;
+}
+
 int svb_ipc_handle(const void *dev_ptr, unsigned char handle[64], int64_t *offset) {
     if (!dev_ptr || !handle || !offset) {
         set_error("svb_ipc_handle: NULL argument");
@@ -731,7 +796,7 @@ int svb_profile_read(int cls, int64_t *launches, double *total_ms, int64_t *alg_
 
 const char *svb_profile_class_name(int cls) {
     static const char *names[PROF_NCLASSES] = {"k_pair_high", "k_pair_low", "k_diag", "k_tiny", "k_fused",
-                                               "k_exchange", "k_norm", "kpass_jit", "k_dense"};
+                                               "k_exchange", "k_norm", "kpass_jit", "k_dense", "k_signal"};
     return (cls >= 0 && cls < PROF_NCLASSES) ? names[cls] : "";
 }
 

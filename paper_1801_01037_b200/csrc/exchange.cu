@@ -70,6 +70,9 @@ __global__ void __launch_bounds__(kXThreads) k_pair_update(double2 *lo_slab, dou
         lo_slab[j] = lo[k];
         hi_slab[j] = hi[k];
     }
+    // peer stores are visible system-wide before the stream's next signal
+    // (k_signal) can be observed by the partner
+    __threadfence_system();
 }
 
 // Control-masked exchange (regime ii, engine.py:444-447): only local indices
@@ -211,6 +214,50 @@ __global__ void __launch_bounds__(kXThreads) k_peer_swap_half(double2 *a, double
         a[ia] = y;
         b[ib] = x;
     }
+    __threadfence_system();
+}
+
+// Stream-ordered pairwise rank synchronisation of the peer transport (no
+// host round trip): k_signal runs after every earlier kernel of its stream
+// (whose peer stores each ended in a system fence) and publishes `value`
+// into the partner's flag word with release semantics; the partner's stream
+// waits on its own word with cuStreamWaitValue32 (>= value), a front-end
+// wait that occupies no SM.
+__global__ void k_signal(unsigned *flag, unsigned value) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(value) : "memory");
+}
+
+LaunchInfo launch_signal(unsigned *flag, unsigned value, cudaStream_t s) {
+    k_signal<<<1, 1, 0, s>>>(flag, value);
+    return LaunchInfo{1, PROF_SYNC, 0};
+}
+
+// SM-driven peer copy (link-ceiling probe): dst[i] = src[i], 16 B per
+// element, four loads in flight per thread, grid-stride over 148 x 8 CTAs.
+__global__ void __launch_bounds__(kXThreads) k_peer_copy(double2 *__restrict__ dst, const double2 *__restrict__ src,
+                                                         int64_t count) {
+    const int64_t stride = int64_t(gridDim.x) * kXThreads * kXUpt;
+    for (int64_t base = int64_t(blockIdx.x) * kXThreads * kXUpt + threadIdx.x; base < count; base += stride) {
+        double2 v[kXUpt];
+#pragma unroll
+        for (int k = 0; k < kXUpt; ++k) {
+            const int64_t j = base + int64_t(k) * kXThreads;
+            if (j < count) v[k] = src[j];
+        }
+#pragma unroll
+        for (int k = 0; k < kXUpt; ++k) {
+            const int64_t j = base + int64_t(k) * kXThreads;
+            if (j < count) dst[j] = v[k];
+        }
+    }
+}
+
+LaunchInfo launch_peer_copy(double2 *dst, const double2 *src, int64_t count, cudaStream_t s) {
+    if (count <= 0) return LaunchInfo{0, PROF_EXCHANGE, 0};
+    const int64_t blocks = std::min<int64_t>((count + kXThreads * kXUpt - 1) / (kXThreads * kXUpt), 148 * 8);
+    k_peer_copy<<<(unsigned)blocks, kXThreads, 0, s>>>(dst, src, count);
+    return LaunchInfo{1, PROF_EXCHANGE, count * 32};
 }
 
 LaunchInfo launch_peer_swap_half(double2 *a, double2 *b, int64_t begin, int64_t end, int bit, int va, int vb,

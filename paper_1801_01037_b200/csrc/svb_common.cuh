@@ -170,7 +170,8 @@ enum ProfClass : int {
     PROF_NORM = 6,       // norm / probs
     PROF_FUSED_JIT = 7,  // kpass: NVRTC-specialised fused pass (jit.cu)
     PROF_DENSE = 8,      // k_dense_embed / k_dense_matvec (dense verifier)
-    PROF_NCLASSES = 9
+    PROF_SYNC = 9,       // k_signal: pairwise rank sync of the peer transport
+    PROF_NCLASSES = 10
 };
 struct LaunchInfo {
     int kernels;

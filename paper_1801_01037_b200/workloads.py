@@ -106,3 +106,31 @@ def sweep_ops(n: int, reps: int = 10, seed: int = SEED_CFG3) -> Circuit:
 def oracle_ops(circuit: Circuit):
     """(gate, target, control|None) triples, the form oracle/ consumes."""
     return [(op.gate, op.target, op.control) for op in circuit.ops]
+
+
+def inverse_circuit(circuit: Circuit) -> Circuit:
+    """U^dagger of a circuit: ops reversed, every gate conjugate-transposed
+    (round-trip checks at sizes no CPU oracle holds)."""
+    ops = []
+    for op in reversed(circuit.ops):
+        g = op.gate
+        gi = Gate2x2(complex(g.q11).conjugate(), complex(g.q21).conjugate(),
+                     complex(g.q12).conjugate(), complex(g.q22).conjugate())
+        ops.append(GateOp(op.kind, gi, op.target, op.control))
+    return Circuit(circuit.n, tuple(ops))
+
+
+def bit_reverse(x: int, n: int) -> int:
+    return int(format(x, f"0{n}b")[::-1], 2)
+
+
+def qft_basis_amplitude(x: int, y: int, n: int) -> complex:
+    """<y| qft_circuit(n) |x> = exp(2 pi i br(x) br(y) / 2^n) / 2^(n/2) (SURVEY
+    8(c) known answer for the LSB-convention QFT with final reversal swaps);
+    the phase is reduced exactly in integers, so it holds at n = 33/34 where
+    br(x) br(y) overflows int64.  A closed form used as a size-independent
+    check in bench.py's multi-GPU line (the tests check it against the
+    oracle's own copy)."""
+    N = 1 << n
+    ph = (bit_reverse(x, n) * bit_reverse(y, n)) % N
+    return complex(np.exp(2j * np.pi * ph / N) / np.sqrt(N))

@@ -40,20 +40,26 @@ for _ in range(160):
 circ = Circuit(n, tuple(ops))
 a = w.random_state_array(np.random.default_rng(8), n)
 want = oracle.run_ops(a.copy(), w.oracle_ops(circ)) if rank == 0 else None
+want2 = oracle.run_ops(want.copy(), w.oracle_ops(circ)) if rank == 0 else None  # the circuit twice
 bad = 0
-for layout in (False, True):
-    for fma in (False, True):
-        eng = DistEngine(n, initial=a, peer=True, layout=layout, fma=fma, jit=fma)
-        eng.run(circ)
-        out = eng.gather()
-        st = eng.stats
-        eng.close()
-        if rank == 0:
-            err = float(np.max(np.abs(out - want)))
-            ok = err <= 1e-12 and (st.exchanges + st.swaps) > 0
-            print(f"world {world} layout {layout} fma {fma}: max err {err:.2e}, exchanges {st.exchanges}, "
-                  f"swaps {st.swaps} {'ok' if ok else 'FAIL'}", flush=True)
-            bad += not ok
+# device-side pairwise sync (default) for every layout x arithmetic mode, and
+# the host-barrier fallback for two of them
+cases = [(layout, fma, True) for layout in (False, True) for fma in (False, True)]
+cases += [(False, False, False), (True, True, False)]
+for layout, fma, gpu_sync in cases:
+    eng = DistEngine(n, initial=a, peer=True, layout=layout, fma=fma, jit=fma, gpu_sync=gpu_sync)
+    assert eng.peer and eng.gpu_sync == gpu_sync, "peer transport / device sync unavailable"
+    eng.run(circ)
+    eng.run(circ)  # twice: the flag counts keep matching across runs
+    out = eng.gather()
+    st = eng.stats
+    eng.close()
+    if rank == 0:
+        err = float(np.max(np.abs(out - want2)))
+        ok = err <= 1e-12 and (st.exchanges + st.swaps) > 0
+        print(f"world {world} layout {layout} fma {fma} gpu_sync {gpu_sync}: max err {err:.2e}, "
+              f"exchanges {st.exchanges}, swaps {st.swaps} {'ok' if ok else 'FAIL'}", flush=True)
+        bad += not ok
 dist.barrier()
 dist.destroy_process_group()
 sys.exit(1 if bad else 0)

@@ -1,6 +1,7 @@
 """Peer-memory transport of the multi-process engine (DistEngine(peer=True)):
 2 and 4 processes on one GPU (CUDA IPC), gloo control plane, against the
-oracle -- see tests/peer_ranks.py."""
+oracle -- see tests/peer_ranks.py.  Covers the device-side pairwise sync
+(svb_stream_signal / svb_stream_wait) and the host-barrier fallback."""
 import os
 import subprocess
 import sys
@@ -19,4 +20,4 @@ def test_peer_transport_ranks_vs_oracle(cuda_ok, world):
                         os.path.join(REPO, "tests", "peer_ranks.py")],
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])
-    assert r.stdout.count(" ok") == 4, r.stdout
+    assert r.stdout.count(" ok") == 6, r.stdout
