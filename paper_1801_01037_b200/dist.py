@@ -948,6 +948,7 @@ def bench_main(args, clock_cls=None, peaks_fn=None) -> None:
 
     # reference-faithful mode: one exchange per global-target gate
     ref_eng = None
+    eng.close()  # partners unmap this slab before it is freed
     del eng
     torch.cuda.empty_cache()
     faithful = None
@@ -981,7 +982,10 @@ def bench_main(args, clock_cls=None, peaks_fn=None) -> None:
         del e4
         torch.cuda.empty_cache()
 
-    transport = _transport_check(dev, world) if world > 1 else None
+    transport = None
+    if world > 1:
+        transport = (_transport_check(dev, world) if backend == "nccl" else
+                     {"skipped": "send/recv of CUDA tensors needs NCCL (this run's control plane is gloo)"})
 
     if rank == 0:
         ms = main["ms"]
