@@ -373,6 +373,53 @@ def cold_start(circuit, layers: int) -> dict:
     return out
 
 
+def seam_rates(circuit) -> dict:
+    """Gate applications/s through the reference-facing seams on HOST arrays:
+    * backend.apply_single / apply_controlled -- svsim's kernel-backend
+      contract (kernel/__init__.py:107-134), one gate per synchronous call,
+      the whole state through PCIe each call (streamed in 64 MiB units);
+      configs[1]'s circuit at n=20 and its first two layers at n=26;
+    * engine.run_circuit(..., fused="fast") at k=0 -- the reference engine's
+      entry point (engine.py:457-512) with the local ops fused, GateStats per
+      gate, gather() to the host included: configs[1] whole."""
+    from paper_1801_01037_b200 import backend, engine, workloads
+    from paper_1801_01037_b200.partition import PartitionPlan
+
+    out = {}
+    for n, layers, nops in ((20, 10, None), (26, 200, 78)):
+        circ = workloads.random_layer_circuit(n, layers) if n != circuit.n else circuit
+        ops = circ.ops[:nops] if nops else circ.ops
+        a = np.zeros(1 << n, np.complex128)
+        a[0] = 1.0
+
+        def apply(op):
+            g = op.gate
+            if op.control is None:
+                backend.apply_single(a, g.q11, g.q12, g.q21, g.q22, op.target, 3, 1)
+            else:
+                backend.apply_controlled(a, g.q11, g.q12, g.q21, g.q22, op.control, op.target, 3, 1)
+
+        apply(ops[0])  # warm: staging buffers, page-locking of `a`
+        t0 = time.perf_counter()
+        for op in ops:
+            apply(op)
+        dt = time.perf_counter() - t0
+        out[f"backend_n{n}"] = {"value": round(len(ops) / dt, 1), "unit": UNIT, "ops": len(ops),
+                                "bytes_per_call": 2 * (16 << n)}
+    t0 = time.perf_counter()
+    ds, stats = engine.run_circuit(circuit, PartitionPlan(circuit.n, 0), fused="fast")
+    t1 = time.perf_counter()
+    amps = engine.gather(ds).amps
+    dt = time.perf_counter() - t0
+    ds.close()
+    out["engine_fused_n%d" % circuit.n] = {"value": round(len(circuit.ops) / dt, 1), "unit": UNIT,
+                                           "run_circuit_s": round(t1 - t0, 3), "gather_s": round(dt - (t1 - t0), 3),
+                                           "gate_stats": len(stats), "norm": float(np.vdot(amps, amps).real),
+                                           "api": "engine.run_circuit(..., fused='fast') + gather() to a new "
+                                                  "host array, plan and kernels already cached"}
+    return out
+
+
 def run_gpu_arm(args) -> None:
     import tempfile
 
@@ -474,6 +521,7 @@ def run_gpu_arm(args) -> None:
         device.simulate(circuit, a_in, out=outs[k], **kw)
     serial_dt = time.perf_counter() - t0
 
+    seam = None if args.no_seam else seam_rates(circuit)
     sweep = None if args.no_sweep else local_gate_sweep(SWEEP_N, SWEEP_REPS, peak)
     qft = None if args.no_sweep else qft20_rate(args)
 
@@ -501,6 +549,7 @@ def run_gpu_arm(args) -> None:
                 "steps": e2e_steps,
                 "serial": {"value": round(nops * serial_steps / serial_dt, 1), "steps": serial_steps,
                            "api": "device.simulate (svb_host_run_ops), one synchronous call per step"}},
+        "e2e_seam": seam,
         "cpu_baseline": cpu,
         "local_gate_sweep": sweep,
         "qft20": qft,
@@ -528,6 +577,7 @@ def main(argv=None):
     ap.add_argument("--no-sweep", action="store_true", help="skip the configs[2] n=30 sweep")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-cold", action="store_true", help="skip the cold-start measurement")
+    ap.add_argument("--no-seam", action="store_true", help="skip the host-seam measurements")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU reference work")
     ap.add_argument("--seq-budget", type=float, default=8.0,
                     help="--impl reference: seconds of the paper's sequential mode (bounded sample)")

@@ -203,6 +203,11 @@ int svb_peer_copy(void *dst, const void *src, int64_t n_amps, void *stream);
  * of the same probe (cudaMemcpyPeerAsync when the two sides sit on
  * different GPUs). */
 int svb_copy_async(void *dst, const void *src, int64_t bytes, void *stream);
+/* Page-lock a caller-owned host array (cudaHostRegister; already registered
+ * is not an error) / release it.  backend.py registers large svsim arrays
+ * once and releases them when the array is garbage-collected. */
+int svb_host_register(void *host, int64_t bytes);
+int svb_host_unregister(void *host);
 
 /* ---- host buffers, synchronous (the svsim kernel-backend contract) ------ */
 
@@ -210,6 +215,10 @@ int svb_copy_async(void *dst, const void *src, int64_t bytes, void *stream);
  * mode, workers) (_stride_py.py:93-98; _stride_cy.pyx:24-25): in place on a
  * host complex128 array; mode/workers are accepted and ignored. */
 int svb_host_apply_1q(double *host_amps, int64_t n_amps, const double q[8], int target);
+/* (From 2^22 amplitudes the state streams through the device in 64 MiB
+ * units on three streams -- H2D, kernel and D2H of different units overlap
+ * -- and units a high control bit switches off are not copied.  Pin the
+ * caller's array once with svb_host_register for full-duplex PCIe.) */
 int svb_host_apply_c1q(double *host_amps, int64_t n_amps, const double q[8], int control,
                        int target);
 /* Whole op list on host memory: H2D of host_in, svb_run_ops, D2H into

@@ -69,6 +69,8 @@ _SIGS = {
     "svb_stream_wait": ([_vp, ctypes.c_uint32, _vp], _int),
     "svb_peer_copy": ([_vp, _vp, _i64, _vp], _int),
     "svb_copy_async": ([_vp, _vp, _i64, _vp], _int),
+    "svb_host_register": ([_vp, _i64], _int),
+    "svb_host_unregister": ([_vp], _int),
     "svb_norm2": ([_vp, _i64, _dp, _vp], _int),
     "svb_probs": ([_vp, _i64, _vp, _vp], _int),
     "svb_dense_embed": ([_vp, _int, _dp, _int, _int, _vp], _int),

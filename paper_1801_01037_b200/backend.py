@@ -10,8 +10,9 @@ _stride_cy.pyx:24-25, 57-58):
 ``amps`` is the caller-owned host complex128 array, updated in place; the
 call is synchronous; mode/workers may be ignored (all reference modes are
 bit-identical).  This module satisfies that contract with libsvb.so:
-svb_host_apply_1q / svb_host_apply_c1q copy the array to HBM, run one
-kernel and copy it back.  Registering it in svsim is a two-line change shown
+svb_host_apply_1q / svb_host_apply_c1q stream the array through HBM (64 MiB
+units on three streams: copies in, kernel and copies out of different units
+overlap; large arrays are page-locked once for full-duplex PCIe).  Registering it in svsim is a two-line change shown
 in INTEGRATION.md.  Validation happens in the caller's wrapper, as in the
 reference; the C layer re-checks and raises ValidationError on bad input.
 """
@@ -19,6 +20,7 @@ reference; the C layer re-checks and raises ValidationError on bad input.
 from __future__ import annotations
 
 import ctypes
+import weakref
 
 import numpy as np
 
@@ -36,9 +38,35 @@ def _q(q11, q12, q21, q22):
     return (ctypes.c_double * 8)(*vals)
 
 
+# Large caller arrays are page-locked once (svb_host_register) so the
+# streamed seam moves them at full-duplex PCIe speed; the registration is
+# released when the array object is garbage-collected.
+_PIN_MIN_BYTES = 4 << 20
+_pinned: dict[tuple[int, int], weakref.finalize] = {}
+
+
+def _unpin(key):
+    _pinned.pop(key, None)
+    try:
+        _lib.load().svb_host_unregister(ctypes.c_void_p(key[0]))
+    except Exception:  # interpreter teardown
+        pass
+
+
+def _pin(amps: np.ndarray) -> None:
+    if amps.nbytes < _PIN_MIN_BYTES:
+        return
+    key = (amps.ctypes.data, amps.nbytes)
+    if key in _pinned:
+        return
+    if _lib.load().svb_host_register(ctypes.c_void_p(key[0]), key[1]) == 0:
+        _pinned[key] = weakref.finalize(amps, _unpin, key)
+
+
 def _ptr(amps: np.ndarray) -> ctypes.c_void_p:
     if not isinstance(amps, np.ndarray) or amps.dtype != np.complex128 or not amps.flags.c_contiguous:
         raise ValidationError("backend operates on contiguous complex128 arrays")
+    _pin(amps)
     return ctypes.c_void_p(amps.ctypes.data)
 
 

@@ -191,6 +191,88 @@ struct Staging {
 };
 static Staging g_stage;
 
+// The single-gate host seam (svsim's backend contract: one gate per call on
+// a caller-owned host array) streamed through the device in units instead
+// of one whole-state H2D, kernel, D2H: a unit is one block of 2^s
+// amplitudes (target t < s) or the two blocks b, b ^ 2^(t-s) a pair spans
+// (t >= s; in the staging slot the partner sits at distance 2^s, so the
+// kernel runs with target s).  Three slots on three streams: the H2D of one
+// unit overlaps the kernel and the D2H of the others (PCIe both ways at
+// once when the host array is pinned or registered, svb_host_register).  A
+// control bit c >= s is constant over a unit: units whose control bit is 0
+// are not copied at all.  Same kernels, same arithmetic: bit-identical.
+struct SeamPipe {
+    int device = -1;
+    double2 *buf = nullptr;  // 3 slots x 2^(s+1) amplitudes
+    int64_t slot_amps = 0;
+    cudaStream_t st[3] = {nullptr, nullptr, nullptr};
+};
+static SeamPipe g_seam;
+constexpr int kSeamBits = 22;  // 64 MiB blocks
+
+static int seam_apply(double *host, int64_t n_amps, const double q[8], int c, int t) {
+    int n = 0;
+    while ((int64_t(1) << n) < n_amps) ++n;
+    const int s = std::min(kSeamBits, n - 3);
+    int d;
+    cudaError_t e = cudaGetDevice(&d);
+    if (e != cudaSuccess) return cuda_status(e, "cudaGetDevice");
+    const int64_t S = int64_t(1) << s;
+    if (g_seam.buf && (g_seam.device != d || g_seam.slot_amps < 2 * S)) {
+        int cur = d;
+        cudaSetDevice(g_seam.device);
+        cudaFree(g_seam.buf);
+        for (auto &x : g_seam.st) cudaStreamDestroy(x);
+        cudaSetDevice(cur);
+        g_seam = SeamPipe();
+    }
+    if (!g_seam.buf) {
+        e = cudaMalloc((void **)&g_seam.buf, size_t(3) * 2 * S * sizeof(double2));
+        if (e != cudaSuccess) {
+            g_seam.buf = nullptr;
+            return cuda_status(e, "seam staging cudaMalloc");
+        }
+        for (auto &x : g_seam.st) cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
+        g_seam.slot_amps = 2 * S;
+        g_seam.device = d;
+    }
+    double2 *h = reinterpret_cast<double2 *>(host);
+    const Gate g = make_gate(q);
+    const bool pair = t >= s;
+    const int64_t nblocks = n_amps >> s;
+    int64_t u = 0;
+    for (int64_t b = 0; b < nblocks; ++b) {
+        if (pair && ((b >> (t - s)) & 1)) continue;  // the upper block of a pair
+        if (c >= s && !((b >> (c - s)) & 1)) continue;  // control clear over the whole unit
+        const int k = int(u++ % 3);
+        cudaStream_t st = g_seam.st[k];
+        double2 *slot = g_seam.buf + k * 2 * S;
+        const int64_t b2 = pair ? (b | (int64_t(1) << (t - s))) : -1;
+        e = cudaMemcpyAsync(slot, h + b * S, S * sizeof(double2), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess && pair)
+            e = cudaMemcpyAsync(slot + S, h + b2 * S, S * sizeof(double2), cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) return cuda_status(e, "seam H2D");
+        prof_begin(st);
+        LaunchInfo li = launch_gate(slot, pair ? 2 * S : S, g, pair ? s : t, c >= 0 && c < s ? c : -1, st);
+        prof_end(st, li);
+        g_launches += li.kernels;
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_status(e, "seam kernel");
+        e = cudaMemcpyAsync(h + b * S, slot, S * sizeof(double2), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess && pair)
+            e = cudaMemcpyAsync(h + b2 * S, slot + S, S * sizeof(double2), cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) return cuda_status(e, "seam D2H");
+    }
+    for (auto &x : g_seam.st) {
+        e = cudaStreamSynchronize(x);
+        if (e != cudaSuccess) return cuda_status(e, "seam sync");
+    }
+    return SVB_OK;
+}
+
+// below this size the whole state goes in one copy each way
+constexpr int64_t kSeamMinAmps = int64_t(1) << 22;
+
 }  // namespace svb
 
 using namespace svb;
@@ -502,6 +584,29 @@ int svb_stream_wait(void *flag, uint32_t value, void *stream) {
     return SVB_OK;
 }
 
+int svb_host_register(void *host, int64_t bytes) {
+    if (!host || bytes <= 0) {
+        set_error("bad arguments to svb_host_register");
+        return SVB_EINVAL;
+    }
+    cudaError_t e = cudaHostRegister(host, size_t(bytes), cudaHostRegisterDefault);
+    if (e == cudaErrorHostMemoryAlreadyRegistered) {
+        cudaGetLastError();
+        return SVB_OK;
+    }
+    if (e != cudaSuccess) return cuda_status(e, "cudaHostRegister");
+    return SVB_OK;
+}
+
+int svb_host_unregister(void *host) {
+    cudaError_t e = cudaHostUnregister(host);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return cuda_status(e, "cudaHostUnregister");
+    }
+    return SVB_OK;
+}
+
 int svb_copy_async(void *dst, const void *src, int64_t bytes, void *stream) {
     if (!dst || !src || bytes < 0) {
         set_error("bad arguments to svb_copy_async");
@@ -615,6 +720,7 @@ int svb_host_apply_1q(double *host_amps, int64_t n_amps, const double q[8], int 
     if (r == SVB_OK) r = check_target(target, n_amps);
     if (r != SVB_OK) return r;
     std::lock_guard<std::mutex> lk(g_stage.mu);
+    if (n_amps >= kSeamMinAmps) return seam_apply(host_amps, n_amps, q, -1, target);
     void *dev;
     if ((r = host_stage(host_amps, n_amps, &dev)) != SVB_OK) return r;
     if ((r = svb_apply_1q(dev, n_amps, q, target, nullptr)) != SVB_OK) return r;
@@ -628,6 +734,7 @@ int svb_host_apply_c1q(double *host_amps, int64_t n_amps, const double q[8], int
     if (r == SVB_OK) r = check_control(control, target, n_amps);
     if (r != SVB_OK) return r;
     std::lock_guard<std::mutex> lk(g_stage.mu);
+    if (n_amps >= kSeamMinAmps) return seam_apply(host_amps, n_amps, q, control, target);
     void *dev;
     if ((r = host_stage(host_amps, n_amps, &dev)) != SVB_OK) return r;
     if ((r = svb_apply_c1q(dev, n_amps, q, control, target, nullptr)) != SVB_OK) return r;

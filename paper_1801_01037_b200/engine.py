@@ -309,21 +309,111 @@ def dist_norm2(ds: DistState) -> float:
     return out.value
 
 
+def _run_fused(ds: DistState, circuit: Circuit, l2p, norm_tol: float | None, fast: bool) -> list[GateStats]:
+    """run_circuit(fused=...): the local ops between two global-target gates
+    run as ONE svb_run_ops per rank (multi-gate HBM passes; each rank gets
+    its own list -- a rank-bit control keeps or drops the op per rank,
+    regime iii); global-target gates go through the pair kernels as in the
+    op-by-op path.  GateStats keep the reference's exact messages / bytes per
+    gate; a batch's measured wall time is split evenly over its ops (per-gate
+    times inside a fused pass do not exist), exchanges are timed one by one.
+    fast=False: strict order, reference arithmetic -- bit-identical to the
+    op-by-op path; fast=True: FMA + runtime-specialised passes (<= 1e-12)."""
+    import torch
+
+    from .core import GateOp
+
+    lib = _lib.load()
+    plan = ds.plan
+    boundary = plan.n - plan.k
+    flags = _lib.run_flags(fuse=True, fma=True, jit=True) if fast else _lib.run_flags(fuse=True, strict_order=True)
+    stats: list[GateStats | None] = [None] * len(circuit.ops)
+    pending: list[list] = [[] for _ in range(plan.p)]
+    batch: list[int] = []  # op positions in the current local batch
+
+    def flush():
+        if not batch:
+            return
+        ds.sync()
+        t0 = time.perf_counter()
+        for r in range(plan.p):
+            if not pending[r]:
+                continue
+            slab = ds.slabs[r]
+            with torch.cuda.device(slab.device):
+                arr, nops = _lib.ops_array(tuple(pending[r]))
+                _lib.check(lib.svb_run_ops(ctypes.c_void_p(slab.data_ptr()), slab.shape[0], arr, nops, flags,
+                                           ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
+                           "run_circuit(fused)")
+        for d in sorted(set(ds.devices)):
+            torch.cuda.synchronize(d)
+        wall = (time.perf_counter() - t0) / len(batch)
+        for pos in batch:
+            op = circuit.ops[pos]
+            stats[pos] = GateStats(op.target, op.control, False, 0, 0, wall)
+        batch.clear()
+        for lst in pending:
+            lst.clear()
+        if norm_tol is not None:
+            drift = abs(dist_norm2(ds) - 1.0)
+            if drift > norm_tol:
+                raise ValidationError(f"norm drifted by {drift:.3e} after gate {pos}")
+
+    for pos, op in enumerate(circuit.ops):
+        tbit = l2p[op.target]
+        cbit = l2p[op.control] if op.control is not None else None
+        if tbit < boundary:
+            for r in range(plan.p):
+                if cbit is None:
+                    pending[r].append(GateOp("single", op.gate, tbit))
+                elif cbit >= boundary:  # regime iii, local target: uncontrolled where the rank bit is set
+                    if (r >> (cbit - boundary)) & 1:
+                        pending[r].append(GateOp("single", op.gate, tbit))
+                else:
+                    pending[r].append(GateOp("controlled", op.gate, tbit, cbit))
+            batch.append(pos)
+            continue
+        flush()
+        if ds.scheme is None:
+            raise ValidationError(f"qubit {tbit} requires communication but no scheme was configured")
+        before_m, before_b = list(ds.messages_sent), list(ds.bytes_sent)
+        t0 = time.perf_counter()
+        if cbit is None:
+            _exchange(ds, op.gate, tbit, ds.scheme)
+        else:
+            dist_apply_controlled(ds, op.gate, cbit, tbit)
+        ds.sync()
+        wall = time.perf_counter() - t0
+        msgs = max(a - b for a, b in zip(ds.messages_sent, before_m))
+        nbytes = max(a - b for a, b in zip(ds.bytes_sent, before_b))
+        stats[pos] = GateStats(op.target, op.control, True, msgs, nbytes, wall)
+        if norm_tol is not None:
+            drift = abs(dist_norm2(ds) - 1.0)
+            if drift > norm_tol:
+                raise ValidationError(f"norm drifted by {drift:.3e} after gate {pos}")
+    flush()
+    return stats  # type: ignore[return-value]
+
+
 def run_circuit(circuit: Circuit, plan: PartitionPlan, scheme: CommScheme | None = None,
                 strat=None, transport: PeerTransport | None = None, execution: str = "cooperative",
                 perm=None, kernel_backend: str | None = None, norm_tol: float | None = None, *,
-                devices=None, initial=None) -> tuple[DistState, list[GateStats]]:
+                devices=None, initial=None, fused=False) -> tuple[DistState, list[GateStats]]:
     """engine.py:457-512 on the device, same positional order (circuit, plan,
     scheme, strat, transport, execution, perm, kernel_backend, norm_tol).
-    Gate-by-gate with a device sync per gate so GateStats.wall_time means
-    what it does in the reference; use device.run_ops / simulate for fused
-    full-speed execution."""
+    Default: gate-by-gate with a device sync per gate so GateStats.wall_time
+    means what it does in the reference.  fused=True (bit-identical) or
+    "fast" (FMA + specialised passes): the local ops between global-target
+    gates run as one fused svb_run_ops per rank, GateStats still per gate
+    (_run_fused)."""
     if circuit.n != plan.n:
         raise ValidationError(f"circuit has {circuit.n} qubits, plan has {plan.n}")
     if perm is not None and perm.n != plan.n:
         raise ValidationError(f"layout is over {perm.n} qubits, plan has {plan.n}")
     ds = dist_init(plan, transport, scheme, execution, strat, kernel_backend, devices=devices, initial=initial)
     l2p = perm.logical_to_phys if perm is not None else tuple(range(plan.n))
+    if fused:
+        return ds, _run_fused(ds, circuit, l2p, norm_tol, fused == "fast")
     boundary = plan.n - plan.k
     stats: list[GateStats] = []
     for pos, op in enumerate(circuit.ops):

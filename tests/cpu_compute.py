@@ -28,6 +28,9 @@ class CpuCompute:
     def zeros(self, count):
         return torch.zeros(count, dtype=torch.complex128)
 
+    def flag_words(self, count):  # peer-transport sync words (never signalled on CPU)
+        return torch.zeros(count, dtype=torch.int32)
+
     def from_numpy(self, arr):
         return torch.from_numpy(np.ascontiguousarray(arr).copy())
 

@@ -416,6 +416,52 @@ def test_engine_vs_reference_golden(cuda_ok):
         pos += nops
 
 
+@pytest.mark.parametrize("fused", [True, "fast"])
+def test_engine_fused_seam_vs_reference_golden(cuda_ok, fused):
+    """run_circuit(fused=...) (local ops between exchanges as one fused
+    svb_run_ops per rank) against the reference's engine goldens: same
+    amplitudes (bit-identical for the strict fused mode where the op-by-op
+    path is), same per-gate messages and bytes."""
+    z = golden("engine.npz")
+    outs = split_cases(z["meta"][:, 0], z["out"])
+    ops = z["ops"]
+    pos = 0
+    for case, ((n, k, scheme_id, nops), want) in enumerate(zip(z["meta"], outs)):
+        rows = ops[ops[:, 0] == case]
+        circ = Circuit(int(n), tuple(
+            GateOp("single" if r[2] < 0 else "controlled", gate_from_q(r[3:]), int(r[1]),
+                   None if r[2] < 0 else int(r[2])) for r in rows))
+        scheme = (SCHEME_A, SCHEME_B, chunked(2))[int(scheme_id)]
+        ds, stats = engine.run_circuit(circ, PartitionPlan(int(n), int(k)), scheme, fused=fused)
+        got = engine.gather(ds).amps
+        ds.close()
+        assert np.max(np.abs(got - want)) <= TOL, case
+        if scheme_id == 1 and fused is True:
+            assert np.array_equal(got, want), case
+        assert len(stats) == nops
+        assert [s.messages_sent_per_rank for s in stats] == list(z["msgs"][pos:pos + nops])
+        assert [s.bytes_sent_per_rank for s in stats] == list(z["bytes"][pos:pos + nops])
+        assert all(s.wall_time >= 0 for s in stats)
+        pos += nops
+
+
+def test_engine_fused_seam_large_matches_op_by_op(cuda_ok):
+    """A configs[1]-style circuit at n=20 over 4 ranks with a global control
+    and target mix: fused (strict) equals op-by-op bit for bit, and the
+    rank-bit-controlled local ops (regime iii) are kept per rank."""
+    n = 20
+    circ = w.random_layer_circuit(n, 6, seed=77)
+    a = w.random_state_array(np.random.default_rng(77), n)
+    ds0, st0 = engine.run_circuit(circ, PartitionPlan(n, 2), SCHEME_B, initial=a)
+    ds1, st1 = engine.run_circuit(circ, PartitionPlan(n, 2), SCHEME_B, initial=a, fused=True)
+    g0, g1 = engine.gather(ds0).amps, engine.gather(ds1).amps
+    ds0.close()
+    ds1.close()
+    assert np.array_equal(g0, g1)
+    assert [(s.comm_required, s.messages_sent_per_rank, s.bytes_sent_per_rank) for s in st0] == \
+        [(s.comm_required, s.messages_sent_per_rank, s.bytes_sent_per_rank) for s in st1]
+
+
 @pytest.mark.parametrize("k", [1, 2, 3])
 def test_engine_partitioned_equals_single_rank(cuda_ok, k):
     n = 16
