@@ -131,6 +131,30 @@ __device__ __forceinline__ void cpa(void *smem, const void *g) {
     asm("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(s) : "l"(smem));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(s), "l"(g) : "memory");
 }
+__device__ __forceinline__ unsigned su32(const void *p) {
+    unsigned s;
+    asm("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(s) : "l"(p));
+    return s;
+}
+// tile ring (mode 3): one mbarrier per buffer counts the fill's cp.async
+// completions (one no-increment arrival per issuing thread)
+__device__ __forceinline__ void mb_init(unsigned long long *m, unsigned count) {
+    asm volatile("mbarrier.init.shared.b64 [%0], %1;" :: "r"(su32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mb_arrive_cp(unsigned long long *m) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" :: "r"(su32(m)) : "memory");
+}
+__device__ __forceinline__ void mb_wait(unsigned long long *m, unsigned parity) {
+    unsigned done;
+    do {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(su32(m)), "r"(parity) : "memory");
+    } while (!done);
+}
+// barrier of one warpgroup (named barrier 1 + wg, its 128 threads)
+__device__ __forceinline__ void wg_sync(int wg, int n) {
+    asm volatile("bar.sync %0, %1;" :: "r"(wg + 1), "r"(n) : "memory");
+}
 __device__ __forceinline__ d2 ldcs(const d2 *p) {
     d2 r;
     asm volatile("ld.global.cs.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
@@ -1009,11 +1033,22 @@ bool pend_on() {
 //      buffer is free, so the next tile's cp.async fill is issued there and
 //      overlaps the last group's arithmetic and direct HBM stores (passes
 //      without a direct last group use mode 0)
+//   3  tile ring (12-qubit tiles with a direct last group; the default
+//      there): one CTA per SM of two warpgroups, each running the pass's
+//      groups on its own tiles (even / odd tile numbers of the CTA), three
+//      64 KiB buffers shared round-robin (tile j in buffer j % 3).  The
+//      warpgroup that has read its last group out of a buffer refills it
+//      at once with tile j + 3 -- the OTHER warpgroup's next-but-one tile
+//      -- so a fill has about half a tile period of lead instead of only the
+//      last group's arithmetic; an mbarrier per buffer (cp.async arrivals)
+//      tells the consumer when its tile has landed.  Transitions sync the
+//      warpgroup only (named barriers).  ncu of mode 2 on configs[1]: 24 % of
+//      the warps' stall samples sat at the tile-start fill wait.
 int jit_mode() {
     static int m = [] {
         const char *e = getenv("SVB_JIT_MODE");
         int v = e ? atoi(e) : -1;
-        return (v >= 0 && v <= 2) ? v : -1;
+        return (v >= 0 && v <= 3) ? v : -1;
     }();
     return m;
 }
@@ -1023,13 +1058,17 @@ int jit_mode() {
 // (measured on configs[1]: fm 13 mode 0 75.2k, mode 2 86.6k gate apps/s)
 int jit_pass_mode(const FPass &P) {
     int m = jit_mode();
-    if (m < 0) m = P.fm > 11 ? 2 : 0;
+    if (m < 0) m = P.fm == 12 ? 3 : (P.fm > 11 ? 2 : 0);
     if (m == 1 && P.fm != 11) m = 0;  // two tiles fit only at fm 11
-    if (m == 2 && !P.direct_last) m = 0;
+    if (m == 3 && (P.fm != 12 || P.fs < 5)) m = 2;  // three 64 KiB tiles per SM, 2 x 128 threads
+    if ((m == 2 || m == 3) && !P.direct_last) m = 0;
     return m;
 }
 
-int jit_threads(const FPass &P) { return (1 << P.fm) >> P.fs; }
+// threads of one tile's worker (a warpgroup in mode 3)
+static int jit_wg_threads(const FPass &P) { return (1 << P.fm) >> P.fs; }
+
+int jit_threads(const FPass &P) { return (jit_pass_mode(P) == 3 ? 2 : 1) * jit_wg_threads(P); }
 
 // resident CTAs per SM the generated kernel is built for (__launch_bounds__):
 // 64K registers / (threads x registers per thread)
@@ -1040,6 +1079,7 @@ int jit_ctas_per_sm(const FPass &P) {
         return (v >= 1 && v <= 8) ? v : 0;
     }();
     if (jit_pass_mode(P) == 1) return 3;
+    if (jit_pass_mode(P) == 3) return 1;
     if (c) return c;
     // 16 amplitudes per thread fit 128 registers, 32 need the full 255
     return std::max(1, 65536 / (jit_threads(P) * (P.fs >= 5 ? 256 : 128)));
@@ -1047,7 +1087,8 @@ int jit_ctas_per_sm(const FPass &P) {
 // tile buffers live in dynamic shared memory when they exceed the 48 KiB
 // static limit (double buffering, or tiles of 12+ qubits)
 size_t jit_dyn_smem(const FPass &P) {
-    const size_t b = (jit_pass_mode(P) == 1 ? 2 : 1) * (size_t(1) << P.fm) * sizeof(double2);
+    const int m = jit_pass_mode(P);
+    const size_t b = (m == 1 ? 2 : m == 3 ? 3 : 1) * (size_t(1) << P.fm) * sizeof(double2);
     return b > 40 * 1024 ? b : 0;
 }
 
@@ -1109,7 +1150,10 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
     const bool fma = variant >= 1, fast = variant == 2;
     const int mode = jit_pass_mode(P);
     Out o;
-    const int FTILE = 1 << P.fm, FTHREADS = jit_threads(P), FTBITS = P.fm - P.fs;
+    const int FTILE = 1 << P.fm, FTHREADS = jit_wg_threads(P), FTBITS = P.fm - P.fs;
+    const bool ring = mode == 3;
+    // CTA-wide barrier, or the warpgroup's own in the ring
+    const std::string SYNC = ring ? "wg_sync(wg, " + std::to_string(FTHREADS) + ");" : "__syncthreads();";
     const int colmask = (1 << P.flow) - 1;
     // Tile-local global offsets are XOR-linear in the thread index and the
     // register number: thread parts are computed per use from the opaque
@@ -1134,12 +1178,18 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
     // tid's remaining bits then k's bits
     auto row_off = [&](int rbit) { return int64_t(1) << P.rowbit[rbit]; };
     o("extern \"C\" __global__ void __launch_bounds__(%d, %d) kpass(d2 *__restrict__ a, i64 ntiles) {\n",
-      FTHREADS, jit_ctas_per_sm(P));
+      jit_threads(P), jit_ctas_per_sm(P));
     if (jit_dyn_smem(P))
         o("extern __shared__ d2 dsm[];\n");
     else
         o("__shared__ alignas(16) d2 dsm[%d];\n", FTILE);
-    o("const int tid = threadIdx.x;\n");
+    if (ring) {
+        o("__shared__ unsigned long long mbar[3];\n");
+        o("const int wg = threadIdx.x >> %d;\n", [&] { int l = 0; while ((1 << l) < FTHREADS) ++l; return l; }());
+        o("const int tid = threadIdx.x & %d;\n", FTHREADS - 1);
+    } else {
+        o("const int tid = threadIdx.x;\n");
+    }
     o("auto tbase = [&](i64 t) { i64 b = 0;\n");
     for (int j = 0; j < P.ncomp; ++j) o("b |= ((t >> %d) & 1) << %d;\n", j, P.comp[j]);
     o("return b; };\n");
@@ -1162,14 +1212,36 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
     thread_parts();
     for (int k = 0; k < NR(); ++k)
         o("cpa(dstb + (s ^ %uu), p + (r ^ %s));\n", k_smem(k), offl(k_row(k)).c_str());
-    o("asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\"); };\n(void)fill;\n");
+    if (ring)
+        o("};\n(void)fill;\n");
+    else
+        o("asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\"); };\n(void)fill;\n");
     const char *wait_all = "asm volatile(\"cp.async.wait_group 0;\\n\" ::: \"memory\");\n";
     const bool direct_first = P.direct_first && mode == 0;
-    if (mode != 0)
-        o("if (blockIdx.x < ntiles) fill(reinterpret_cast<unsigned char *>(dsm), a + tbase(blockIdx.x));\n");
-    o("int it = 0;\nfor (i64 tix = blockIdx.x; tix < ntiles; tix += gridDim.x, ++it) {\n");
-    o("d2 *const pa = a + tbase(tix);\n");
-    if (mode == 1) {
+    if (ring) {
+        // tile j of this CTA = blockIdx.x + j * gridDim.x, buffer j % 3,
+        // worked by warpgroup j & 1; its fill completes mbar[j % 3]'s phase j / 3
+        o("auto fill3 = [&](int bi, i64 j) {\n"
+          "const i64 t = blockIdx.x + j * gridDim.x;\n"
+          "if (t < ntiles) { fill(reinterpret_cast<unsigned char *>(dsm + bi * %d), a + tbase(t)); "
+          "mb_arrive_cp(&mbar[bi]); } };\n", FTILE);
+        o("if (threadIdx.x < 3) mb_init(&mbar[threadIdx.x], %d);\n__syncthreads();\n", FTHREADS);
+        o("if (wg == 0) { fill3(0, 0); fill3(2, 2); } else { fill3(1, 1); }\n");
+        o("for (i64 j = wg;; j += 2) {\n"
+          "const i64 tix = blockIdx.x + j * gridDim.x;\n"
+          "if (tix >= ntiles) break;\n"
+          "const int bi = (int)(j %% 3);\n");
+        o("d2 *const pa = a + tbase(tix);\n");
+        o("d2 *buf = dsm + bi * %d;\n", FTILE);
+        o("mb_wait(&mbar[bi], (unsigned)((j / 3) & 1));\n");
+    } else {
+        if (mode != 0)
+            o("if (blockIdx.x < ntiles) fill(reinterpret_cast<unsigned char *>(dsm), a + tbase(blockIdx.x));\n");
+        o("int it = 0;\nfor (i64 tix = blockIdx.x; tix < ntiles; tix += gridDim.x, ++it) {\n");
+        o("d2 *const pa = a + tbase(tix);\n");
+    }
+    if (ring) {
+    } else if (mode == 1) {
         o("d2 *buf = dsm + (it & 1) * %d;\n", FTILE);
         o.s += wait_all;
         o("__syncthreads();\n{ const i64 nx = tix + gridDim.x; if (nx < ntiles) "
@@ -1209,6 +1281,10 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             // every thread has its registers: refill the buffer with the next tile
             o("__syncthreads();\n{ const i64 nx = tix + gridDim.x; if (nx < ntiles) "
               "fill(reinterpret_cast<unsigned char *>(dsm), a + tbase(nx)); }\n");
+        }
+        if (last_group && ring) {
+            // the warpgroup has its registers: the buffer takes tile j + 3
+            o("%s\nfill3(bi, j + 3);\n", SYNC.c_str());
         }
         uint64_t pend[FSMAX] = {0};
         if (fma && pend_on()) t_pend = pend;
@@ -1252,7 +1328,7 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
         t_pend = nullptr;
         t_code = nullptr;
         if (last_group && P.direct_last) {
-            if (G.perm && gi == 0 && direct_first) o("__syncthreads();\n");
+            if (G.perm && gi == 0 && direct_first) o("%s\n", SYNC.c_str());
             o("%s s0 = %s;\n", OFF, offl(P.gs_b).c_str());
             o("{\n%s", kOpaqueTid);
             for (int j = 0; j < FTBITS; ++j) o("if ((tg >> %d) & 1) s0 ^= %s;\n", j, offl(P.gs_t[j]).c_str());
@@ -1267,9 +1343,9 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             // narrowest barrier that covers every overlap
             const int hz = (gi == 0 && direct_first) ? 0 : store_hazard(G, FTHREADS, FTBITS);
             if (G.perm)
-                o("__syncthreads();\n");
+                o("%s\n", SYNC.c_str());
             else if (hz == 2)
-                o("__syncthreads();  // cross-warp store hazard\n");
+                o("%s  // cross-warp store hazard\n", SYNC.c_str());
             else if (hz == 1)
                 o("__syncwarp();\n");
             o("unsigned b0 = %uu;\n", (unsigned)G.st_b);
@@ -1280,7 +1356,7 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             o("}\n");
             for (int i = 0; i < NR(); ++i)
                 o("*reinterpret_cast<d2 *>(sb + (b0 ^ %uu)) = v[%d];\n", xcombo_h(G.st_s, i), i);
-            o("__syncthreads();\n");
+            o("%s\n", SYNC.c_str());
         }
         o("}\n");
     }
@@ -1295,7 +1371,7 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
     // order reuse with the barrier after the next wait
     if (mode == 0) o("__syncthreads();\n");
     o("}\n");
-    if (mode != 0) o.s += wait_all;
+    if (mode != 0 && !ring) o.s += wait_all;
     o("}\n");
     return o.s;
 }

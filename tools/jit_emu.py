@@ -19,6 +19,7 @@ import sys
 import numpy as np
 
 SHIM = r"""
+#include <atomic>
 #include <barrier>
 #include <cmath>
 #include <cstdint>
@@ -69,6 +70,18 @@ static inline double ng(double x) { return -x; }
 static inline double cneg(double x, unsigned m) {
     uint64_t b; std::memcpy(&b, &x, 8); b ^= uint64_t(m) << 32; std::memcpy(&x, &b, 8); return x;
 }
+// tile ring (mode 3): cp.async is a synchronous copy here, so an mbarrier
+// only counts arrivals and flips its phase; warpgroup barriers are barriers
+// over the warpgroup's threads
+struct EmuMbar { std::atomic<unsigned> count{0}, phase{0}; unsigned expected = 0; };
+static EmuMbar g_mbar[3];
+static void mb_init(EmuMbar *m, unsigned c) { m->expected = c; m->count = 0; m->phase = 0; }
+static void mb_arrive_cp(EmuMbar *m) {
+    if (m->count.fetch_add(1) + 1 == m->expected) { m->count = 0; m->phase.fetch_add(1); }
+}
+static void mb_wait(EmuMbar *m, unsigned parity) { while ((m->phase.load() & 1) == parity) std::this_thread::yield(); }
+static std::barrier<> *g_wgbar[2];
+static void wg_sync(int wg, int) { g_wgbar[wg]->arrive_and_wait(); }
 static thread_local int t_tid;
 static int g_bid, g_grid;
 static d2 *g_smem;
@@ -82,6 +95,9 @@ extern "C" void emu_run(d2 *a, long long ntiles, int nthreads, int grid) {
     g_smem = sm.data();
     std::barrier<> bar(nthreads);
     g_bar = &bar;
+    std::barrier<> wb0(nthreads / 2 > 0 ? nthreads / 2 : 1), wb1(nthreads / 2 > 0 ? nthreads / 2 : 1);
+    g_wgbar[0] = &wb0;
+    g_wgbar[1] = &wb1;
     g_grid = grid;
     for (g_bid = 0; g_bid < grid; ++g_bid) {
         std::vector<std::thread> th;
@@ -111,9 +127,13 @@ def translate(src: str):
     # the same warp have not loaded yet (the row swizzle changes between
     # transitions): the device kernel orders them with __syncwarp(); the
     # emulator's threads are independent, so order them with the barrier
-    body = body.replace("__syncwarp();", "g_bar->arrive_and_wait();")
+    ring = "__shared__ unsigned long long mbar[3];" in body
+    # (ring: the two warpgroups run out of phase -- their own barrier)
+    body = body.replace("__syncwarp();", "wg_sync(wg, 0);" if ring else "g_bar->arrive_and_wait();")
+    body = body.replace("__shared__ unsigned long long mbar[3];", "EmuMbar *mbar = g_mbar;")
     nregs = int(re.search(r"d2 v\[(\d+)\];", body).group(1))
-    return f"#define SVB_FMA {1 if fma else 0}\n" + SHIM + body + DRIVER, nthreads * nregs
+    tile = (nthreads // 2 if ring else nthreads) * nregs  # ring: two warpgroups, one tile each
+    return f"#define SVB_FMA {1 if fma else 0}\n" + SHIM + body + DRIVER, tile
 
 
 def build(path_cu: str, out_dir: str):
