@@ -131,6 +131,9 @@ __device__ __forceinline__ void cpa(void *smem, const void *g) {
     asm("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(s) : "l"(smem));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(s), "l"(g) : "memory");
 }
+__device__ __forceinline__ void cpa_u(unsigned s, const void *g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(s), "l"(g) : "memory");
+}
 __device__ __forceinline__ unsigned su32(const void *p) {
     unsigned s;
     asm("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(s) : "l"(p));
@@ -1033,8 +1036,8 @@ bool pend_on() {
 //      buffer is free, so the next tile's cp.async fill is issued there and
 //      overlaps the last group's arithmetic and direct HBM stores (passes
 //      without a direct last group use mode 0)
-//   3  tile ring (12-qubit tiles with a direct last group; the default
-//      there): one CTA per SM of two warpgroups, each running the pass's
+//   3  tile ring (12-qubit tiles with a direct last group; measured, not
+//      the default): one CTA per SM of two warpgroups, each running the pass's
 //      groups on its own tiles (even / odd tile numbers of the CTA), three
 //      64 KiB buffers shared round-robin (tile j in buffer j % 3).  The
 //      warpgroup that has read its last group out of a buffer refills it
@@ -1043,12 +1046,23 @@ bool pend_on() {
 //      last group's arithmetic; an mbarrier per buffer (cp.async arrivals)
 //      tells the consumer when its tile has landed.  Transitions sync the
 //      warpgroup only (named barriers).  ncu of mode 2 on configs[1]: 24 % of
-//      the warps' stall samples sat at the tile-start fill wait.
+//      the warps' stall samples sat at the tile-start fill wait; the ring
+//      cut that to ~5 % but ran configs[1] 4 % slower (DRAM throughput of
+//      light passes fell, STG / LDS queue stalls rose: 117.0k vs 121-123k).
+//   4  split prefetch (12-qubit tiles with a direct last group; measured, not
+//      the default -- configs[1] 123.9k vs mode 2's 123.5k, within noise):
+//      mode 2's two CTAs per SM, each with its 64 KiB working buffer W plus
+//      a 32 KiB buffer F.  A tile is filled in halves: half A (the fill's
+//      registers 0-15, byte offsets < 32 KiB) into F as soon as the first
+//      group of the previous tile has read F -- a whole tile of lead -- and
+//      half B (offsets >= 32 KiB) into its own place in W once the last
+//      group has its registers, as in mode 2 but half the bytes.  The first
+//      group reads through the affine map o -> o + 64 KiB * (o < 32 KiB).
 int jit_mode() {
     static int m = [] {
         const char *e = getenv("SVB_JIT_MODE");
         int v = e ? atoi(e) : -1;
-        return (v >= 0 && v <= 3) ? v : -1;
+        return (v >= 0 && v <= 4) ? v : -1;
     }();
     return m;
 }
@@ -1058,10 +1072,10 @@ int jit_mode() {
 // (measured on configs[1]: fm 13 mode 0 75.2k, mode 2 86.6k gate apps/s)
 int jit_pass_mode(const FPass &P) {
     int m = jit_mode();
-    if (m < 0) m = P.fm == 12 ? 3 : (P.fm > 11 ? 2 : 0);
+    if (m < 0) m = P.fm > 11 ? 2 : 0;
     if (m == 1 && P.fm != 11) m = 0;  // two tiles fit only at fm 11
-    if (m == 3 && (P.fm != 12 || P.fs < 5)) m = 2;  // three 64 KiB tiles per SM, 2 x 128 threads
-    if ((m == 2 || m == 3) && !P.direct_last) m = 0;
+    if ((m == 3 || m == 4) && (P.fm != 12 || P.fs < 5)) m = 2;  // 64 KiB tiles, 32 registers per thread
+    if ((m == 2 || m == 3 || m == 4) && !P.direct_last) m = 0;
     return m;
 }
 
@@ -1088,7 +1102,8 @@ int jit_ctas_per_sm(const FPass &P) {
 // static limit (double buffering, or tiles of 12+ qubits)
 size_t jit_dyn_smem(const FPass &P) {
     const int m = jit_pass_mode(P);
-    const size_t b = (m == 1 ? 2 : m == 3 ? 3 : 1) * (size_t(1) << P.fm) * sizeof(double2);
+    const size_t t = (size_t(1) << P.fm) * sizeof(double2);
+    const size_t b = m == 1 ? 2 * t : m == 3 ? 3 * t : m == 4 ? t + t / 2 : t;
     return b > 40 * 1024 ? b : 0;
 }
 
@@ -1152,6 +1167,7 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
     Out o;
     const int FTILE = 1 << P.fm, FTHREADS = jit_wg_threads(P), FTBITS = P.fm - P.fs;
     const bool ring = mode == 3;
+    const bool split = mode == 4;
     // CTA-wide barrier, or the warpgroup's own in the ring
     const std::string SYNC = ring ? "wg_sync(wg, " + std::to_string(FTHREADS) + ");" : "__syncthreads();";
     const int colmask = (1 << P.flow) - 1;
@@ -1208,14 +1224,38 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
         return v;
     };
     auto k_smem = [&](int k) { return (unsigned)(16 * swz_h(k * FTHREADS)); };
-    o("auto fill = [&](unsigned char *dstb, const d2 *p) {\n%s", kOpaqueTid);
-    thread_parts();
-    for (int k = 0; k < NR(); ++k)
-        o("cpa(dstb + (s ^ %uu), p + (r ^ %s));\n", k_smem(k), offl(k_row(k)).c_str());
+    if (ring) {
+        // buffer byte offset bo (a multiple of 2^16) XORed into the shared
+        // address, which stays a 32-bit shared-window offset
+        o("const unsigned sbase = su32(dsm);\n");
+        o("auto fill = [&](unsigned bo, const d2 *p) {\n%s", kOpaqueTid);
+        thread_parts();
+        o("s ^= bo;\n");
+        for (int k = 0; k < NR(); ++k)
+            o("cpa_u(sbase + (s ^ %uu), p + (r ^ %s));\n", k_smem(k), offl(k_row(k)).c_str());
+    } else {
+        o("auto fill = [&](unsigned char *dstb, const d2 *p) {\n%s", kOpaqueTid);
+        thread_parts();
+        for (int k = 0; k < NR(); ++k)
+            o("cpa(dstb + (s ^ %uu), p + (r ^ %s));\n", k_smem(k), offl(k_row(k)).c_str());
+    }
     if (ring)
         o("};\n(void)fill;\n");
     else
         o("asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\"); };\n(void)fill;\n");
+    if (split) {
+        // the fill's registers 0..NR/2-1 are the tile's bytes [0, 32K) (the
+        // top register bit is element bit fm-1, byte bit 15): half A goes to
+        // F = [64K, 96K), half B to its own place in W = [32K, 64K)
+        for (int h = 0; h < 2; ++h) {
+            o("auto fill%c = [&](const d2 *p) {\n%s", h ? 'B' : 'A', kOpaqueTid);
+            thread_parts();
+            for (int k = h * NR() / 2; k < (h + 1) * NR() / 2; ++k)
+                o("cpa(reinterpret_cast<unsigned char *>(dsm) + (s ^ %uu), p + (r ^ %s));\n",
+                  k_smem(k) + (h ? 0u : 0x10000u), offl(k_row(k)).c_str());
+            o("asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\"); };\n");
+        }
+    }
     const char *wait_all = "asm volatile(\"cp.async.wait_group 0;\\n\" ::: \"memory\");\n";
     const bool direct_first = P.direct_first && mode == 0;
     if (ring) {
@@ -1223,8 +1263,7 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
         // worked by warpgroup j & 1; its fill completes mbar[j % 3]'s phase j / 3
         o("auto fill3 = [&](int bi, i64 j) {\n"
           "const i64 t = blockIdx.x + j * gridDim.x;\n"
-          "if (t < ntiles) { fill(reinterpret_cast<unsigned char *>(dsm + bi * %d), a + tbase(t)); "
-          "mb_arrive_cp(&mbar[bi]); } };\n", FTILE);
+          "if (t < ntiles) { fill((unsigned)bi << 16, a + tbase(t)); mb_arrive_cp(&mbar[bi]); } };\n");
         o("if (threadIdx.x < 3) mb_init(&mbar[threadIdx.x], %d);\n__syncthreads();\n", FTHREADS);
         o("if (wg == 0) { fill3(0, 0); fill3(2, 2); } else { fill3(1, 1); }\n");
         o("for (i64 j = wg;; j += 2) {\n"
@@ -1235,7 +1274,9 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
         o("d2 *buf = dsm + bi * %d;\n", FTILE);
         o("mb_wait(&mbar[bi], (unsigned)((j / 3) & 1));\n");
     } else {
-        if (mode != 0)
+        if (split)
+            o("if (blockIdx.x < ntiles) { fillA(a + tbase(blockIdx.x)); fillB(a + tbase(blockIdx.x)); }\n");
+        else if (mode != 0)
             o("if (blockIdx.x < ntiles) fill(reinterpret_cast<unsigned char *>(dsm), a + tbase(blockIdx.x));\n");
         o("int it = 0;\nfor (i64 tix = blockIdx.x; tix < ntiles; tix += gridDim.x, ++it) {\n");
         o("d2 *const pa = a + tbase(tix);\n");
@@ -1249,7 +1290,7 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
           FTILE);
     } else {
         o("d2 *buf = dsm;\n");
-        if (mode == 2) {
+        if (mode == 2 || split) {
             o.s += wait_all;
             o("__syncthreads();\n");
         } else if (!direct_first) {
@@ -1258,10 +1299,30 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             o("__syncthreads();\n");
         }
     }
-    o("unsigned char *sb = reinterpret_cast<unsigned char *>(buf);\n");
+    if (ring) {
+        // buffer bi starts at byte bi << 16 of the tile area and every in-tile
+        // byte offset is < 2^16: the buffer folds into the per-thread XOR base
+        // (bo), so shared accesses keep the constant dsm base and the XOR
+        // address form (no per-access add)
+        o("unsigned char *sb = reinterpret_cast<unsigned char *>(dsm);\n(void)buf;\n");
+        o("const unsigned bo = (unsigned)bi << 16;\n");
+    } else {
+        o("unsigned char *sb = reinterpret_cast<unsigned char *>(buf);\n");
+    }
     o("d2 v[%d];\n", NR());
     for (int gi = 0; gi < P.ngroups; ++gi) {
-        const FGroup &G = P.groups[gi];
+        FGroup Gx;
+        if (split && gi == 0) {
+            // first group: bytes [0, 32K) of the tile sit in F at +64K.  The
+            // map o -> o ^ L(o) ^ K (L: byte bit 15 -> bit 16, K = 64K) is
+            // affine, so every XOR term c becomes c ^ L(c), the base also ^ K
+            Gx = P.groups[0];
+            auto L = [](uint32_t c) { return c ^ (((c >> 15) & 1u) << 16); };
+            Gx.ld_b = L(Gx.ld_b) ^ 0x10000u;
+            for (int j = 0; j < FTBMAX; ++j) Gx.ld_t[j] = L(Gx.ld_t[j]);
+            for (int k = 0; k < FSMAX; ++k) Gx.ld_s[k] = L(Gx.ld_s[k]);
+        }
+        const FGroup &G = (split && gi == 0) ? Gx : P.groups[gi];
         const bool last_group = gi == P.ngroups - 1;
         o("{ // group %d\n", gi);
         if (gi == 0 && direct_first) {
@@ -1271,7 +1332,7 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             for (int i = 0; i < NR(); ++i)
                 o("v[%d] = ldcs(pa + (g0 ^ %s));\n", i, offl(xcombo_g(P.gl_s, i)).c_str());
         } else {
-            o("unsigned a0 = %uu;\n", (unsigned)G.ld_b);
+            o("unsigned a0 = %uu%s;\n", (unsigned)G.ld_b, ring ? " ^ bo" : "");
             o.s += kOpaqueTid;
             for (int j = 0; j < FTBITS; ++j) o("if ((tg >> %d) & 1) a0 ^= %uu;\n", j, (unsigned)G.ld_t[j]);
             for (int i = 0; i < NR(); ++i)
@@ -1281,6 +1342,12 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             // every thread has its registers: refill the buffer with the next tile
             o("__syncthreads();\n{ const i64 nx = tix + gridDim.x; if (nx < ntiles) "
               "fill(reinterpret_cast<unsigned char *>(dsm), a + tbase(nx)); }\n");
+        }
+        if (last_group && split) {
+            // registers in hand: W's half B (and, when this is also the first
+            // group, F) take the next tile
+            o("__syncthreads();\n{ const i64 nx = tix + gridDim.x; if (nx < ntiles) { %sfillB(a + tbase(nx)); } }\n",
+              gi == 0 ? "fillA(a + tbase(nx)); " : "");
         }
         if (last_group && ring) {
             // the warpgroup has its registers: the buffer takes tile j + 3
@@ -1348,7 +1415,7 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
                 o("%s  // cross-warp store hazard\n", SYNC.c_str());
             else if (hz == 1)
                 o("__syncwarp();\n");
-            o("unsigned b0 = %uu;\n", (unsigned)G.st_b);
+            o("unsigned b0 = %uu%s;\n", (unsigned)G.st_b, ring ? " ^ bo" : "");
             o("{\n%s", kOpaqueTid);
             for (int j = 0; j < FTBITS; ++j) o("if ((tg >> %d) & 1) b0 ^= %uu;\n", j, (unsigned)G.st_t[j]);
             for (int k = 0; k < NS(); ++k)
@@ -1357,6 +1424,8 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             for (int i = 0; i < NR(); ++i)
                 o("*reinterpret_cast<d2 *>(sb + (b0 ^ %uu)) = v[%d];\n", xcombo_h(G.st_s, i), i);
             o("%s\n", SYNC.c_str());
+            if (split && gi == 0)  // every thread has read F: it takes the next tile's half A
+                o("{ const i64 nx = tix + gridDim.x; if (nx < ntiles) fillA(a + tbase(nx)); }\n");
         }
         o("}\n");
     }
