@@ -400,42 +400,19 @@ struct PlanPass {
 
 static int popc(uint64_t x) { return __builtin_popcountll(x); }
 
-static int flow_bits() {
-    static int f = [] {
-        const char *e = getenv("SVB_FUSE_FLOW");
-        int v = e ? atoi(e) : 3;  // 128 B runs; frees one more tile qubit than 4 (+1 %)
-        return v < 3 ? 3 : (v > 5 ? 5 : v);
-    }();
-    return f;
-}
+// 128 B runs (3 low qubits in every tile; 4 measured 1 % slower)
+static int flow_bits() { return 3; }
 
-// SVB_FUSE_PERM=0 runs X/CNOT through the arithmetic arms instead of folding
-// them into the store map (both exact; for measurement).
-static bool perm_fold() {
-    static bool f = [] {
-        const char *e = getenv("SVB_FUSE_PERM");
-        return !(e && atoi(e) == 0);
-    }();
-    return f;
-}
+// X/CNOT fold into the load / store maps (instead of the arithmetic arms)
+static bool perm_fold() { return true; }
 
-// SVB_FUSE_DIRECT=0 disables direct HBM first/last groups (for measurement)
-static bool no_direct() {
-    static bool f = [] {
-        const char *e = getenv("SVB_FUSE_DIRECT");
-        return e && atoi(e) == 0;
-    }();
-    return f;
-}
+// direct HBM first/last groups are always on
+static bool no_direct() { return false; }
 // First / last groups move registers from / to HBM directly even when their
 // lanes do not cover whole 128 B lines: a 32 B sector is then touched by
 // two instructions and L2 merges them, which costs less than a shared-memory
-// round trip (configs[1]: 82.2k -> 85.6k).  SVB_FUSE_DIRECT=1 keeps only the
-// fully coalesced ones, =0 none.
-static bool direct_any() {
-    const char *e = getenv("SVB_FUSE_DIRECT");
-    return !e || atoi(e) == 2;
-}
+// round trip (configs[1]: 82.2k -> 85.6k).
+static bool direct_any() { return true; }
 
 static uint64_t op_mask(const svb_op &o) {
     uint64_t m = uint64_t(1) << o.target;
@@ -454,13 +431,7 @@ struct Blocking {
     uint64_t z = 0, x = 0, g = 0;
     uint64_t all() const { return z | x | g; }
 };
-static bool commute_hoist() {
-    static int v = [] {
-        const char *e = getenv("SVB_FUSE_COMMUTE");
-        return e ? atoi(e) : 1;
-    }();
-    return v != 0;
-}
+static bool commute_hoist() { return true; }
 static Blocking op_class(const svb_op &o) {
     Blocking b;
     const Gate g = make_gate(o.q);
@@ -496,13 +467,7 @@ static void block_add(Blocking &blk, const Blocking &c) {
 // Greedy pass construction.  strict: only contiguous runs of ops.  Otherwise
 // a scan over the remaining ops that hoists an op past skipped ones only if
 // it shares no qubit with any skipped op (so every qubit keeps its order).
-static int planner_kind() {  // 1 greedy, 2 lookahead, 3 two-pass lookahead (default)
-    static int k = [] {
-        const char *e = getenv("SVB_FUSE_PLANNER");
-        return e ? atoi(e) : 3;
-    }();
-    return k;
-}
+static int planner_kind() { return 3; }  // 1 greedy, 2 lookahead (async JIT's quick plan), 3 two-pass lookahead
 
 // Lookahead pass construction (non-strict): grow the pass's qubit set S one
 // gate's qubits at a time, choosing among the ready gates the one whose new
@@ -591,10 +556,7 @@ static std::vector<PlanPass> plan_lookahead(int n, const svb_op *ops, int nops, 
 // that pass greedily, then plan the following pass greedily too, and keep the
 // first growth that retires the most ops over both passes.  Host-only and
 // run once per circuit (compiled plans are cached).
-static bool rotate_low() {  // SVB_FUSE_ROTATE=0: qubits 0..flow-1 in every tile
-    const char *e = getenv("SVB_FUSE_ROTATE");
-    return !e || atoi(e) != 0;
-}
+static bool rotate_low() { return true; }  // (fixed low qubits measured 203 vs 171 passes)
 
 // Qubits a pass need not tile (outside = true, runtime-specialised passes
 // only): an op acts on each of its qubits as Z-type (diagonal there -- a
@@ -628,8 +590,7 @@ static std::vector<PlanPass> plan_beam(int n, const svb_op *ops, int nops, int f
     }
     std::vector<uint64_t> need(nops);  // qubits op i needs in the tile
     for (int i = 0; i < nops; ++i) need[i] = need_mask(ops[i], outside);
-    // SVB_FUSE_TCAP: at most this many distinct non-diagonal targets per pass
-    static const int tcap = getenv("SVB_FUSE_TCAP") ? atoi(getenv("SVB_FUSE_TCAP")) : 64;
+    const int tcap = 64;  // distinct non-diagonal targets per pass: no cap (caps measured slower)
     const int window = 1024;
     auto absorb = [&](std::vector<char> &done, int first, PlanPass &p, bool mark) {
         Blocking blocked;
@@ -711,9 +672,7 @@ static std::vector<PlanPass> plan_beam(int n, const svb_op *ops, int nops, int f
         PlanPass p0;
         p0.S = rotate ? 0 : low;
         absorb(d0, first, p0, true);
-        static const int ncand = getenv("SVB_BEAM_C") ? atoi(getenv("SVB_BEAM_C")) : 12;
-        static const int wa = getenv("SVB_BEAM_W") ? atoi(getenv("SVB_BEAM_W")) : 2;
-        static const int depth = getenv("SVB_BEAM_D") ? atoi(getenv("SVB_BEAM_D")) : 3;
+        const int ncand = 12, wa = 2, depth = 3;  // candidates, first-pass weight, passes looked at
         std::vector<uint64_t> cands = candidates(d0, first, p0, ncand);
         // candidates are scored independently (each on its own copy of
         // `done`), on up to 16 host threads; the first best in candidate
@@ -902,18 +861,12 @@ static bool reg_perm(unsigned flags) {
     return e ? atoi(e) != 0 : (flags & SVB_RUN_JIT) != 0;
 }
 
-static bool reg_perm_any_ctl() {
-    const char *e = getenv("SVB_FUSE_REGPERM_CTL");
-    return !e || atoi(e) != 0;
-}
+static bool reg_perm_any_ctl() { return true; }
 
-// SVB_FUSE_GROUPLA=1: choose each register group's slot set by a dry-run
-// lookahead instead of first come (configs[1]: 544 -> 535 groups for 2x the
-// planning time; off by default)
-static bool group_lookahead() {
-    const char *e = getenv("SVB_FUSE_GROUPLA");
-    return e && atoi(e) != 0;
-}
+// (choosing each register group's slot set by a dry-run lookahead instead of
+// first come was measured: configs[1] 544 -> 535 groups for twice the
+// planning time and no speedup; off)
+static bool group_lookahead() { return false; }
 
 // Build the kernel descriptor for one pass; false if it does not fit.
 // Qubit layout: logical qubit q lives at physical index bit phys[q] (nullptr:
@@ -923,10 +876,7 @@ static bool group_lookahead() {
 // its last group then stores every register through the extra bit
 // permutation.  Gates name logical qubits; everything on the device is
 // physical.
-static bool defer_diag() {
-    const char *e = getenv("SVB_FUSE_DEFERDIAG");
-    return !e || atoi(e) != 0;
-}
+static bool defer_diag() { return true; }
 
 static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, bool strict, bool regperm,
                        int fm, const int8_t *phys = nullptr, const int8_t *phys_next = nullptr,
@@ -1091,8 +1041,7 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
                     // an X / CNOT whose target fits the group's slots runs in
                     // registers (a masked register swap) instead of being
                     // deferred to the store map, so it blocks nothing
-                    // (SVB_FUSE_REGPERM_CTL=0: only when the control is already a
-                    // slot -- a thread-bit control costs a divergent swap)
+                    // (also with a thread-bit control: a per-thread conditional swap)
                     const bool ctl_ok = m.cl < 0 || reg_perm_any_ctl() ||
                                         std::find(g.slots.begin(), g.slots.end(), m.cl) != g.slots.end();
                     const bool inreg = m.perm && mode == 0 && regperm && ctl_ok && (bits & blocked) == 0 &&
@@ -1169,7 +1118,6 @@ static bool build_pass(int n, const svb_op *ops, const PlanPass &pp, FPass &P, b
     // between): diagonals on thread or tile bits become per-thread phases
     // that cost one multiply of every register per group that has any, so
     // gathering them into fewer groups saves those multiplies.
-    // SVB_FUSE_DEFERDIAG=0 keeps them where the scan put them.
     if (!strict && gps.size() > 1 && defer_diag()) {
         const int G = (int)gps.size();
         std::vector<uint64_t> in_perm(G, 0), out_perm(G, 0);  // local bits the load / store maps touch

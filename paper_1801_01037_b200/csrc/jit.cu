@@ -634,11 +634,8 @@ void emit_gate_fold(Out &o, const FGate &g, int *code) {
 //     is consumed;
 //   diagonal (d0, d1): ph *= p ? d1 : d0, hi registers *= p ? d0/d1 : d1/d0.
 // Z^p is a sign-bit XOR of the slot's hi registers; all of it costs a few
-// integer ops instead of a select per register.  SVB_JIT_PENDTHRU=0: off.
-int pend_thru_mode() {  // bits: 1 X-type, 2 Y-like, 4 Ry-like, 8 H-like, 16 diagonal
-    const char *e = getenv("SVB_JIT_PENDTHRU");
-    return e ? atoi(e) : 31;
-}
+// integer ops instead of a select per register.
+int pend_thru_mode() { return 31; }  // bits: 1 X-type, 2 Y-like, 4 Ry-like, 8 H-like, 16 diagonal
 bool ceq(double2 a, double2 b) { return a.x == b.x && a.y == b.y; }
 double2 cdivh(double2 a, double2 b);
 double2 cnegh(double2 a) { return make_double2(-a.x, -a.y); }
@@ -843,16 +840,13 @@ double2 pick_factor(const double2 *m, bool diag) {
 // generator multiplies them into a per-thread `ph` (a few scalar
 // instructions per gate instead of a predicated multiply of every register)
 // and applies ph once, at the end of the group, fused with the global
-// factor when that is due.  SVB_JIT_PHASE=0 turns it off (measurement).
+// factor when that is due.
 // (Found with it: the last-pass flag was shadowed by the last-group flag, so
 // F was applied at the end of every pass -- exact, but one multiply of every
 // register per pass; now only the circuit's last pass applies it.)
 thread_local bool t_phase = false;  // the current group's ph is not 1
 
-int phase_mode() {  // bits: 1 thread targets, 2 tile targets, 4 controlled (0: off)
-    const char *e = getenv("SVB_JIT_PHASE");
-    return e ? atoi(e) : 7;
-}
+int phase_mode() { return 7; }  // bits: 1 thread targets, 2 tile targets, 4 controlled
 
 // ph *= (target bit ? d1 : d0), under the (thread / tile) control if any
 void emit_phase(Out &o, const FGate &g) {
@@ -891,13 +885,10 @@ std::string cm_ph(int c) {
 // per-thread value.  Those values are multiplied into a per-thread `hs<s>`
 // (scalar work) and applied to the 16 registers once, when a non-diagonal
 // gate targets s, a pending swap along s is flushed, or the group ends:
-// QFT passes carry dozens of such phases per slot.  SVB_JIT_SLOTPH=0: off.
+// QFT passes carry dozens of such phases per slot.
 thread_local unsigned t_hs = 0;  // slots whose hs is not 1
 
-bool slot_phase_on() {
-    const char *e = getenv("SVB_JIT_SLOTPH");
-    return !e || atoi(e) != 0;
-}
+bool slot_phase_on() { return true; }
 
 void slot_phase_flush(Out &o, int s) {
     if (!((t_hs >> s) & 1) || !t_code) return;
@@ -1021,11 +1012,7 @@ void emit_gate_fast(Out &o, const FGate &g, int *code, double2 &F) {
 
 }  // namespace
 
-// SVB_JIT_PEND=0 turns pending swaps off (measurement)
-bool pend_on() {
-    const char *e = getenv("SVB_JIT_PEND");
-    return !e || atoi(e) != 0;
-}
+bool pend_on() { return true; }
 
 // Tile pipelining modes of the generated kernel:
 //   0  one shared buffer, 4 CTAs/SM; the first group reads HBM directly when
@@ -1087,14 +1074,8 @@ int jit_threads(const FPass &P) { return (jit_pass_mode(P) == 3 ? 2 : 1) * jit_w
 // resident CTAs per SM the generated kernel is built for (__launch_bounds__):
 // 64K registers / (threads x registers per thread)
 int jit_ctas_per_sm(const FPass &P) {
-    static int c = [] {
-        const char *e = getenv("SVB_JIT_CTAS");
-        int v = e ? atoi(e) : 0;
-        return (v >= 1 && v <= 8) ? v : 0;
-    }();
     if (jit_pass_mode(P) == 1) return 3;
     if (jit_pass_mode(P) == 3) return 1;
-    if (c) return c;
     // 16 amplitudes per thread fit 128 registers, 32 need the full 255
     return std::max(1, 65536 / (jit_threads(P) * (P.fs >= 5 ? 256 : 128)));
 }
