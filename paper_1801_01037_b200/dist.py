@@ -635,6 +635,51 @@ class DistEngine:
         self.stats.elided += elided
         return self
 
+    def run_with_stats(self, circuit: Circuit, scheme=None) -> list:
+        """run_circuit's per-gate GateStats (engine.py:483-505) for this
+        multi-process engine: ops one at a time (no fusion, no layout
+        swaps), each bracketed by a device synchronize and timed in wall
+        clock like the reference; per gate the slowest rank's time and the
+        max over ranks of the messages / bytes the reference protocol
+        `scheme` (default b, the paper's) sends -- exact formulas
+        (partition.protocol_accounting), zero for rank-local targets.
+        time_ratio(comm, nocomm) then works on these as on the reference's."""
+        import torch
+
+        from .engine import GateStats
+        from .partition import SCHEME_B, protocol_accounting
+
+        if circuit.n != self.n:
+            raise ValidationError(f"circuit has {circuit.n} qubits, engine has {self.n}")
+        scheme = SCHEME_B if scheme is None else scheme
+        if self.layout:
+            raise ValidationError("run_with_stats runs gate by gate: build the engine with layout=False")
+        b = self.boundary
+        self._flush()
+        rows = []
+        for op in circuit.ops:
+            self.compute.synchronize()
+            t0 = time.perf_counter()
+            self.apply(op)
+            self._flush()
+            self.compute.synchronize()
+            wall = time.perf_counter() - t0
+            m = nb = 0
+            t, c = op.target, op.control
+            if t >= b:
+                act = c is None or c < b or ((self.rank >> (c - b)) & 1)
+                if act:
+                    partner = self.rank ^ (1 << (t - b))
+                    m, nb = protocol_accounting(self.plan, scheme, self.rank < partner,
+                                                c if (c is not None and c < b) else None)
+            rows.append((wall, m, nb))
+        dev = self._coll_device()
+        red = torch.tensor(rows, dtype=torch.float64, device=dev).reshape(-1, 3)
+        self.dist.all_reduce(red, op=self.dist.ReduceOp.MAX, group=self.group)
+        red = red.cpu().numpy()
+        return [GateStats(op.target, op.control, op.target >= b, int(red[i, 1]), int(red[i, 2]), float(red[i, 0]))
+                for i, op in enumerate(circuit.ops)]
+
     def norm2(self) -> float:
         import torch
 

@@ -155,3 +155,54 @@ def test_dist_engine_peer_export_failure_falls_back_together(world):
         p.join(timeout=180)
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     assert q.get(timeout=5)
+
+
+def _worker_stats(rank, world, port, n, scheme_name, queue):
+    # DistEngine.run_with_stats: per-gate GateStats of the multi-process
+    # engine equal the reference protocol's accounting (engine.protocol_stats,
+    # pinned to the reference's own run_circuit by test_host.py), and the
+    # state still matches the oracle
+    sys.path.insert(0, HERE)
+    sys.path.insert(0, os.path.dirname(HERE))
+    sys.path.insert(0, os.path.join(os.path.dirname(HERE), "oracle"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from cpu_compute import CpuCompute
+        from paper_1801_01037_b200 import engine, time_ratio, workloads as w
+        from paper_1801_01037_b200.dist import DistEngine
+        from paper_1801_01037_b200.partition import SCHEME_A, SCHEME_B, PartitionPlan, chunked
+
+        scheme = {"a": SCHEME_A, "b": SCHEME_B, "c4": chunked(4)}[scheme_name]
+        k = world.bit_length() - 1
+        a0 = w.seeded_state(n, 8)
+        circ = _circuit(n, k, seed=n + world)
+        eng = DistEngine(n, compute=CpuCompute(), initial=a0, chunk=8)
+        stats = eng.run_with_stats(circ, scheme)
+        full = eng.gather()
+        if rank == 0:
+            import oracle
+
+            want = oracle.run_ops(a0.copy(), w.oracle_ops(circ))
+            ref = engine.protocol_stats(circ, PartitionPlan(n, k), scheme)
+            got = [(s.messages_sent_per_rank, s.bytes_sent_per_rank) for s in stats]
+            comm = [s for s in stats if s.comm_required]
+            local = [s for s in stats if not s.comm_required]
+            ratio = time_ratio(comm[0], local[0])
+            queue.put((bool(np.array_equal(full, want)), got == ref, len(stats) == len(circ.ops), ratio > 0))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,scheme", [(2, "b"), (4, "a"), (4, "c4")])
+def test_dist_engine_per_gate_stats(world, scheme):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_stats, args=(r, world, port, 9, scheme, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    assert q.get(timeout=5) == (True, True, True, True)
