@@ -506,15 +506,21 @@ def run_gpu_arm(args) -> None:
     pin_in = torch.zeros(1 << n, dtype=torch.complex128).pin_memory()
     pin_in[0] = 1.0
     a_in = pin_in.numpy()
-    e2e_steps = max(3, 2 * args.steps)  # a serving batch; the pipeline fill and drain amortised
-    outs = [torch.empty(1 << n, dtype=torch.complex128).pin_memory().numpy() for _ in range(e2e_steps)]
+    e2e_steps = max(3, 4 * args.steps)  # a serving batch of 20 states by default; the pipeline fill (first H2D) and drain (last D2H) amortised over it
+    # six pinned result buffers used round robin (the library copies results
+    # out in order on one stream, so a buffer is rewritten only after it was
+    # filled six states earlier)
+    bufs = [torch.empty(1 << n, dtype=torch.complex128).pin_memory().numpy() for _ in range(min(e2e_steps, 6))]
+    outs = [bufs[k % len(bufs)] for k in range(e2e_steps)]
     kw = dict(fuse=not args.no_fuse, fma=args.fma, jit=args.jit)
     device.simulate_batch(circuit, [a_in], [outs[0]], **kw)
+    for b in bufs:
+        b[:] = 0
     t0 = time.perf_counter()
     device.simulate_batch(circuit, [a_in] * e2e_steps, outs, **kw)
     e2e_dt = time.perf_counter() - t0
     e2e_norm = float(np.vdot(outs[-1], outs[-1]).real)
-    e2e_same = all(np.array_equal(o, outs[0]) for o in outs[1:])
+    e2e_same = all(np.array_equal(o, bufs[0]) for o in bufs[1:])
     serial_steps = max(1, min(args.steps, 3))
     t0 = time.perf_counter()
     for k in range(serial_steps):
