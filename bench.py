@@ -420,6 +420,40 @@ def seam_rates(circuit) -> dict:
     return out
 
 
+def qft33_rate(args, reps: int = 3) -> dict:
+    """BASELINE configs[3]'s workload on ONE GPU -- QFT n=33 (128 GiB state)
+    from the seeded device-drawn Gaussian state, the bench's arithmetic mode,
+    one QFT per repetition over the current state: the N=1 point of the
+    configs[3] strong-scaling curve that `bench.py --gpus N` (N=2/4/8) prints
+    as its headline.  Known answers are tested in tests/test_gpu_large.py."""
+    import torch
+
+    from paper_1801_01037_b200 import device, workloads
+
+    n = 33
+    circ = workloads.qft_circuit(n)
+    torch.cuda.empty_cache()
+    st = device.DeviceState.random(n, seed=7)
+    kw = dict(fuse=not args.no_fuse, fma=args.fma, jit=args.jit)
+    device.run_ops(st, circ, **kw)  # plan + compile
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        device.run_ops(st, circ, **kw)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    nrm = device.norm2(st)
+    del st
+    torch.cuda.empty_cache()
+    return {"config": "QFT n=33 on one GPU (BASELINE configs[3] workload, N=1 point of its strong scaling)",
+            "ops": len(circ.ops), "ms_per_circuit": round(ms, 3),
+            "gate_apps_per_s": round(len(circ.ops) / (ms / 1e3), 1),
+            "hbm_passes": device.plan_passes(n, circ, fuse=not args.no_fuse, jit=args.jit),
+            "state_bytes": 16 << n, "norm_after": nrm}
+
+
 def run_gpu_arm(args) -> None:
     import tempfile
 
@@ -531,6 +565,15 @@ def run_gpu_arm(args) -> None:
     sweep = None if args.no_sweep else local_gate_sweep(SWEEP_N, SWEEP_REPS, peak)
     qft = None if args.no_sweep else qft20_rate(args)
 
+    del st
+    torch.cuda.empty_cache()
+    qft33 = None
+    if not args.no_sweep:
+        try:
+            qft33 = qft33_rate(args)
+        except Exception as exc:  # (a GPU without 128 GiB free)
+            qft33 = {"skipped": str(exc)[:200]}
+
     cores = host_cores()
     cpu = None
     if not args.no_cpu:
@@ -559,6 +602,7 @@ def run_gpu_arm(args) -> None:
         "cpu_baseline": cpu,
         "local_gate_sweep": sweep,
         "qft20": qft,
+        "qft33": qft33,
         "clocks": clk.summary(),
         "check": {"norm_after_step": norm_after, "e2e_norm": e2e_norm, "e2e_outputs_identical": e2e_same},
         "cold_start": cold,

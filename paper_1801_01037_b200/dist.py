@@ -1044,6 +1044,7 @@ def bench_main(args, clock_cls=None, peaks_fn=None) -> None:
                        "n_qubits": n, "global_qubits": k, "ops_per_circuit": nops,
                        "parallelism": f"state partition x{world}",
                        "step": "one QFT over the current state (no reset between steps)",
+                       "n1_point": "the N=1 bench line's `qft33` (the same QFT-33 on one GPU, 128 GiB)",
                        "l2": f"{slab_bytes >> 30} GiB per GPU > 126 MB L2; no flush needed"},
             "transport": ("peer memory (CUDA IPC), device-side pairwise sync" if peer else
                           "NCCL send/recv, chunk-pipelined"),
