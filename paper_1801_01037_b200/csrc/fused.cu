@@ -1860,8 +1860,10 @@ static size_t plan_cache_bytes() {
 static std::shared_ptr<const CompiledPlan> compiled_plan(int n, const svb_op *ops, int nops, bool strict,
                                                          bool regperm, int fm, int fs, bool outside,
                                                          int kind = planner_kind(), bool peek = false) {
-    static std::mutex mu;
-    static std::vector<std::pair<uint64_t, std::shared_ptr<const CompiledPlan>>> cache;  // MRU first
+    // (never destroyed: a background compile still running at process exit
+    // may use them after static destruction began)
+    static std::mutex &mu = *new std::mutex;
+    static auto &cache = *new std::vector<std::pair<uint64_t, std::shared_ptr<const CompiledPlan>>>;  // MRU first
     uint64_t key = fnv1a(ops, sizeof(svb_op) * size_t(nops), 1469598103934665603ull);
     key = fnv1a(&n, sizeof n, key);
     key = fnv1a(&strict, sizeof strict, key);
@@ -1915,8 +1917,8 @@ static std::shared_ptr<const CompiledPlan> compiled_plan(int n, const svb_op *op
 // call finds it through compiled_plan(..., peek) with jit_state 1.
 static bool start_async_jit(int n, const svb_op *ops, int nops, bool strict, bool regperm, int fm, int fs,
                             bool outside, int variant) {
-    static std::mutex mu;
-    static std::vector<uint64_t> inflight;
+    static std::mutex &mu = *new std::mutex;  // (never destroyed, as the plan cache)
+    static std::vector<uint64_t> &inflight = *new std::vector<uint64_t>;
     uint64_t key = fnv1a(ops, sizeof(svb_op) * size_t(nops), 0x2545f4914f6cdd1dull);
     key = fnv1a(&n, sizeof n, key);
     key = fnv1a(&variant, sizeof variant, key);

@@ -1498,11 +1498,13 @@ static const Nvrtc &nvrtc() {
 bool jit_available() { return nvrtc().ok; }
 
 static const std::vector<const char *> &nvrtc_opts() {
-    static const std::vector<const char *> opts = [] {
+    // (function-local statics a background compile uses are never destroyed:
+    // one may still run while static destruction proceeds at process exit)
+    static const std::vector<const char *> &opts = *new std::vector<const char *>([] {
         std::vector<const char *> o = {"-arch=sm_100a", "-std=c++17", "-default-device", "-fmad=false"};
         if (getenv("SVB_JIT_LINEINFO")) o.push_back("-lineinfo");  // for ncu source pages
         return o;
-    }();
+    }());
     return opts;
 }
 
@@ -1541,7 +1543,7 @@ static bool nvrtc_compile_now(const std::string &src, std::vector<char> &cubin, 
 // carries a magic and the source length and hash, re-checked on read, and is
 // written to a temporary name and renamed (concurrent writers are harmless).
 static const std::string &jit_cache_dir() {
-    static const std::string dir = [] {
+    static const std::string &dir = *new std::string([] {
         std::string d;
         if (const char *e = getenv("SVB_JIT_CACHE")) {
             d = e;
@@ -1558,7 +1560,7 @@ static const std::string &jit_cache_dir() {
             if (stat(d.c_str(), &st) != 0 || !S_ISDIR(st.st_mode)) d.clear();
         }
         return d;
-    }();
+    }());
     return dir;
 }
 
@@ -1710,8 +1712,8 @@ static bool ensure_dyn_smem(cudaKernel_t fn, size_t bytes) {
     if (!bytes) return true;
     int d = 0;
     if (cudaGetDevice(&d) != cudaSuccess) return false;
-    static std::mutex mu;
-    static std::unordered_map<const void *, uint64_t> done;  // kernel -> devices with the attribute
+    static std::mutex &mu = *new std::mutex;
+    static auto &done = *new std::unordered_map<const void *, uint64_t>;  // kernel -> devices with the attribute
     std::lock_guard<std::mutex> lk(mu);
     uint64_t &mask = done[(const void *)fn];
     const uint64_t bit = d < 64 ? uint64_t(1) << d : 0;
