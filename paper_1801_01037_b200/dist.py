@@ -221,6 +221,7 @@ class DistEngine:
         self._pending: list[GateOp] = []
         self._pending_key = None  # the cached tuple _pending was copied from, if any
         self._scheds: dict = {}
+        self._pi = self._ident = tuple(range(n))  # current qubit layout, logical -> physical (layout mode)
         self._bufs = None
         # peer: exchanges and swaps read / write the partner's slab in place
         # (CUDA IPC; NVLink P2P between GPUs) -- one kernel per rank.  The two
@@ -479,21 +480,30 @@ class DistEngine:
         self.stats.bytes_recv += 16 * (self.L // 2)
         self._peer_sync(partner)
 
-    def _schedule_layout(self, ops: tuple) -> tuple[list, int]:
-        """Action list with dynamic global<->local qubit swaps.
-        The layout is kept as disjoint transpositions (global home position
-        <-> local home position): a non-diagonal gate on a qubit that sits at
-        a rank bit first swaps it with the local qubit whose next use as a
-        non-diagonal target is farthest away (Belady), or swaps back a local
-        qubit that was parked there.  Gates then address physical positions;
-        the transpositions are undone at the end."""
+    def _schedule_layout(self, ops: tuple, start: tuple | None = None) -> tuple[list, int, tuple]:
+        """Action list with dynamic global<->local qubit swaps,
+        from the layout `start` (logical -> physical; default identity) to the
+        returned end layout.  The layout is kept as disjoint transpositions
+        (global home position <-> local home position): a non-diagonal gate
+        on a qubit that sits at a rank bit first swaps it with the local
+        qubit whose next use as a non-diagonal target is farthest away
+        (Belady; with the circuit taken as cyclic -- a qubit not used again
+        in this run counts from its first use in the next run of the same
+        circuit, which is what repeated runs see), or swaps back a local
+        qubit that was parked there.  Gates then address physical
+        positions.  The transpositions are NOT undone at the end: the engine
+        keeps the layout across runs and restores the identity only when the
+        state is read in logical order (canonical())."""
         n, b = self.n, self.boundary
-        pi = list(range(n))   # logical -> physical
-        inv = list(range(n))  # physical -> logical
+        pi = list(start) if start is not None else list(range(n))  # logical -> physical
+        inv = [0] * n  # physical -> logical
+        for q, ph in enumerate(pi):
+            inv[ph] = q
         uses = [[] for _ in range(n)]  # op indices where a qubit is a non-diagonal target
         for i, op in enumerate(ops):
             if not _is_diag(op.gate):
                 uses[op.target].append(i)
+        first = [u[0] if u else len(ops) for u in uses]
         ptr = [0] * n
         actions, pending = [], []
         elided = 0
@@ -514,7 +524,7 @@ class DistEngine:
             u = uses[q]
             while ptr[q] < len(u) and u[ptr[q]] < i:
                 ptr[q] += 1
-            return u[ptr[q]] if ptr[q] < len(u) else len(ops) + 1
+            return u[ptr[q]] if ptr[q] < len(u) else len(ops) + first[q]
 
         for i, op in enumerate(ops):
             g = op.gate
@@ -549,16 +559,15 @@ class DistEngine:
                 d = Gate2x2(s_, 0, 0, s_)
                 pending.append(GateOp("single", d, 0) if c is None else
                                GateOp("controlled", d, 1 if c == 0 else 0, c))
-        for gp in range(b, n):  # undo the parked transpositions
-            if inv[gp] != gp:
-                swap(gp, pi[gp])
         flush()
-        return actions, elided
+        return actions, elided, tuple(pi)
 
     # -- public ---------------------------------------------------------------
 
     def apply(self, op: GateOp) -> None:
         """One op with the reference's regime dispatch (engine.py:488-494, 415-450)."""
+        if self._pi != self._ident:  # ops address logical qubits: identity layout first
+            self.canonical()
         t, c, g = op.target, op.control, op.gate
         b = self.boundary
         if c is not None and c >= b:
@@ -584,15 +593,19 @@ class DistEngine:
         and ("exchange", gate, target, control) steps -- as apply() would
         produce it; cached per circuit so repeated runs do no per-op Python
         work (the local tuples also hit the packed-op cache)."""
+        if self.layout:
+            key = (id(ops), self._pi)
+            hit = self._scheds.get(key)
+            if hit is not None and hit[0] is ops:
+                return hit[1], hit[2], hit[3]
+            actions, elided, end = self._schedule_layout(ops, self._pi)
+            if len(self._scheds) >= 16:
+                self._scheds.pop(next(iter(self._scheds)))
+            self._scheds[key] = (ops, actions, elided, end)
+            return actions, elided, end
         hit = self._scheds.get(id(ops))
         if hit is not None and hit[0] is ops:
-            return hit[1], hit[2]
-        if self.layout:
-            actions, elided = self._schedule_layout(ops)
-            if len(self._scheds) >= 8:
-                self._scheds.pop(next(iter(self._scheds)))
-            self._scheds[id(ops)] = (ops, actions, elided)
-            return actions, elided
+            return hit[1], hit[2], None
         saved, self._pending = self._pending, []
         actions, elided = [], 0
         exchange = self._exchange
@@ -613,16 +626,32 @@ class DistEngine:
         finally:
             self._exchange = exchange
             self._pending = saved
-        if len(self._scheds) >= 8:
+        if len(self._scheds) >= 16:
             self._scheds.pop(next(iter(self._scheds)))
         self._scheds[id(ops)] = (ops, actions, elided)
-        return actions, elided
+        return actions, elided, None
+
+    def canonical(self) -> "DistEngine":
+        """Restore the identity qubit layout (undo the parked global<->local
+        transpositions a layout run leaves): afterwards the slab holds its
+        amplitudes in logical index order.  gather() calls it; norm2 needs
+        no call (permutation-invariant)."""
+        self._flush()
+        n, b = self.n, self.boundary
+        for g in range(b, n):
+            q = self._pi.index(g)  # the logical qubit at global position g
+            if q != g:
+                self._swap(g, self._pi[g])
+                pi = list(self._pi)
+                pi[q], pi[g] = pi[g], pi[q]
+                self._pi = tuple(pi)
+        return self
 
     def run(self, circuit: Circuit) -> "DistEngine":
         if circuit.n != self.n:
             raise ValidationError(f"circuit has {circuit.n} qubits, engine has {self.n}")
         self._flush()
-        actions, elided = self._schedule(circuit.ops)
+        actions, elided, end = self._schedule(circuit.ops)
         for act in actions:
             if act[0] == "local":
                 self._pending = list(act[1])
@@ -633,6 +662,8 @@ class DistEngine:
             else:
                 self._exchange(act[1], act[2], act[3])
         self.stats.elided += elided
+        if end is not None:
+            self._pi = end
         return self
 
     def run_with_stats(self, circuit: Circuit, scheme=None) -> list:
@@ -699,7 +730,7 @@ class DistEngine:
         """Full state on rank 0 (engine.py:188-192); None elsewhere."""
         import torch
 
-        self._flush()
+        self.canonical()
         dev = self._coll_device()
         mine = self.slab.to(dev)
         parts = [torch.zeros(self.L, dtype=torch.complex128, device=dev) for _ in range(self.world)]
@@ -871,10 +902,12 @@ def _qft_checks(eng: "DistEngine", circ: Circuit, dev) -> dict:
     x = 0x1234567 % N
     rng = np_.random.default_rng(5)
     ys = [0, 1, N - 1] + [int(v) for v in rng.integers(0, N, size=61)]
+    eng.canonical()
     eng.slab.zero_()
     if x // L == r:
         eng.slab[x % L] = 1.0
     eng.run(circ)
+    eng.canonical()
     eng.compute.synchronize()
     err = 0.0
     for y in ys:
@@ -886,6 +919,7 @@ def _qft_checks(eng: "DistEngine", circ: Circuit, dev) -> dict:
     init = eng.slab.clone()
     eng.run(circ)
     eng.run(workloads.inverse_circuit(circ))
+    eng.canonical()
     eng.compute.synchronize()
     rt = _allmax(float((eng.slab - init).abs().max().item()), dev)
     del init
@@ -981,6 +1015,7 @@ def bench_main(args, clock_cls=None, peaks_fn=None) -> None:
         for _ in range(e2e_steps):
             eng.slab.copy_(host, non_blocking=True)
             eng.run(circ)
+            eng.canonical()  # the result in logical order
             host.copy_(eng.slab, non_blocking=True)
             torch.cuda.synchronize()
         e2e_dt = _allmax(time.perf_counter() - t0, dev)

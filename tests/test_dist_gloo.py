@@ -206,3 +206,58 @@ def test_dist_engine_per_gate_stats(world, scheme):
         p.join(timeout=180)
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     assert q.get(timeout=5) == (True, True, True, True)
+
+
+def _worker_layout_runs(rank, world, port, n, queue):
+    # the layout engine keeps its global<->local transpositions across runs
+    # (restored only when the state is read in logical order): three runs,
+    # then one op through apply() (which restores the layout first), then
+    # gather -- equal to the oracle applying the same ops in order
+    sys.path.insert(0, HERE)
+    sys.path.insert(0, os.path.dirname(HERE))
+    sys.path.insert(0, os.path.join(os.path.dirname(HERE), "oracle"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from cpu_compute import CpuCompute
+        from paper_1801_01037_b200 import GateOp, standard_gate, workloads as w
+        from paper_1801_01037_b200.dist import DistEngine
+
+        k = world.bit_length() - 1
+        a0 = w.seeded_state(n, 9)
+        circ = _circuit(n, k, seed=5 * n + world)
+        qft = w.qft_circuit(n)
+        eng = DistEngine(n, compute=CpuCompute(), initial=a0, chunk=8, layout=True)
+        eng.run(circ)
+        eng.run(qft)
+        eng.run(circ)
+        parked = eng._pi != tuple(range(n))
+        extra = GateOp("single", standard_gate("h"), n - 1)
+        eng.apply(extra)
+        full = eng.gather()
+        if rank == 0:
+            import oracle
+
+            want = a0.copy()
+            for c in (circ, qft, circ):
+                want = oracle.run_ops(want, w.oracle_ops(c))
+            want = oracle.run_ops(want, [(extra.gate, extra.target, None)])
+            queue.put((bool(np.max(np.abs(full - want)) <= 1e-12), parked))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_dist_engine_layout_persists_across_runs(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_layout_runs, args=(r, world, port, 10, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    ok, parked = q.get(timeout=5)
+    assert ok
+    assert parked  # the layout really was left permuted between runs
