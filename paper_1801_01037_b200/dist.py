@@ -38,7 +38,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .core import Circuit, Gate2x2, GateOp
-from .errors import ValidationError
+from .errors import ContractViolation, ValidationError
 from .partition import PartitionPlan
 
 DEFAULT_CHUNK = 1 << 24  # amplitudes per pipelined message (256 MiB)
@@ -178,6 +178,11 @@ class ExchangeStats:
 
 def _is_diag(g: Gate2x2) -> bool:
     return complex(g.q12) == 0 and complex(g.q21) == 0
+
+
+def _is_x(op: GateOp) -> bool:
+    g = op.gate
+    return complex(g.q11) == 0 and complex(g.q22) == 0 and complex(g.q12) == 1 and complex(g.q21) == 1
 
 
 class DistEngine:
@@ -483,25 +488,41 @@ class DistEngine:
     def _schedule_layout(self, ops: tuple, start: tuple | None = None) -> tuple[list, int, tuple]:
         """Action list with dynamic global<->local qubit swaps,
         from the layout `start` (logical -> physical; default identity) to the
-        returned end layout.  The layout is kept as disjoint transpositions
-        (global home position <-> local home position): a non-diagonal gate
-        on a qubit that sits at a rank bit first swaps it with the local
-        qubit whose next use as a non-diagonal target is farthest away
-        (Belady; with the circuit taken as cyclic -- a qubit not used again
-        in this run counts from its first use in the next run of the same
-        circuit, which is what repeated runs see), or swaps back a local
-        qubit that was parked there.  Gates then address physical
-        positions.  The transpositions are NOT undone at the end: the engine
-        keeps the layout across runs and restores the identity only when the
-        state is read in logical order (canonical())."""
+        returned end layout.  A non-diagonal gate on a qubit that sits at a
+        rank bit first swaps it (one half-slab exchange) with the local
+        position whose qubit's next use as a non-diagonal target is farthest
+        away (Belady; with the circuit taken as cyclic -- a qubit not used
+        again in this run counts from its first use in the next run of the
+        same circuit, which is what repeated runs see), keeping the gate's
+        control local.  A SWAP written as three CNOTs (c->t, t->c, c->t, the
+        reference's form, e.g. the QFT's final reversal) is a relabeling:
+        the two logical qubits trade physical positions and nothing moves
+        (unless both sit at rank bits).  Gates then address physical
+        positions.  The layout is NOT restored at the end: the engine keeps
+        it across runs and restores the identity only when the state is read
+        in logical order (canonical())."""
         n, b = self.n, self.boundary
         pi = list(start) if start is not None else list(range(n))  # logical -> physical
         inv = [0] * n  # physical -> logical
         for q, ph in enumerate(pi):
             inv[ph] = q
+        triple = set()  # op indices starting a CNOT-triple SWAP
+        i = 0
+        while i + 2 < len(ops):
+            a, bb, cc = ops[i], ops[i + 1], ops[i + 2]
+            if (_is_x(a) and _is_x(bb) and _is_x(cc) and a.control is not None and bb.control is not None
+                    and cc.control is not None and bb.control == a.target and bb.target == a.control
+                    and cc.control == a.control and cc.target == a.target):
+                triple.add(i)
+                i += 3
+            else:
+                i += 1
+        skip = set()
+        for i in triple:
+            skip.update((i, i + 1, i + 2))
         uses = [[] for _ in range(n)]  # op indices where a qubit is a non-diagonal target
         for i, op in enumerate(ops):
-            if not _is_diag(op.gate):
+            if i not in skip and not _is_diag(op.gate):
                 uses[op.target].append(i)
         first = [u[0] if u else len(ops) for u in uses]
         ptr = [0] * n
@@ -526,25 +547,32 @@ class DistEngine:
                 ptr[q] += 1
             return u[ptr[q]] if ptr[q] < len(u) else len(ops) + first[q]
 
-        for i, op in enumerate(ops):
+        i = 0
+        while i < len(ops):
+            op = ops[i]
+            if i in triple:
+                qa, qb = op.control, op.target
+                if pi[qa] < b or pi[qb] < b:  # relabel: no data moves
+                    pa, pb = pi[qa], pi[qb]
+                    pi[qa], pi[qb] = pb, pa
+                    inv[pa], inv[pb] = qb, qa
+                    i += 3
+                    continue
             g = op.gate
             t = pi[op.target]
             c = pi[op.control] if op.control is not None else None
             if t >= b and not (self.elide_diagonal and _is_diag(g)):
-                if inv[t] >= b:  # a global qubit at home: park a local one there
-                    best, far = -1, -1
-                    for lp in range(b):
-                        q = inv[lp]
-                        if q != lp or lp == c:  # keep transpositions disjoint; keep the control local
-                            continue
-                        nu = next_use(q, i)
-                        if nu > far:
-                            best, far = lp, nu
-                    swap(t, best)
-                else:  # a parked local qubit p = inv[t]: swap it back to its home p
-                    swap(t, inv[t])
+                best, far = -1, -1
+                for lp in range(b):
+                    if lp == c:  # keep the control local
+                        continue
+                    nu = next_use(inv[lp], i)
+                    if nu > far:
+                        best, far = lp, nu
+                swap(t, best)
                 t = pi[op.target]
                 c = pi[op.control] if op.control is not None else None
+            i += 1
             if c is not None and c >= b:
                 if not (self.rank >> (c - b)) & 1:
                     continue
@@ -632,19 +660,44 @@ class DistEngine:
         return actions, elided, None
 
     def canonical(self) -> "DistEngine":
-        """Restore the identity qubit layout (undo the parked global<->local
-        transpositions a layout run leaves): afterwards the slab holds its
-        amplitudes in logical index order.  gather() calls it; norm2 needs
-        no call (permutation-invariant)."""
+        """Restore the identity qubit layout a layout run leaves (rank-bit
+        positions by half-slab swaps, then the local bit permutation as SWAP
+        gates -- three CNOTs each, register renames in one fused run):
+        afterwards the slab holds its amplitudes in logical index order.
+        gather() and apply() call it; norm2 needs no call
+        (permutation-invariant)."""
         self._flush()
+        if self._pi == self._ident:
+            return self
         n, b = self.n, self.boundary
+        pi = list(self._pi)
+        inv = [0] * n
+        for q, p in enumerate(pi):
+            inv[p] = q
         for g in range(b, n):
-            q = self._pi.index(g)  # the logical qubit at global position g
-            if q != g:
-                self._swap(g, self._pi[g])
-                pi = list(self._pi)
-                pi[q], pi[g] = pi[g], pi[q]
-                self._pi = tuple(pi)
+            if inv[g] == g:
+                continue
+            p = pi[g]  # where logical qubit g sits
+            if p >= b:
+                raise ContractViolation("layout permutes rank bits among themselves")  # never scheduled
+            self._swap(g, p)
+            qg, qp = inv[g], inv[p]
+            pi[qg], pi[qp] = p, g
+            inv[g], inv[p] = qp, qg
+        x = Gate2x2(0, 1, 1, 0)
+        ops = []
+        for l in range(b):
+            if inv[l] == l:
+                continue
+            p = pi[l]  # physical position of logical l (local)
+            ops += [GateOp("controlled", x, p, l), GateOp("controlled", x, l, p), GateOp("controlled", x, p, l)]
+            ql, qp = inv[l], inv[p]
+            pi[ql], pi[qp] = p, l
+            inv[l], inv[p] = qp, ql
+        if ops:
+            self._pending = ops
+            self._flush()
+        self._pi = self._ident
         return self
 
     def run(self, circuit: Circuit) -> "DistEngine":
