@@ -757,6 +757,8 @@ class DistEngine:
                     m, nb = protocol_accounting(self.plan, scheme, self.rank < partner,
                                                 c if (c is not None and c < b) else None)
             rows.append((wall, m, nb))
+        if not rows:  # (every rank holds the same circuit: all return here)
+            return []
         dev = self._coll_device()
         red = torch.tensor(rows, dtype=torch.float64, device=dev).reshape(-1, 3)
         self.dist.all_reduce(red, op=self.dist.ReduceOp.MAX, group=self.group)

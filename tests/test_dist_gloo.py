@@ -179,6 +179,8 @@ def _worker_stats(rank, world, port, n, scheme_name, queue):
         circ = _circuit(n, k, seed=n + world)
         eng = DistEngine(n, compute=CpuCompute(), initial=a0, chunk=8)
         stats = eng.run_with_stats(circ, scheme)
+        assert eng.run_with_stats(type(circ)(n, ()), scheme) == []  # empty circuit
+        eng.run(type(circ)(n, ()))
         full = eng.gather()
         if rank == 0:
             import oracle
