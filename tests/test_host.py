@@ -188,3 +188,25 @@ def test_library_refuses_without_cuda():
 
     with pytest.raises(NativeLibraryMissing):
         device.simulate(workloads.qft_circuit(3))
+
+
+def test_c_abi_example_links():
+    """examples/qft_host.c (a compiled caller using only include/svb.h) builds
+    and links against libsvb.so; on a host without a GPU it runs up to the
+    first device call and fails loudly (no CPU fallback)."""
+    import subprocess
+
+    exe = os.path.join(REPO, "examples", "qft_host")
+    if not os.path.exists(exe):
+        pytest.skip("examples/qft_host not built (run build())")
+    r = subprocess.run([exe, "18", "12345"], capture_output=True, text=True, timeout=300)
+    try:
+        import torch
+
+        has_gpu = torch.cuda.is_available()
+    except Exception:
+        has_gpu = False
+    if has_gpu:
+        assert r.returncode == 0, r.stdout + r.stderr
+    else:
+        assert r.returncode == 2, r.stdout + r.stderr  # the library reports the missing device
