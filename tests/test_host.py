@@ -190,23 +190,31 @@ def test_library_refuses_without_cuda():
         device.simulate(workloads.qft_circuit(3))
 
 
-def test_c_abi_example_links():
-    """examples/qft_host.c (a compiled caller using only include/svb.h) builds
-    and links against libsvb.so; on a host without a GPU it runs up to the
-    first device call and fails loudly (no CPU fallback)."""
+def _run_qft_host(n, x):
     import subprocess
 
     exe = os.path.join(REPO, "examples", "qft_host")
     if not os.path.exists(exe):
         pytest.skip("examples/qft_host not built (run build())")
-    r = subprocess.run([exe, "18", "12345"], capture_output=True, text=True, timeout=300)
-    try:
-        import torch
+    return subprocess.run([exe, str(n), str(x)], capture_output=True, text=True, timeout=300)
 
-        has_gpu = torch.cuda.is_available()
-    except Exception:
-        has_gpu = False
-    if has_gpu:
-        assert r.returncode == 0, r.stdout + r.stderr
-    else:
-        assert r.returncode == 2, r.stdout + r.stderr  # the library reports the missing device
+
+def test_c_abi_example_links():
+    """examples/qft_host.c (a compiled caller using only include/svb.h) builds
+    and links against libsvb.so; on a host without a GPU it runs up to the
+    first device call and fails loudly (no CPU fallback)."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: tests/test_host.py::test_c_abi_example_on_gpu runs it")
+    r = _run_qft_host(6, 3)
+    assert r.returncode == 2, r.stdout + r.stderr  # the library reports the missing device
+
+
+@pytest.mark.gpu
+def test_c_abi_example_on_gpu(cuda_ok):
+    """The same C program on the B200: QFT n=18 of |12345> through
+    svb_host_run_ops, every amplitude within 1e-12 of the closed form."""
+    r = _run_qft_host(18, 12345)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "max|err|" in r.stdout
