@@ -651,9 +651,11 @@ void emit_zp(Out &o, int s, uint64_t mask) {
         if ((i >> s) & 1) o("v[%d] = mk(cneg(v[%d].x, pm), cneg(v[%d].y, pm));\n", i, i, i);
     o("}\n");
 }
+extern thread_local bool t_phase_sign;
 void emit_phase_sign(Out &o, uint64_t mask) {  // ph *= (-1)^p
     o("{ const unsigned pm = %s ? 0x80000000u : 0u; ph = mk(cneg(ph.x, pm), cneg(ph.y, pm)); }\n",
       pcond(mask).c_str());
+    if (!t_phase) t_phase_sign = true;  // (ph stays +-1 unless a phase joins)
     t_phase = true;
 }
 
@@ -697,6 +699,7 @@ bool pend_through(Out &o, const FGate &g, int *code, double2 &F) {
     o("ph = cm(p ? %s : %s, p ? %s : %s, ph);\n", lit(d1.x).c_str(), lit(d0.x).c_str(), lit(d1.y).c_str(),
       lit(d0.y).c_str());
     t_phase = true;
+    t_phase_sign = false;
     const int ur = unit_code(r), uri = unit_code(ri);
     if (ur >= 0 && uri >= 0) {
         // r = i^u, 1/r = i^-u = i^u (-1)^[u odd]: a code plus a conditional sign
@@ -845,6 +848,7 @@ double2 pick_factor(const double2 *m, bool diag) {
 // F was applied at the end of every pass -- exact, but one multiply of every
 // register per pass; now only the circuit's last pass applies it.)
 thread_local bool t_phase = false;  // the current group's ph is not 1
+thread_local bool t_phase_sign = false;  // ... and it is only a sign, +-1
 
 int phase_mode() { return 7; }  // bits: 1 thread targets, 2 tile targets, 4 controlled
 
@@ -865,6 +869,7 @@ void emit_phase(Out &o, const FGate &g) {
     if (g.cl >= 0) o("}\n");
     o("}\n");
     t_phase = true;
+    t_phase_sign = false;
 }
 
 // ph * (i^c X) for register X holding a pending unit factor c
@@ -887,6 +892,21 @@ std::string cm_ph(int c) {
 // gate targets s, a pending swap along s is flushed, or the group ends:
 // QFT passes carry dozens of such phases per slot.
 thread_local unsigned t_hs = 0;  // slots whose hs is not 1
+
+// Pending constant diagonals (fast mode).  An uncontrolled diagonal gate on
+// slot s, diag(1, d) after factor extraction with d not a unit, multiplies
+// the 16 registers with slot bit s set by the compile-time constant d.  It
+// commutes with every gate that does not target s (a pair update along
+// another slot sees the same factor on both registers of a pair; controls
+// on s select whole halves), so it is kept pending as t_pd[s] -- further
+// diagonals on s multiply into it -- and applied when a gate targets s or
+// at the group's end, where each register's pending constants ride on the
+// per-thread phase or the global factor that is applied anyway (one
+// complex multiply per register for all of them).
+thread_local double2 t_pd[FSMAX];
+thread_local unsigned t_pdm = 0;  // slots with a pending constant
+
+void pd_flush(Out &o, int s);
 
 bool slot_phase_on() { return true; }
 
@@ -940,7 +960,10 @@ bool pend_through(Out &o, const FGate &g, int *code, double2 &F);
 void emit_gate_fast(Out &o, const FGate &g, int *code, double2 &F) {
     const int op = g.op;
     if (slot_phase_take(o, g)) return;
-    if (op < FOP_DIAG) slot_phase_flush(o, (op >> 1) % FSMAX);  // a non-diagonal gate on that slot
+    if (op < FOP_DIAG) {  // a non-diagonal gate on that slot
+        slot_phase_flush(o, (op >> 1) % FSMAX);
+        pd_flush(o, (op >> 1) % FSMAX);
+    }
     if (pend_through(o, g, code, F)) return;
     if (op >= FOP_DIAG && phase_mode()) {
         const int c = op - FOP_DIAG, pm = phase_mode();
@@ -1007,7 +1030,34 @@ void emit_gate_fast(Out &o, const FGate &g, int *code, double2 &F) {
         }
         return;
     }
+    if (unit_code(d0) == 0 && unit_code(d1) < 0 && !(t_pend && t_pend[tpos])) {
+        if (!((t_pdm >> tpos) & 1)) t_pd[tpos] = make_double2(1.0, 0.0);
+        t_pd[tpos] = cmulh(t_pd[tpos], d1);  // pending on slot tpos's hi half
+        t_pdm |= 1u << tpos;
+        return;
+    }
+    pd_flush(o, tpos);
     for (int i = 0; i < NR(); ++i) mul(i, ((i >> tpos) & 1) ? d1 : d0, false);
+}
+
+// apply slot s's pending constant to its hi half
+void pd_flush(Out &o, int s) {
+    if (!((t_pdm >> s) & 1) || !t_code) return;
+    const double2 d = t_pd[s];
+    for (int i = 0; i < NR(); ++i) {
+        if (!((i >> s) & 1)) continue;
+        o("{ const d2 X = v[%d]; v[%d] = %s; }\n", i, i, cm_fold(d, t_code[i]).c_str());
+        t_code[i] = 0;
+    }
+    t_pdm &= ~(1u << s);
+}
+
+// register i's product of pending slot constants (1 if none)
+double2 pd_of(int i) {
+    double2 c = make_double2(1.0, 0.0);
+    for (int s = 0; s < NS(); ++s)
+        if (((t_pdm >> s) & 1) && ((i >> s) & 1)) c = cmulh(c, t_pd[s]);
+    return c;
 }
 
 }  // namespace
@@ -1340,7 +1390,9 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             int code[FREGMAX] = {0};
             t_code = code;
             t_phase = false;
+            t_phase_sign = false;
             t_hs = 0;
+            t_pdm = 0;
             o("d2 ph = mk(1.0, 0.0);\n");
             for (int k = 0; k < NS(); ++k) o("d2 hs%d = mk(1.0, 0.0);\n", k);
             for (int q = G.first; q < G.first + G.count; ++q) emit_gate_fast(o, P.gates[q], code, F);
@@ -1348,21 +1400,51 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             const double mag = cabsh(F);
             const bool applyF = gi == P.ngroups - 1 && (last || mag < 0x1p-200 || mag > 0x1p200) &&
                                 !(F.x == 1.0 && F.y == 0.0);
-            if (t_phase) {  // ph (times F when due) on every register
+            if (t_phase && t_phase_sign && !applyF && !t_pdm) {
+                // ph is +-1: flip the sign bits of every register (integer pipe)
+                // instead of a complex multiply; pending unit factors commute
+                o("{ const unsigned pm = (unsigned)__double2hiint(ph.x) & 0x80000000u;\n");
+                for (int i = 0; i < NR(); ++i) o("v[%d] = mk(cneg(v[%d].x, pm), cneg(v[%d].y, pm));\n", i, i, i);
+                o("}\n");
+            } else if (t_phase) {  // ph (times F when due, times the pending slot constants) on every register
                 if (applyF) {
                     o("ph = cm(%s, %s, ph);\n", lit(F.x).c_str(), lit(F.y).c_str());
                     F = make_double2(1.0, 0.0);
                 }
+                // one per-thread scalar per pattern of pending slots: ph * constant
+                std::vector<int> made(1u << NS(), 0);
                 for (int i = 0; i < NR(); ++i) {
-                    o("{ const d2 X = v[%d]; v[%d] = %s; }\n", i, i, cm_ph(code[i]).c_str());
+                    const unsigned pat = t_pdm & unsigned(i);
+                    std::string var = "ph";
+                    if (pat) {
+                        var = "php" + std::to_string(pat);
+                        if (!made[pat]) {
+                            const double2 c = pd_of(i);
+                            o("const d2 %s = cm(%s, %s, ph);\n", var.c_str(), lit(c.x).c_str(), lit(c.y).c_str());
+                            made[pat] = 1;
+                        }
+                    }
+                    std::string e = cm_ph(code[i]);
+                    for (size_t at; (at = e.find("ph.")) != std::string::npos;) e.replace(at, 3, var + "#");
+                    for (size_t at; (at = e.find("#")) != std::string::npos;) e.replace(at, 1, ".");
+                    o("{ const d2 X = v[%d]; v[%d] = %s; }\n", i, i, e.c_str());
                     code[i] = 0;
                 }
+                t_pdm = 0;
             } else if (applyF) {
                 for (int i = 0; i < NR(); ++i) {  // stored * F = true amplitude
-                    o("{ const d2 X = v[%d]; v[%d] = %s; }\n", i, i, cm_fold(F, code[i]).c_str());
+                    o("{ const d2 X = v[%d]; v[%d] = %s; }\n", i, i, cm_fold(cmulh(F, pd_of(i)), code[i]).c_str());
                     code[i] = 0;
                 }
+                t_pdm = 0;
                 F = make_double2(1.0, 0.0);
+            } else if (t_pdm) {  // the pending slot constants alone, one multiply per register
+                for (int i = 0; i < NR(); ++i) {
+                    if (!(t_pdm & unsigned(i))) continue;
+                    o("{ const d2 X = v[%d]; v[%d] = %s; }\n", i, i, cm_fold(pd_of(i), code[i]).c_str());
+                    code[i] = 0;
+                }
+                t_pdm = 0;
             }
             for (int i = 0; i < NR(); ++i) materialize(o, code, i);
         } else if (fma) {

@@ -67,6 +67,7 @@ static inline d2 ldcs(const d2 *p) { return *p; }
 static inline void stcs(d2 *p, d2 v) { *p = v; }
 static inline int swz(int l) { return l ^ ((l >> 3) ^ (l >> 6) ^ (l >> 9) ^ (l >> 12)) & 7; }
 static inline double ng(double x) { return -x; }
+static inline int __double2hiint(double x) { uint64_t b; std::memcpy(&b, &x, 8); return (int)(b >> 32); }
 static inline double cneg(double x, unsigned m) {
     uint64_t b; std::memcpy(&b, &x, 8); b ^= uint64_t(m) << 32; std::memcpy(&x, &b, 8); return x;
 }
