@@ -652,6 +652,7 @@ void emit_zp(Out &o, int s, uint64_t mask) {
     o("}\n");
 }
 extern thread_local bool t_phase_sign;
+extern thread_local unsigned t_hs;
 void emit_phase_sign(Out &o, uint64_t mask) {  // ph *= (-1)^p
     o("{ const unsigned pm = %s ? 0x80000000u : 0u; ph = mk(cneg(ph.x, pm), cneg(ph.y, pm)); }\n",
       pcond(mask).c_str());
@@ -712,18 +713,11 @@ bool pend_through(Out &o, const FGate &g, int *code, double2 &F) {
                 if ((i >> s) & 1) o("v[%d] = mk(cneg(v[%d].x, pm), cneg(v[%d].y, pm));\n", i, i, i);
         }
     } else {
-        o("const double cx = p ? %s : %s, cy = p ? %s : %s;\n", lit(ri.x).c_str(), lit(r.x).c_str(),
-          lit(ri.y).c_str(), lit(r.y).c_str());
-        for (int i = 0; i < NR(); ++i) {
-            if (!((i >> s) & 1)) continue;
-            double k1 = 1.0, k2 = 1.0;
-            const char *m1 = phys(code[i], 0, k1), *m2 = phys(code[i], 1, k2);
-            auto sg = [](double k) { return k < 0 ? "-" : ""; };
-            o("{ const d2 X = v[%d]; v[%d] = mk(__fma_rn(cx, %sX.%s, %s__dmul_rn(cy, X.%s)), "
-              "__fma_rn(cx, %sX.%s, %s__dmul_rn(cy, X.%s))); }\n",
-              i, i, sg(k1), m1, sg(-k2), m2, sg(k2), m2, sg(k1), m1);
-            code[i] = 0;
-        }
+        // the hi registers' factor p ? 1/r : r joins slot s's per-slot phase
+        // (applied once, merged with the group-end multiply when there is one)
+        o("hs%d = cm(p ? %s : %s, p ? %s : %s, hs%d);\n", s, lit(ri.x).c_str(), lit(r.x).c_str(),
+          lit(ri.y).c_str(), lit(r.y).c_str(), s);
+        t_hs |= 1u << s;
     }
     o("}\n");
     return true;
@@ -1396,32 +1390,51 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             o("d2 ph = mk(1.0, 0.0);\n");
             for (int k = 0; k < NS(); ++k) o("d2 hs%d = mk(1.0, 0.0);\n", k);
             for (int q = G.first; q < G.first + G.count; ++q) emit_gate_fast(o, P.gates[q], code, F);
-            for (int k = 0; k < NS(); ++k) slot_phase_flush(o, k);
             const double mag = cabsh(F);
             const bool applyF = gi == P.ngroups - 1 && (last || mag < 0x1p-200 || mag > 0x1p200) &&
                                 !(F.x == 1.0 && F.y == 0.0);
-            if (t_phase && t_phase_sign && !applyF && !t_pdm) {
+            if (!t_phase && !applyF)  // nothing multiplies every register: per-slot phases alone
+                for (int k = 0; k < NS(); ++k) slot_phase_flush(o, k);
+            if (t_phase && t_phase_sign && !applyF && !t_pdm && !t_hs) {
                 // ph is +-1: flip the sign bits of every register (integer pipe)
                 // instead of a complex multiply; pending unit factors commute
                 o("{ const unsigned pm = (unsigned)__double2hiint(ph.x) & 0x80000000u;\n");
                 for (int i = 0; i < NR(); ++i) o("v[%d] = mk(cneg(v[%d].x, pm), cneg(v[%d].y, pm));\n", i, i, i);
                 o("}\n");
-            } else if (t_phase) {  // ph (times F when due, times the pending slot constants) on every register
-                if (applyF) {
+            } else if (t_phase || applyF) {
+                // every register is multiplied anyway (ph and / or F): the
+                // pending per-slot phases hs (runtime) and constants (pd) ride
+                // on that multiply -- one per-thread scalar per pattern of
+                // pending slots a register lies in, one multiply per register
+                const bool rt = t_phase;  // runtime base (ph) or compile-time (F)
+                if (rt && applyF) {
                     o("ph = cm(%s, %s, ph);\n", lit(F.x).c_str(), lit(F.y).c_str());
                     F = make_double2(1.0, 0.0);
                 }
-                // one per-thread scalar per pattern of pending slots: ph * constant
-                std::vector<int> made(1u << NS(), 0);
+                std::vector<unsigned> made;  // patterns whose scalar exists
                 for (int i = 0; i < NR(); ++i) {
-                    const unsigned pat = t_pdm & unsigned(i);
+                    const unsigned hpat = t_hs & unsigned(i), ppat = t_pdm & unsigned(i);
+                    const double2 c = rt ? pd_of(i) : cmulh(F, pd_of(i));
+                    if (!rt && !hpat) {  // a compile-time constant
+                        o("{ const d2 X = v[%d]; v[%d] = %s; }\n", i, i, cm_fold(c, code[i]).c_str());
+                        code[i] = 0;
+                        continue;
+                    }
                     std::string var = "ph";
-                    if (pat) {
-                        var = "php" + std::to_string(pat);
-                        if (!made[pat]) {
-                            const double2 c = pd_of(i);
-                            o("const d2 %s = cm(%s, %s, ph);\n", var.c_str(), lit(c.x).c_str(), lit(c.y).c_str());
-                            made[pat] = 1;
+                    if (hpat || ppat || !rt) {
+                        const unsigned key = hpat | (ppat << NS());
+                        var = "fm" + std::to_string(key);
+                        if (std::find(made.begin(), made.end(), key) == made.end()) {
+                            made.push_back(key);
+                            // base (ph, or the constant F * pd), times hs of the
+                            // register's pending slots, times the constant pd
+                            const std::string acc = rt ? "ph" : "mk(" + lit(c.x) + ", " + lit(c.y) + ")";
+                            o("d2 %s = %s;\n", var.c_str(), acc.c_str());
+                            for (int k = 0; k < NS(); ++k)
+                                if ((hpat >> k) & 1) o("%s = cm(hs%d.x, hs%d.y, %s);\n", var.c_str(), k, k, var.c_str());
+                            if (rt && ppat)
+                                o("%s = cm(%s, %s, %s);\n", var.c_str(), lit(c.x).c_str(), lit(c.y).c_str(),
+                                  var.c_str());
                         }
                     }
                     std::string e = cm_ph(code[i]);
@@ -1430,14 +1443,11 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
                     o("{ const d2 X = v[%d]; v[%d] = %s; }\n", i, i, e.c_str());
                     code[i] = 0;
                 }
+                for (int k = 0; k < NS(); ++k)
+                    if ((t_hs >> k) & 1) o("hs%d = mk(1.0, 0.0);\n", k);
+                t_hs = 0;
                 t_pdm = 0;
-            } else if (applyF) {
-                for (int i = 0; i < NR(); ++i) {  // stored * F = true amplitude
-                    o("{ const d2 X = v[%d]; v[%d] = %s; }\n", i, i, cm_fold(cmulh(F, pd_of(i)), code[i]).c_str());
-                    code[i] = 0;
-                }
-                t_pdm = 0;
-                F = make_double2(1.0, 0.0);
+                if (applyF) F = make_double2(1.0, 0.0);
             } else if (t_pdm) {  // the pending slot constants alone, one multiply per register
                 for (int i = 0; i < NR(); ++i) {
                     if (!(t_pdm & unsigned(i))) continue;
