@@ -1249,6 +1249,24 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
         return v;
     };
     auto k_smem = [&](int k) { return (unsigned)(16 * swz_h(k * FTHREADS)); };
+    // Global addresses as base + constant.  The thread's offset r and a
+    // register's offset k_row(k) are XORs of different address bits, so
+    // r ^ k_row(k) == r + k_row(k): one 64-bit pointer per thread and the
+    // register part as the access's immediate offset (a per-access XOR costs
+    // five integer instructions of 64-bit address arithmetic; the heaviest
+    // configs[1] passes, whose bodies overflow the instruction cache, ran 13 %
+    // faster without them).
+    bool fill_add = true;
+    {
+        int64_t tm = colmask;
+        for (int j = P.flow; j < lt; ++j) tm |= row_off(j - P.flow);
+        for (int k = 0; k < NR(); ++k)
+            if (k_row(k) & tm) fill_add = false;
+    }
+    auto fill_ptr = [&]() { if (fill_add) o("const d2 *const pr = p + r;\n"); };
+    auto fill_src = [&](int k) {
+        return fill_add ? "pr + " + offl(k_row(k)) : "p + (r ^ " + offl(k_row(k)) + ")";
+    };
     if (ring) {
         // buffer byte offset bo (a multiple of 2^16) XORed into the shared
         // address, which stays a 32-bit shared-window offset
@@ -1256,13 +1274,15 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
         o("auto fill = [&](unsigned bo, const d2 *p) {\n%s", kOpaqueTid);
         thread_parts();
         o("s ^= bo;\n");
+        fill_ptr();
         for (int k = 0; k < NR(); ++k)
-            o("cpa_u(sbase + (s ^ %uu), p + (r ^ %s));\n", k_smem(k), offl(k_row(k)).c_str());
+            o("cpa_u(sbase + (s ^ %uu), %s);\n", k_smem(k), fill_src(k).c_str());
     } else {
         o("auto fill = [&](unsigned char *dstb, const d2 *p) {\n%s", kOpaqueTid);
         thread_parts();
+        fill_ptr();
         for (int k = 0; k < NR(); ++k)
-            o("cpa(dstb + (s ^ %uu), p + (r ^ %s));\n", k_smem(k), offl(k_row(k)).c_str());
+            o("cpa(dstb + (s ^ %uu), %s);\n", k_smem(k), fill_src(k).c_str());
     }
     if (ring)
         o("};\n(void)fill;\n");
@@ -1275,12 +1295,48 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
         for (int h = 0; h < 2; ++h) {
             o("auto fill%c = [&](const d2 *p) {\n%s", h ? 'B' : 'A', kOpaqueTid);
             thread_parts();
+            fill_ptr();
             for (int k = h * NR() / 2; k < (h + 1) * NR() / 2; ++k)
-                o("cpa(reinterpret_cast<unsigned char *>(dsm) + (s ^ %uu), p + (r ^ %s));\n",
-                  k_smem(k) + (h ? 0u : 0x10000u), offl(k_row(k)).c_str());
+                o("cpa(reinterpret_cast<unsigned char *>(dsm) + (s ^ %uu), %s);\n",
+                  k_smem(k) + (h ? 0u : 0x10000u), fill_src(k).c_str());
             o("asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\"); };\n");
         }
     }
+    // Direct HBM loads / stores of a group: address = pa + (x0 ^ combo(i)), x0
+    // the thread's XOR-linear offset, combo(i) the XOR of the slot terms of
+    // register i.  A slot term that shares no bit with any thread-varying
+    // term, the constant start or another slot term only ever adds to the
+    // address: those go into the access as a constant offset off a per-thread
+    // pointer; the others (a CNOT folded into the map, a pending swap) keep
+    // the XOR, one pointer per pattern of them.
+    auto direct_access = [&](const char *x0, int64_t b, const int64_t *t, const int64_t *sl, const uint64_t *pend,
+                             const std::function<void(int, const std::string &)> &emit) {
+        int64_t vary = b;
+        for (int j = 0; j < FTBITS; ++j) vary |= t[j];
+        for (int k = 0; k < NS(); ++k)
+            if (pend && pend[k]) vary |= sl[k];
+        unsigned xset = 0;  // slot bits that keep the XOR
+        for (int k = 0; k < NS(); ++k) {
+            int64_t others = vary;
+            for (int k2 = 0; k2 < NS(); ++k2)
+                if (k2 != k) others |= sl[k2];
+            if ((sl[k] & others) || (pend && pend[k])) xset |= 1u << k;
+        }
+        if (__builtin_popcount(xset) > 2) xset = (1u << NS()) - 1;  // too many pointers: plain XOR form
+        const bool all_xor = xset == (1u << NS()) - 1;
+        if (!all_xor)
+            for (int i = 0; i < NR(); ++i) {
+                if (unsigned(i) & ~xset) continue;  // i is a pattern of XOR slots only
+                o("d2 *const p%s_%d = pa + (%s ^ %s);\n", x0, i, x0, offl(xcombo_g(sl, i)).c_str());
+            }
+        for (int i = 0; i < NR(); ++i) {
+            if (all_xor) {
+                emit(i, std::string("pa + (") + x0 + " ^ " + offl(xcombo_g(sl, i)) + ")");
+            } else {
+                emit(i, std::string("p") + x0 + "_" + std::to_string(unsigned(i) & xset) + " + " + offl(xcombo_g(sl, unsigned(i) & ~xset)));
+            }
+        }
+    };
     const char *wait_all = "asm volatile(\"cp.async.wait_group 0;\\n\" ::: \"memory\");\n";
     const bool direct_first = P.direct_first && mode == 0;
     if (ring) {
@@ -1354,8 +1410,9 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             o("%s g0 = %s;\n", OFF, offl(P.gl_b).c_str());
             o.s += kOpaqueTid;
             for (int j = 0; j < FTBITS; ++j) o("if ((tg >> %d) & 1) g0 ^= %s;\n", j, offl(P.gl_t[j]).c_str());
-            for (int i = 0; i < NR(); ++i)
-                o("v[%d] = ldcs(pa + (g0 ^ %s));\n", i, offl(xcombo_g(P.gl_s, i)).c_str());
+            direct_access("g0", P.gl_b, P.gl_t, P.gl_s, nullptr, [&](int i, const std::string &adr) {
+                o("v[%d] = ldcs(%s);\n", i, adr.c_str());
+            });
         } else {
             o("unsigned a0 = %uu%s;\n", (unsigned)G.ld_b, ring ? " ^ bo" : "");
             o.s += kOpaqueTid;
@@ -1475,8 +1532,9 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             for (int k = 0; k < NS(); ++k)  // pending swaps: per-thread store address
                 if (pend[k]) o("if (%s) s0 ^= %s;\n", pcond(pend[k]).c_str(), offl(P.gs_s[k]).c_str());
             o("}\n");
-            for (int i = 0; i < NR(); ++i)
-                o("stcs(pa + (s0 ^ %s), v[%d]);\n", offl(xcombo_g(P.gs_s, i)).c_str(), i);
+            direct_access("s0", P.gs_b, P.gs_t, P.gs_s, pend, [&](int i, const std::string &adr) {
+                o("stcs(%s, v[%d]);\n", adr.c_str(), i);
+            });
         } else {
             // the store overwrites chunks other threads may not have loaded
             // yet (the swizzle changes per transition): order them with the
@@ -1505,8 +1563,12 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
     if (!P.direct_last) {
         o("{\n%s", kOpaqueTid);
         thread_parts();
+        if (fill_add) o("d2 *const pw = pa + r;\n");
         for (int k = 0; k < NR(); ++k)
-            o("pa[r ^ %s] = *reinterpret_cast<const d2 *>(sb + (s ^ %uu));\n", offl(k_row(k)).c_str(), k_smem(k));
+            if (fill_add)
+                o("pw[%s] = *reinterpret_cast<const d2 *>(sb + (s ^ %uu));\n", offl(k_row(k)).c_str(), k_smem(k));
+            else
+                o("pa[r ^ %s] = *reinterpret_cast<const d2 *>(sb + (s ^ %uu));\n", offl(k_row(k)).c_str(), k_smem(k));
         o("}\n");
     }
     // mode 0: the buffer must be free before the next tile's loads; modes 1/2
