@@ -1078,7 +1078,7 @@ def bench_main(args, clock_cls=None, peaks_fn=None) -> None:
                "h2d_bytes_per_step": world * slab_bytes, "d2h_bytes_per_step": world * slab_bytes,
                "api": "DistEngine.run on each rank's slab, pinned H2D + run + D2H per step", "steps": e2e_steps}
         del host
-    except RuntimeError as exc:  # pinned host memory exhausted
+    except Exception as exc:  # noqa: BLE001  (pinned host memory exhausted, ...)
         e2e = {"skipped": f"pinned host buffer of {slab_bytes} B per rank unavailable: {str(exc)[:120]}"}
 
     # reference-faithful mode: one exchange per global-target gate
@@ -1086,40 +1086,60 @@ def bench_main(args, clock_cls=None, peaks_fn=None) -> None:
     eng.close()  # partners unmap this slab before it is freed
     del eng
     torch.cuda.empty_cache()
-    faithful = None
-    if world > 1 and os.environ.get("SVB_BENCH_FAITHFUL", "1") != "0":
+    # (the sections below are reported next to the headline; a failure in one
+    # of them -- every rank runs the same code, so they fail together -- is
+    # recorded in the line instead of losing the measured headline)
+    def _section(fn):
+        try:
+            return fn()
+        except Exception as exc:  # noqa: BLE001
+            torch.cuda.empty_cache()
+            return {"error": f"{type(exc).__name__}: {str(exc)[:200]}"}
+
+    def _faithful():
         ref_eng = DistEngine(n, fma=fma, jit=jit, layout=False, elide_diagonal=False, peer=peer)
-        device_gaussian(ref_eng, 7, dev)
-        fr = _timed_runs(ref_eng, circ, 1, 1, dev)
-        faithful = {"mode": "exchange per global-target gate (diagonal ones too), identity layout",
+        try:
+            device_gaussian(ref_eng, 7, dev)
+            fr = _timed_runs(ref_eng, circ, 1, 1, dev)
+            return {"mode": "exchange per global-target gate (diagonal ones too), identity layout",
                     "value": round(nops / (fr["ms"] / 1e3), 1), "ms_per_step": round(fr["ms"], 3),
                     "exchanges_per_step": fr["exchanges"], "link": _link_summary(fr["log"], ceiling, dev)}
-        ref_eng.close()
-        del ref_eng
-        torch.cuda.empty_cache()
+        finally:
+            ref_eng.close()
+            del ref_eng
+            torch.cuda.empty_cache()
+
+    faithful = None
+    if world > 1 and os.environ.get("SVB_BENCH_FAITHFUL", "1") != "0":
+        faithful = _section(_faithful)
 
     cfg4 = None
     if (world == 8 or os.environ.get("SVB_BENCH_CFG4") == "1") and os.environ.get("SVB_BENCH_CFG4") != "0":
-        n4 = int(os.environ.get("SVB_BENCH_CFG4_N", "34"))
-        c4 = workloads.random_layer_circuit(n4, 50)
-        e4 = DistEngine(n4, fma=fma, jit=jit, layout=True, peer=peer)
-        r4 = _timed_runs(e4, c4, 1, 1, dev)
-        nrm = e4.norm2()
-        glob = sum(1 for op in c4.ops if op.control is not None
-                   and (op.target >= n4 - k or op.control >= n4 - k))
-        pairs = sum(1 for op in c4.ops if op.control is not None)
-        cfg4 = {"workload": f"random layer circuit n={n4}, 50 layers (BASELINE configs[4]), |0...0>",
-                "ops": len(c4.ops), "value": round(len(c4.ops) / (r4["ms"] / 1e3), 1),
-                "ms_per_step": round(r4["ms"], 3), "swaps_per_step": r4["swaps"],
-                "cnot_pairs_touching_global": round(glob / max(pairs, 1), 4),
-                "link": _link_summary(r4["log"], ceiling, dev), "norm_after": nrm}
-        e4.close()
-        del e4
-        torch.cuda.empty_cache()
+        def _cfg4():
+            n4 = int(os.environ.get("SVB_BENCH_CFG4_N", "34"))
+            c4 = workloads.random_layer_circuit(n4, 50)
+            e4 = DistEngine(n4, fma=fma, jit=jit, layout=True, peer=peer)
+            try:
+                r4 = _timed_runs(e4, c4, 1, 1, dev)
+                nrm = e4.norm2()
+                glob = sum(1 for op in c4.ops if op.control is not None
+                           and (op.target >= n4 - k or op.control >= n4 - k))
+                pairs = sum(1 for op in c4.ops if op.control is not None)
+                return {"workload": f"random layer circuit n={n4}, 50 layers (BASELINE configs[4]), |0...0>",
+                        "ops": len(c4.ops), "value": round(len(c4.ops) / (r4["ms"] / 1e3), 1),
+                        "ms_per_step": round(r4["ms"], 3), "swaps_per_step": r4["swaps"],
+                        "cnot_pairs_touching_global": round(glob / max(pairs, 1), 4),
+                        "link": _link_summary(r4["log"], ceiling, dev), "norm_after": nrm}
+            finally:
+                e4.close()
+                del e4
+                torch.cuda.empty_cache()
+
+        cfg4 = _section(_cfg4)
 
     transport = None
     if world > 1:
-        transport = (_transport_check(dev, world) if backend == "nccl" else
+        transport = (_section(lambda: _transport_check(dev, world)) if backend == "nccl" else
                      {"skipped": "send/recv of CUDA tensors needs NCCL (this run's control plane is gloo)"})
 
     if rank == 0:
