@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <vector>
 
 #define CK(x)                                                                          \
@@ -63,13 +64,24 @@ int main(int argc, char **argv) {
     int grid = (int)(cps * sms + 0.5);
     if (grid > ntiles) grid = (int)ntiles;
     void *args[] = {&a, &ntiles};
+    CUdeviceptr ctr = 0;  // dynamic tile scheduling variants (tools/dyn_patch.py): zeroed before every launch
+    {
+        size_t cb = 0;
+        if (cuModuleGetGlobal(&ctr, &cb, mod, "g_ctr") != CUDA_SUCCESS) ctr = 0;
+    }
     CUevent e0, e1;
     CK(cuEventCreate(&e0, 0));
     CK(cuEventCreate(&e1, 0));
-    for (int i = 0; i < 3; ++i) CK(cuLaunchKernel(fn, grid, 1, 1, threads, 1, 1, smem, 0, args, nullptr));
+    for (int i = 0; i < 3; ++i) {
+        if (ctr) CK(cuMemsetD32Async(ctr, 0, 1, 0));
+        CK(cuLaunchKernel(fn, grid, 1, 1, threads, 1, 1, smem, 0, args, nullptr));
+    }
     CK(cuCtxSynchronize());
     CK(cuEventRecord(e0, 0));
-    for (int i = 0; i < reps; ++i) CK(cuLaunchKernel(fn, grid, 1, 1, threads, 1, 1, smem, 0, args, nullptr));
+    for (int i = 0; i < reps; ++i) {
+        if (ctr) CK(cuMemsetD32Async(ctr, 0, 1, 0));
+        CK(cuLaunchKernel(fn, grid, 1, 1, threads, 1, 1, smem, 0, args, nullptr));
+    }
     CK(cuEventRecord(e1, 0));
     CK(cuCtxSynchronize());
     float ms = 0;
@@ -90,6 +102,25 @@ int main(int argc, char **argv) {
             for (int q = 0; q < 64; ++q)
                 if (acc[q]) printf(" %d:%.0f", q, double(acc[q]) / per);
             printf("\n");
+        }
+    }
+    {
+        // per-CTA timeline of an instrumented variant (tools/trace_patch.py), last launch
+        CUdeviceptr g;
+        size_t gb = 0;
+        if (cuModuleGetGlobal(&g, &gb, mod, "g_trace") == CUDA_SUCCESS) {
+            std::vector<long long> tr(gb / 8);
+            CK(cuMemcpyDtoH(tr.data(), g, gb));
+            for (int sm = 0; sm < 4; ++sm) {
+                const long long t0 = std::min(tr[((sm * 2 + 0) * 2 + 0) * 64], tr[((sm * 2 + 1) * 2 + 0) * 64]);
+                for (int slot = 0; slot < 2; ++slot) {
+                    printf("  SM %d CTA %d tile starts (cycles):", sm, slot);
+                    for (int it = 0; it < 24; ++it) printf(" %lld", tr[((sm * 2 + slot) * 2 + 0) * 64 + it] - t0);
+                    printf("\n  SM %d CTA %d last-group starts:    ", sm, slot);
+                    for (int it = 0; it < 24; ++it) printf(" %lld", tr[((sm * 2 + slot) * 2 + 1) * 64 + it] - t0);
+                    printf("\n");
+                }
+            }
         }
     }
     return 0;
