@@ -25,6 +25,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <atomic>
 #include <cstdarg>
@@ -1138,6 +1139,86 @@ size_t jit_dyn_smem(const FPass &P) {
 // the tile loop and kept live (or spilled) across the gate arithmetic.
 const char *kOpaqueTid = "unsigned tg = tid; asm volatile(\"\" : \"+r\"(tg));\n";
 
+// SVB_JIT_RESWZ=0 keeps the planner's swizzles (measurement)
+bool t_reswz_on() {
+    static const bool on = [] {
+        const char *e = getenv("SVB_JIT_RESWZ");
+        return !e || atoi(e) != 0;
+    }();
+    return on;
+}
+
+// Re-search the swizzle of the transition A -> B (fused.cu, "Shared-memory
+// swizzle per transition": an XOR-linear map h of a local index's bits >= 3
+// into its 16 B chunk number) when A's pending swaps `pend` make its store
+// phases conflict: lane bit j of the store carries A's thread term j plus the
+// slot term of every pending swap whose condition contains thread bit j.
+void reswizzle(FGroup &A, FGroup &B, const uint64_t *pend, int fm, int tbits) {
+    const int fs = NS();
+    auto ways3 = [](int a, int b, int c) {
+        int seen[8] = {0}, w = 0;
+        for (int l = 0; l < 8; ++l) w = std::max(w, ++seen[((l & 1) ? a : 0) ^ ((l & 2) ? b : 0) ^ ((l & 4) ? c : 0)]);
+        return w;
+    };
+    auto chunk = [](uint32_t off) { return int(off >> 4) & 7; };
+    bool lane_pend = false;
+    int eff[3];
+    for (int j = 0; j < 3; ++j) {
+        eff[j] = chunk(A.st_t[j]);
+        for (int k = 0; k < fs; ++k)
+            if ((pend[k] >> j) & 1) {
+                eff[j] ^= chunk(A.st_s[k]);
+                lane_pend = true;
+            }
+    }
+    if (!lane_pend || ways3(eff[0], eff[1], eff[2]) <= 1) return;
+    typedef std::array<int, FMMAX> Hmap;
+    auto bank = [&](int v, const Hmap &h) {
+        int c = v & 7;
+        for (int j = 3; j < fm; ++j)
+            if ((v >> j) & 1) c ^= h[j];
+        return c;
+    };
+    auto cost = [&](const Hmap &h) {
+        int e[3];
+        for (int j = 0; j < 3; ++j) {
+            e[j] = bank(A.mcol[A.tmap[j]], h);
+            for (int k = 0; k < fs; ++k)
+                if ((pend[k] >> j) & 1) e[j] ^= bank(A.mcol[A.pos[k]], h);
+        }
+        return ways3(e[0], e[1], e[2]) +
+               ways3(bank(B.qcol[B.tmap[0]], h), bank(B.qcol[B.tmap[1]], h), bank(B.qcol[B.tmap[2]], h));
+    };
+    Hmap best{};
+    int bc = 1 << 30;
+    uint32_t rng = 0x2545f491u;
+    for (int tries = 0; tries < 2000 && bc > 2; ++tries) {
+        Hmap h{};
+        for (int j = 3; j < fm; ++j) {
+            rng = rng * 1664525u + 1013904223u;
+            h[j] = (rng >> 29) & 7;
+        }
+        const int c = cost(h);
+        if (c < bc) {
+            bc = c;
+            best = h;
+        }
+    }
+    // the swizzle in force costs ways(eff) + 1 at best; keep it unless the search found better
+    if (bc >= ways3(eff[0], eff[1], eff[2]) + 1) return;
+    auto off = [&](int v) { return (uint32_t)(16 * ((v & ~7) | bank(v, best))); };
+    for (int j = 0; j < tbits; ++j) {
+        A.st_t[j] = off(A.mcol[A.tmap[j]]);
+        B.ld_t[j] = off(B.qcol[B.tmap[j]]);
+    }
+    for (int k = 0; k < fs; ++k) {
+        A.st_s[k] = off(A.mcol[A.pos[k]]);
+        B.ld_s[k] = off(B.qcol[B.pos[k]]);
+    }
+    A.st_b = off(A.mb);
+    B.ld_b = off(B.qb);
+}
+
 // Overlap between a group's shared-memory stores and other threads' loads
 // of the same group: 0 none (each thread rewrites only chunks it read), 1
 // within warps only, 2 across warps.  Pending swaps only exchange a thread's
@@ -1391,19 +1472,21 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
         o("unsigned char *sb = reinterpret_cast<unsigned char *>(buf);\n");
     }
     o("d2 v[%d];\n", NR());
+    // (the groups' shared-memory maps may be re-swizzled below: a local copy)
+    std::vector<FGroup> GR(P.groups, P.groups + P.ngroups);
     for (int gi = 0; gi < P.ngroups; ++gi) {
         FGroup Gx;
         if (split && gi == 0) {
             // first group: bytes [0, 32K) of the tile sit in F at +64K.  The
             // map o -> o ^ L(o) ^ K (L: byte bit 15 -> bit 16, K = 64K) is
             // affine, so every XOR term c becomes c ^ L(c), the base also ^ K
-            Gx = P.groups[0];
+            Gx = GR[0];
             auto L = [](uint32_t c) { return c ^ (((c >> 15) & 1u) << 16); };
             Gx.ld_b = L(Gx.ld_b) ^ 0x10000u;
             for (int j = 0; j < FTBMAX; ++j) Gx.ld_t[j] = L(Gx.ld_t[j]);
             for (int k = 0; k < FSMAX; ++k) Gx.ld_s[k] = L(Gx.ld_s[k]);
         }
-        const FGroup &G = (split && gi == 0) ? Gx : P.groups[gi];
+        const FGroup &G = (split && gi == 0) ? Gx : GR[gi];
         const bool last_group = gi == P.ngroups - 1;
         o("{ // group %d\n", gi);
         if (gi == 0 && direct_first) {
@@ -1539,6 +1622,15 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             // the store overwrites chunks other threads may not have loaded
             // yet (the swizzle changes per transition): order them with the
             // narrowest barrier that covers every overlap
+            // A pending swap conditioned on lane bits 0-2 XORs its slot's
+            // store term into some lanes' addresses, chunk bits included: the
+            // 8-lane phases the planner made conflict-free (it cannot know
+            // the pending swaps) may then hit a bank group twice.  configs[1]:
+            // 63 of 355 store phases ran 2-way conflicts (ncu: every STS of
+            // such a phase at twice its wavefronts).  Search this
+            // transition's swizzle again with the lanes' real XOR terms and
+            // move this group's store map and the next group's load map to it.
+            if (t_reswz_on() && !(split && gi == 0)) reswizzle(GR[gi], GR[gi + 1], pend, P.fm, FTBITS);
             const int hz = (gi == 0 && direct_first) ? 0 : store_hazard(G, FTHREADS, FTBITS);
             if (G.perm)
                 o("%s\n", SYNC.c_str());
