@@ -908,7 +908,8 @@ def _link_summary(log, ceiling: dict | None, dev) -> dict:
     return out
 
 
-def _timed_runs(eng: "DistEngine", circuit: Circuit, steps: int, warmup: int, dev, clock=None) -> dict:
+def _timed_runs(eng: "DistEngine", circuit: Circuit, steps: int, warmup: int, dev, clock=None,
+                settle: bool = False) -> dict:
     """W untimed runs, then K timed runs of `circuit` on the current state
     (no reset: every step applies the circuit once more), bracketed by a
     barrier + device synchronize; slowest rank's CUDA-event time."""
@@ -920,6 +921,19 @@ def _timed_runs(eng: "DistEngine", circuit: Circuit, steps: int, warmup: int, de
 
     for _ in range(max(warmup, 0)):
         eng.run(circuit)
+    # Layout mode keeps the qubit layout a run ends in, so the next run's local
+    # segments are new circuits in physical qubits (new plans, new NVRTC
+    # compiles) until the layout sequence closes its cycle (QFT: period 2).
+    # Further untimed runs until one compiles nothing on any rank (even count,
+    # bounded), so the timed region measures the engine and not the compiler.
+    settle_runs = 0
+    while settle and settle_runs < 8:
+        c0 = _lib.jit_counters()[1]
+        eng.run(circuit)
+        eng.compute.synchronize()
+        settle_runs += 1
+        if _allmax(float(_lib.jit_counters()[1] - c0), dev) == 0:
+            break
     launches0 = _lib.launch_count()
     st0 = (eng.stats.exchanges, eng.stats.swaps, eng.stats.bytes_sent)
     eng.link_log = []
@@ -936,7 +950,7 @@ def _timed_runs(eng: "DistEngine", circuit: Circuit, steps: int, warmup: int, de
     eng.dist.barrier(group=eng.group)
     ms = _allmax(e0.elapsed_time(e1), dev)
     log, eng.link_log = eng.link_log, None
-    return {"ms": ms, "launches": _lib.launch_count() - launches0, "log": log, "clk": clk,
+    return {"ms": ms, "launches": _lib.launch_count() - launches0, "log": log, "clk": clk, "settle_runs": settle_runs,
             "exchanges": (eng.stats.exchanges - st0[0]) / max(steps, 1),
             "swaps": (eng.stats.swaps - st0[1]) / max(steps, 1),
             "bytes_sent": (eng.stats.bytes_sent - st0[2]) / max(steps, 1)}
@@ -1052,7 +1066,7 @@ def bench_main(args, clock_cls=None, peaks_fn=None) -> None:
     ceiling = link_ceiling(eng, 1 << 30, dev)
     device_gaussian(eng, 7, dev)
     sampler = clock_cls(local) if (clock_cls and rank == 0) else None
-    main = _timed_runs(eng, circ, args.steps, args.warmup, dev, sampler)
+    main = _timed_runs(eng, circ, args.steps, args.warmup, dev, sampler, settle=True)
     link = _link_summary(main["log"], ceiling, dev)
     checks = _qft_checks(eng, circ, dev)
 
@@ -1120,7 +1134,15 @@ def bench_main(args, clock_cls=None, peaks_fn=None) -> None:
             c4 = workloads.random_layer_circuit(n4, 50)
             e4 = DistEngine(n4, fma=fma, jit=jit, layout=True, peer=peer)
             try:
-                r4 = _timed_runs(e4, c4, 1, 1, dev)
+                # one untimed run from |0...0> compiles the circuit's passes;
+                # the timed run starts from the same state and layout (the
+                # identity), so it meets the same local segments, cached
+                e4.run(c4)
+                e4.canonical()
+                e4.slab.zero_()
+                if e4.rank == 0:
+                    e4.slab[0] = 1.0
+                r4 = _timed_runs(e4, c4, 1, 0, dev)
                 nrm = e4.norm2()
                 glob = sum(1 for op in c4.ops if op.control is not None
                            and (op.target >= n4 - k or op.control >= n4 - k))
@@ -1128,6 +1150,7 @@ def bench_main(args, clock_cls=None, peaks_fn=None) -> None:
                 return {"workload": f"random layer circuit n={n4}, 50 layers (BASELINE configs[4]), |0...0>",
                         "ops": len(c4.ops), "value": round(len(c4.ops) / (r4["ms"] / 1e3), 1),
                         "ms_per_step": round(r4["ms"], 3), "swaps_per_step": r4["swaps"],
+                        "step": "one run from |0...0> in the identity layout, plans cached by an untimed run before",
                         "cnot_pairs_touching_global": round(glob / max(pairs, 1), 4),
                         "link": _link_summary(r4["log"], ceiling, dev), "norm_after": nrm}
             finally:
@@ -1159,6 +1182,7 @@ def bench_main(args, clock_cls=None, peaks_fn=None) -> None:
             "transport": ("peer memory (CUDA IPC), device-side pairwise sync" if peer else
                           "NCCL send/recv, chunk-pipelined"),
             "exchanges_per_step": main["exchanges"], "layout_swaps_per_step": main["swaps"],
+            "settle_runs": main["settle_runs"],
             "nvlink": link, "link_ceiling": ceiling,
             "gpu_launches": main["launches"],
             "e2e": e2e, "check": checks,
