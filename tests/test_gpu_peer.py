@@ -41,3 +41,6 @@ def test_multi_gpu_bench_path_smoke(cuda_ok):
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["check"]["pass"], line["check"]
     assert line["nvlink"]["global_ops"] > 0 and line["reference_faithful"]["exchanges_per_step"] > 0
     assert abs(line["configs4"]["norm_after"] - 1.0) < 1e-12
+    # the timed regions run on cached plans: settle runs after the warm-ups
+    # (layout mode), configs[4] from |0...0> after an untimed run of the same kind
+    assert 1 <= line["settle_runs"] <= 8 and "identity layout" in line["configs4"]["step"]
