@@ -44,6 +44,12 @@ int main(int argc, char **argv) {
     CUcontext ctx;
     CK(cuDevicePrimaryCtxRetain(&ctx, dev));
     CK(cuCtxSetCurrent(ctx));
+    if (const char *g = getenv("PASSRUN_L2_FETCH")) {  // experiment: L2 fetch granularity (32 / 64 / 128 B)
+        CK(cuCtxSetLimit(CU_LIMIT_MAX_L2_FETCH_GRANULARITY, (size_t)atoi(g)));
+        size_t v = 0;
+        cuCtxGetLimit(&v, CU_LIMIT_MAX_L2_FETCH_GRANULARITY);
+        fprintf(stderr, "L2 fetch granularity %zu\n", v);
+    }
     int sms = 0;
     CK(cuDeviceGetAttribute(&sms, CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT, dev));
     CUmodule mod;
