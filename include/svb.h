@@ -94,6 +94,14 @@ int svb_apply_c1q(void *amps, int64_t n_amps, const double q[8], int control, in
 int svb_run_ops(void *amps, int64_t n_amps, const svb_op *ops, int nops, unsigned flags,
                 void *stream);
 
+/* Number of trailing ops (a multiple of 3, 0 if none) that form a SWAP network
+ * of CNOT triples -- pairwise disjoint, each of the five lowest qubits swapped
+ * with a higher one: the QFT's final qubit reversal (workloads.qft_circuit;
+ * reference form core.py SWAP = 3 CNOTs) -- which svb_run_ops applies in one
+ * in-place HBM pass (k_swap_bits) after the fused passes of the ops before it.
+ * Host only. */
+int svb_swap_suffix(int n_qubits, const svb_op *ops, int nops);
+
 /* Number of HBM passes svb_run_ops would make for these ops, and (groups,
  * may be NULL) the total shared-memory register groups of the fused passes.
  * Planner only, no device work. */

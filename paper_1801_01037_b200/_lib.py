@@ -62,6 +62,7 @@ _SIGS = {
     "svb_run_ops": ([_vp, _i64, ctypes.POINTER(SvbOp), _int, ctypes.c_uint, _vp], _int),
     "svb_plan_passes": ([_int, ctypes.POINTER(SvbOp), _int, ctypes.c_uint, ctypes.POINTER(_int),
                          ctypes.POINTER(_int)], _int),
+    "svb_swap_suffix": ([_int, ctypes.POINTER(SvbOp), _int], _int),
     "svb_jit_check": ([_int, ctypes.POINTER(SvbOp), _int, ctypes.c_uint, ctypes.POINTER(_int)], _int),
     "svb_jit_counters": ([ctypes.POINTER(ctypes.c_long), ctypes.POINTER(ctypes.c_long)], None),
     "svb_jit_wait": ([], None),

@@ -46,6 +46,8 @@ int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsi
                    cudaStream_t s, int64_t *launches);
 int plan_passes(int n, const svb_op *ops, int nops, unsigned flags, int *groups);
 int jit_check(int n, const svb_op *ops, int nops, unsigned flags);
+struct SwapNet;
+int swap_suffix(int n, const svb_op *ops, int nops, SwapNet *out);
 
 static thread_local char g_err[512];
 std::atomic<int64_t> g_launches{0};
@@ -337,6 +339,11 @@ int svb_jit_check(int n_qubits, const svb_op *ops, int nops, unsigned flags, int
     if (c < 0) return SVB_ESTATE;
     *compiled = c;
     return SVB_OK;
+}
+
+int svb_swap_suffix(int n_qubits, const svb_op *ops, int nops) {
+    if (n_qubits < 1 || n_qubits > 62 || check_ops(n_qubits, ops, nops) != SVB_OK) return 0;
+    return swap_suffix(n_qubits, ops, nops, nullptr);
 }
 
 int svb_plan_passes(int n_qubits, const svb_op *ops, int nops, unsigned flags, int *passes,
@@ -903,7 +910,8 @@ int svb_profile_read(int cls, int64_t *launches, double *total_ms, int64_t *alg_
 
 const char *svb_profile_class_name(int cls) {
     static const char *names[PROF_NCLASSES] = {"k_pair_high", "k_pair_low", "k_diag", "k_tiny", "k_fused",
-                                               "k_exchange", "k_norm", "kpass_jit", "k_dense", "k_signal"};
+                                               "k_exchange", "k_norm", "kpass_jit", "k_dense", "k_signal",
+                                               "k_swap_bits"};
     return (cls >= 0 && cls < PROF_NCLASSES) ? names[cls] : "";
 }
 

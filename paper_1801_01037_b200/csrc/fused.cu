@@ -1733,7 +1733,135 @@ static void lower_plan(int n, const svb_op *ops, int nops, bool strict, bool reg
 }
 
 // host-only: plan, lower and NVRTC-compile every fused pass (no device work)
+// ---------------------------------------------------------------------------
+// Trailing SWAP network in one HBM pass.
+//
+// A circuit that ends in SWAPs written as CNOT triples (the reference's form:
+// the QFT's final qubit reversal, core.py / workloads.qft_circuit) permutes
+// the bits of every amplitude index.  Through fused passes that costs one
+// pass per ~4-6 swaps (both qubits of a swap must share a 12-qubit tile that
+// also holds physical bits 0-2): QFT-30 spent 3 of its 7 passes moving data
+// for the reversal.  When the swaps are pairwise disjoint and each of the K
+// lowest qubits is swapped with a qubit >= K, the whole network is done in
+// place in ONE pass: split the index into the low block A (bits 0..K-1), its
+// partners B and the rest R; the network maps tile r (all 2^K x 2^K
+// combinations of A and B bits) to the transposed tile at sigma_R(r).  A CTA
+// loads tile r and its partner tile into shared memory as 2^K rows of 2^K
+// contiguous amplitudes (512 B at K = 5) and stores each transposed into the
+// other's place.  Pure data movement: bit-identical to applying the CNOTs.
+struct SwapNet {
+    int n, nrest, npairs;
+    int8_t hi[8];         // partner (>= K) of low qubit i
+    int8_t rest[64];      // qubits outside A and B, ascending = bit j of the tile index
+    int8_t pu[32], pv[32];  // swaps inside R, as tile-index bit positions
+};
+constexpr int SWAPNET_K = 5;
+
+__global__ void __launch_bounds__(256) k_swap_bits(double2 *__restrict__ a, SwapNet w) {
+    constexpr int K = SWAPNET_K, T = 1 << K;
+    __shared__ double2 s1[T][T + 1], s2[T][T + 1];  // [B value][A value], padded: transposed reads hit 8 bank groups
+    const int64_t ntiles = int64_t(1) << w.nrest;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int64_t tp = t;
+        for (int j = 0; j < w.npairs; ++j)
+            if (((t >> w.pu[j]) ^ (t >> w.pv[j])) & 1) tp ^= (int64_t(1) << w.pu[j]) | (int64_t(1) << w.pv[j]);
+        if (tp < t) continue;  // a pair of tiles is exchanged at its lower index
+        int64_t base = 0, basep = 0;
+        for (int j = 0; j < w.nrest; ++j) {
+            base |= ((t >> j) & 1) << w.rest[j];
+            basep |= ((tp >> j) & 1) << w.rest[j];
+        }
+        int64_t yo[(T * T) / 256];
+#pragma unroll
+        for (int r = 0; r < (T * T) / 256; ++r) {
+            const int y = (threadIdx.x + r * 256) >> K;
+            int64_t o = 0;
+#pragma unroll
+            for (int i = 0; i < K; ++i) o |= int64_t((y >> i) & 1) << w.hi[i];
+            yo[r] = o;
+        }
+#pragma unroll
+        for (int r = 0; r < (T * T) / 256; ++r) {
+            const int e = threadIdx.x + r * 256, x = e & (T - 1), y = e >> K;
+            s1[y][x] = a[base + yo[r] + x];
+            if (tp != t) s2[y][x] = a[basep + yo[r] + x];
+        }
+        __syncthreads();
+        // the amplitude the network puts at (A = x, B = y) of tile tp comes from (A = y, B = x) of tile t
+#pragma unroll
+        for (int r = 0; r < (T * T) / 256; ++r) {
+            const int e = threadIdx.x + r * 256, x = e & (T - 1), y = e >> K;
+            a[basep + yo[r] + x] = s1[x][y];
+            if (tp != t) a[base + yo[r] + x] = s2[x][y];
+        }
+        __syncthreads();
+    }
+}
+
+static bool swapnet_on() {
+    static const bool on = [] {
+        const char *e = getenv("SVB_FUSE_SWAPNET");
+        return !e || atoi(e) != 0;
+    }();
+    return on;
+}
+
+// Length (in ops, a multiple of 3) of the trailing SWAP network that
+// k_swap_bits applies, 0 if the ops do not end in one that qualifies.
+int swap_suffix(int n, const svb_op *ops, int nops, SwapNet *out) {
+    constexpr int K = SWAPNET_K;
+    if (!swapnet_on() || n < 2 * K + 2 || n > 62) return 0;
+    auto is_cx = [&](const svb_op &o, int c, int t) {
+        static const double X[8] = {0, 0, 1, 0, 1, 0, 0, 0};
+        return o.kind == 1 && o.control == c && o.target == t && memcmp(o.q, X, sizeof X) == 0;
+    };
+    int sigma[64];
+    for (int q = 0; q < n; ++q) sigma[q] = q;
+    int i = nops, swaps = 0;
+    while (i >= 3) {
+        const svb_op &o = ops[i - 1];
+        if (o.kind != 1) break;
+        const int c = o.control, t = o.target;
+        if (c == t || c < 0 || t < 0 || c >= n || t >= n) break;
+        if (!is_cx(ops[i - 1], c, t) || !is_cx(ops[i - 2], t, c) || !is_cx(ops[i - 3], c, t)) break;
+        if (sigma[c] != c || sigma[t] != t) break;  // not disjoint from the swaps taken so far
+        sigma[c] = t;
+        sigma[t] = c;
+        i -= 3;
+        ++swaps;
+    }
+    // worth a dedicated pass only for a network (a few swaps relabel for free inside fused passes)
+    if (swaps < 3) return 0;
+    for (int q = 0; q < K; ++q)
+        if (sigma[q] < K) return 0;  // the low block must move out whole
+    if (out) {
+        SwapNet &w = *out;
+        memset(&w, 0, sizeof w);
+        w.n = n;
+        bool in_b[64] = {false};
+        for (int q = 0; q < K; ++q) {
+            w.hi[q] = (int8_t)sigma[q];
+            in_b[sigma[q]] = true;
+        }
+        int pos[64];
+        for (int q = K; q < n; ++q)
+            if (!in_b[q]) {
+                pos[q] = w.nrest;
+                w.rest[w.nrest++] = (int8_t)q;
+            }
+        for (int q = K; q < n; ++q)
+            if (!in_b[q] && sigma[q] > q) {
+                if (w.npairs >= 32) return 0;
+                w.pu[w.npairs] = (int8_t)pos[q];
+                w.pv[w.npairs] = (int8_t)pos[sigma[q]];
+                ++w.npairs;
+            }
+    }
+    return nops - i;
+}
+
 int jit_check(int n, const svb_op *ops, int nops, unsigned flags) {
+    if (fuse_enabled(n, flags | SVB_RUN_FUSE)) nops -= swap_suffix(n, ops, nops, nullptr);  // (k_swap_bits runs the rest)
     const bool strict = flags & SVB_RUN_STRICT_ORDER;
     std::vector<FPass> passes;
     std::vector<PlanStep> steps;
@@ -1749,6 +1877,8 @@ int jit_check(int n, const svb_op *ops, int nops, unsigned flags) {
 int plan_passes(int n, const svb_op *ops, int nops, unsigned flags, int *groups) {
     if (groups) *groups = 0;
     if (!fuse_enabled(n, flags)) return nops;
+    const int tail = swap_suffix(n, ops, nops, nullptr);  // one k_swap_bits pass
+    if (tail) return plan_passes(n, ops, nops - tail, flags, groups) + 1;
     const bool strict = flags & SVB_RUN_STRICT_ORDER;
     const int fm = plan_fm(n, flags);
     std::vector<FPass> passes;
@@ -1958,6 +2088,27 @@ int run_ops_device(double2 *a, int64_t n_amps, const svb_op *ops, int nops, unsi
     };
     if (!fuse_enabled(n, flags)) {
         for (int i = 0; i < nops; ++i) single(ops[i]);
+        return SVB_OK;
+    }
+    SwapNet net;
+    const int tail = swap_suffix(n, ops, nops, &net);
+    if (tail) {
+        // the ops before the network through the usual plan, then the network in one pass
+        int r = nops > tail ? run_ops_device(a, n_amps, ops, nops - tail, flags, s, launches) : SVB_OK;
+        if (r != SVB_OK) return r;
+        static const int sms = [] {
+            int d = 0, v = 148;
+            cudaGetDevice(&d);
+            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+            return v;
+        }();
+        const int64_t ntiles = int64_t(1) << net.nrest;
+        prof_begin(s);
+        k_swap_bits<<<(unsigned)std::min<int64_t>(ntiles, int64_t(sms) * 6), 256, 0, s>>>(a, net);
+        prof_end(s, LaunchInfo{1, PROF_SWAPNET, n_amps * 32});
+        *launches += 1;
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_status(e, "k_swap_bits launch");
         return SVB_OK;
     }
     {  // the dynamic shared-memory opt-in is per device: set it for each device used

@@ -171,7 +171,8 @@ enum ProfClass : int {
     PROF_FUSED_JIT = 7,  // kpass: NVRTC-specialised fused pass (jit.cu)
     PROF_DENSE = 8,      // k_dense_embed / k_dense_matvec (dense verifier)
     PROF_SYNC = 9,       // k_signal: pairwise rank sync of the peer transport
-    PROF_NCLASSES = 10
+    PROF_SWAPNET = 10,   // k_swap_bits: a trailing SWAP network in one pass (fused.cu)
+    PROF_NCLASSES = 11
 };
 struct LaunchInfo {
     int kernels;
