@@ -78,6 +78,13 @@ struct ConstPool {
 };
 thread_local ConstPool *t_pool = nullptr;
 
+// a run of values at consecutive slots (tables indexed at run time): not interned
+int pool_block(const std::vector<double> &v) {
+    const int start = (int)t_pool->vals.size();
+    t_pool->vals.insert(t_pool->vals.end(), v.begin(), v.end());
+    return start;
+}
+
 std::string lit(double x) {
     if (!t_pool) return hexf(x);
     uint64_t bits;
@@ -848,9 +855,118 @@ thread_local bool t_phase_sign = false;  // ... and it is only a sign, +-1
 int phase_mode() { return 7; }  // bits: 1 thread targets, 2 tile targets, 4 controlled
 
 // ph *= (target bit ? d1 : d0), under the (thread / tile) control if any
+// Tile-uniform phase factors of a group, merged.  A controlled phase whose
+// phase-carrying bit is a tile bit (a qubit outside the tile) multiplies ph by
+// a value every thread of the tile computes alike; the QFT's passes carry
+// chains of ~18 of them per thread-bit qubit (a complex multiply and two
+// selects each: 100 in QFT-30's first pass, a fifth of its instructions).
+// They all commute with everything until ph is applied at the group's end,
+// so they are collected per thread condition and emitted there as products
+// looked up in small tables: up to five tile bits index a 32-entry table of
+// precomputed products in the constant bank (a uniform load), one complex
+// multiply per table instead of one per gate.  SVB_JIT_TPH=0 keeps one
+// multiply per gate (measurement).
+struct TilePhase {
+    uint32_t mask;  // tile-index bits that must all be set
+    int cond;       // thread bit that must be set too, -1: none
+    double2 d;
+};
+thread_local std::vector<TilePhase> *t_tph = nullptr;
+
+bool tph_on() {
+    static const bool on = [] {
+        const char *e = getenv("SVB_JIT_TPH");
+        return !e || atoi(e) != 0;
+    }();
+    return on;
+}
+
+void flush_tile_phases(Out &o) {
+    if (!t_tph || t_tph->empty()) return;
+    std::vector<int> conds;
+    for (const TilePhase &f : *t_tph)
+        if (std::find(conds.begin(), conds.end(), f.cond) == conds.end()) conds.push_back(f.cond);
+    for (int c : conds) {
+        std::vector<TilePhase> fs;
+        for (const TilePhase &f : *t_tph)
+            if (f.cond == c) fs.push_back(f);
+        std::vector<char> done(fs.size(), 0);
+        for (size_t i = 0; i < fs.size(); ++i) {
+            if (done[i]) continue;
+            // grow a chunk of at most five tile bits from the unplaced factors, in order
+            uint32_t bits = 0;
+            std::vector<size_t> in;
+            for (size_t j = i; j < fs.size(); ++j) {
+                if (done[j]) continue;
+                if (__builtin_popcount(bits | fs[j].mask) > 5) continue;
+                bits |= fs[j].mask;
+                in.push_back(j);
+                done[j] = 1;
+            }
+            std::vector<int> pos;
+            for (int b = 0; b < 32; ++b)
+                if ((bits >> b) & 1) pos.push_back(b);
+            const int nb = (int)pos.size();
+            std::vector<double> tab;
+            for (int ix = 0; ix < (1 << nb); ++ix) {
+                uint32_t set = 0;
+                for (int k = 0; k < nb; ++k)
+                    if ((ix >> k) & 1) set |= 1u << pos[k];
+                double2 v = make_double2(1.0, 0.0);
+                for (size_t j : in)
+                    if ((fs[j].mask & set) == fs[j].mask) v = cmulh(v, fs[j].d);
+                tab.push_back(v.x);
+                tab.push_back(v.y);
+            }
+            const int start = pool_block(tab);
+            o("{ const unsigned ix = 0u");
+            for (int k = 0; k < nb; ++k) o(" | (((unsigned)(tix >> %d) & 1u) << %d)", pos[k], k);
+            o(";\n");
+            if (c < 0)
+                o("ph = cm(kc[%d + 2 * ix], kc[%d + 2 * ix], ph);\n", start, start + 1);
+            else  // branch-free, like emit_phase
+                o("{ const bool b = %s; ph = cm(b ? kc[%d + 2 * ix] : 1.0, b ? kc[%d + 2 * ix] : 0.0, ph); }\n",
+                  pbit(c).c_str(), start, start + 1);
+            o("}\n");
+        }
+    }
+    t_tph->clear();
+}
+
 void emit_phase(Out &o, const FGate &g) {
     const double2 d0 = g.m[0], d1 = g.m[3];
     const bool one0 = unit_code(d0) == 0;
+    if (t_tph && t_pool && one0 && tph_on()) {
+        // phase d1 where every bit of the gate is set; at least one of them a tile bit
+        const bool tt = g.tl >= FTILEBIT, ct = g.cl >= FTILEBIT;
+        TilePhase f;
+        f.d = d1;
+        f.mask = 0;
+        f.cond = -1;
+        bool ok = false;
+        if (tt && g.tl - FTILEBIT < 32) {
+            f.mask = 1u << (g.tl - FTILEBIT);
+            if (g.cl < 0) {
+                ok = true;
+            } else if (ct && g.cl - FTILEBIT < 32) {
+                f.mask |= 1u << (g.cl - FTILEBIT);
+                ok = true;
+            } else if (!ct) {
+                f.cond = g.cl;
+                ok = true;
+            }
+        } else if (!tt && ct && g.cl - FTILEBIT < 32) {
+            f.mask = 1u << (g.cl - FTILEBIT);
+            f.cond = g.tl;
+            ok = true;
+        }
+        if (ok) {
+            t_tph->push_back(f);
+            t_phase = true;
+            t_phase_sign = false;
+            return;
+        }
+    }
     o("{ const bool b = %s;\n", pbit(g.tl).c_str());
     if (g.cl >= 0) o("if (%s) {\n", pbit(g.cl).c_str());
     // branch-free (a predicated update of ph is miscompiled by ptxas -O1+ in
@@ -1529,7 +1645,11 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             t_pdm = 0;
             o("d2 ph = mk(1.0, 0.0);\n");
             for (int k = 0; k < NS(); ++k) o("d2 hs%d = mk(1.0, 0.0);\n", k);
+            std::vector<TilePhase> tph;
+            t_tph = &tph;
             for (int q = G.first; q < G.first + G.count; ++q) emit_gate_fast(o, P.gates[q], code, F);
+            flush_tile_phases(o);  // (ph is only read below, at the group's end)
+            t_tph = nullptr;
             const double mag = cabsh(F);
             const bool applyF = gi == P.ngroups - 1 && (last || mag < 0x1p-200 || mag > 0x1p200) &&
                                 !(F.x == 1.0 && F.y == 0.0);
