@@ -872,6 +872,15 @@ struct TilePhase {
     double2 d;
 };
 thread_local std::vector<TilePhase> *t_tph = nullptr;
+// the same for per-slot phases hs<s> (a controlled phase between slot s and a
+// qubit outside the tile): factor f1 where the tile bit is set, f0 where not
+struct SlotTilePhase {
+    int bit;
+    double2 f1, f0;
+};
+thread_local std::vector<SlotTilePhase> *t_shs = nullptr;  // [slot]
+
+void materialize_slot_tile(Out &o, int s);
 
 bool tph_on() {
     static const bool on = [] {
@@ -931,6 +940,44 @@ void flush_tile_phases(Out &o) {
         }
     }
     t_tph->clear();
+}
+
+// multiply slot s's collected tile-uniform factors into hs<s> (before hs<s> is read)
+void materialize_slot_tile(Out &o, int s) {
+    if (!t_shs || t_shs[s].empty()) return;
+    std::vector<SlotTilePhase> &fs = t_shs[s];
+    std::vector<char> done(fs.size(), 0);
+    for (size_t i = 0; i < fs.size(); ++i) {
+        if (done[i]) continue;
+        uint32_t bits = 0;
+        std::vector<size_t> in;
+        for (size_t j = i; j < fs.size(); ++j) {
+            if (done[j]) continue;
+            if (__builtin_popcount(bits | (1u << fs[j].bit)) > 5) continue;
+            bits |= 1u << fs[j].bit;
+            in.push_back(j);
+            done[j] = 1;
+        }
+        std::vector<int> pos;
+        for (int b = 0; b < 32; ++b)
+            if ((bits >> b) & 1) pos.push_back(b);
+        const int nb = (int)pos.size();
+        std::vector<double> tab;
+        for (int ix = 0; ix < (1 << nb); ++ix) {
+            uint32_t set = 0;
+            for (int k = 0; k < nb; ++k)
+                if ((ix >> k) & 1) set |= 1u << pos[k];
+            double2 v = make_double2(1.0, 0.0);
+            for (size_t j : in) v = cmulh(v, ((set >> fs[j].bit) & 1) ? fs[j].f1 : fs[j].f0);
+            tab.push_back(v.x);
+            tab.push_back(v.y);
+        }
+        const int start = pool_block(tab);
+        o("{ const unsigned ix = 0u");
+        for (int k = 0; k < nb; ++k) o(" | (((unsigned)(tix >> %d) & 1u) << %d)", pos[k], k);
+        o("; hs%d = cm(kc[%d + 2 * ix], kc[%d + 2 * ix], hs%d); }\n", s, start, start + 1, s);
+    }
+    fs.clear();
 }
 
 void emit_phase(Out &o, const FGate &g) {
@@ -1023,6 +1070,7 @@ bool slot_phase_on() { return true; }
 
 void slot_phase_flush(Out &o, int s) {
     if (!((t_hs >> s) & 1) || !t_code) return;
+    materialize_slot_tile(o, s);
     for (int i = 0; i < NR(); ++i) {
         if (!((i >> s) & 1)) continue;
         double k1 = 1.0, k2 = 1.0;
@@ -1060,6 +1108,14 @@ bool slot_phase_take(Out &o, const FGate &g) {
         return false;
     }
     if (t_pend && t_pend[s]) return false;  // (the pending-swap paths handle it)
+    {
+        const int pb = (tpos < FTPOS_THREAD) ? g.cl : g.tl;  // the predicate's bit
+        if (t_shs && t_pool && tph_on() && pb >= FTILEBIT && pb - FTILEBIT < 32) {
+            t_shs[s].push_back(SlotTilePhase{pb - FTILEBIT, f1, f0});
+            t_hs |= 1u << s;
+            return true;
+        }
+    }
     o("{ const bool b = %s; hs%d = cm(b ? %s : %s, b ? %s : %s, hs%d); }\n", pred.c_str(), s, lit(f1.x).c_str(),
       lit(f0.x).c_str(), lit(f1.y).c_str(), lit(f0.y).c_str(), s);
     t_hs |= 1u << s;
@@ -1646,10 +1702,14 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             o("d2 ph = mk(1.0, 0.0);\n");
             for (int k = 0; k < NS(); ++k) o("d2 hs%d = mk(1.0, 0.0);\n", k);
             std::vector<TilePhase> tph;
+            std::vector<SlotTilePhase> shs[FSMAX];
             t_tph = &tph;
+            t_shs = shs;
             for (int q = G.first; q < G.first + G.count; ++q) emit_gate_fast(o, P.gates[q], code, F);
             flush_tile_phases(o);  // (ph is only read below, at the group's end)
+            for (int k = 0; k < NS(); ++k) materialize_slot_tile(o, k);  // (hs<k> too)
             t_tph = nullptr;
+            t_shs = nullptr;
             const double mag = cabsh(F);
             const bool applyF = gi == P.ngroups - 1 && (last || mag < 0x1p-200 || mag > 0x1p200) &&
                                 !(F.x == 1.0 && F.y == 0.0);
