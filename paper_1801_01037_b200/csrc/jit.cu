@@ -882,45 +882,6 @@ thread_local std::vector<SlotTilePhase> *t_shs = nullptr;  // [slot]
 
 void materialize_slot_tile(Out &o, int s);
 
-// Thread-only phase factors, hoisted.  A phase factor whose predicate bits are
-// all thread bits has the same value in every tile: the statements that would
-// multiply it into ph / hs<s> once per tile are collected per accumulator and,
-// where the accumulator is next read, emitted ONCE into the kernel's prologue
-// (their product stored in a per-thread shared-memory slot) while the tile
-// loop only multiplies the stored product in.  SVB_JIT_HOIST=0 turns it off.
-constexpr int kMaxPre = 16;                      // slots of 128 x 16 B
-thread_local Out *t_pro = nullptr;               // prologue text (spliced before the tile loop)
-thread_local int t_npre = 0;
-thread_local std::vector<std::string> *t_tid = nullptr;  // [0]: ph, [1 + s]: hs<s>; statements on "pq"
-
-bool hoist_on() {
-    static const bool on = [] {
-        const char *e = getenv("SVB_JIT_HOIST");
-        return !e || atoi(e) != 0;
-    }();
-    return on;
-}
-
-// emit the collected thread-only factors of accumulator `acc` (index k)
-void materialize_tid(Out &o, int k, const char *acc) {
-    if (!t_tid || t_tid[k].empty()) return;
-    std::vector<std::string> &st = t_tid[k];
-    if (t_pro && st.size() >= 2 && t_npre < kMaxPre) {
-        Out &p = *t_pro;
-        p("{ d2 pq = mk(1.0, 0.0);\n");
-        for (const std::string &x : st) p.s += x;
-        p("spre[%d][tid] = pq; }\n", t_npre);
-        o("{ const d2 pq = spre[%d][tid]; %s = cm(pq.x, pq.y, %s); }\n", t_npre, acc, acc);
-        ++t_npre;
-    } else {
-        for (std::string x : st) {  // in place, on the accumulator itself
-            for (size_t at; (at = x.find("pq")) != std::string::npos;) x.replace(at, 2, acc);
-            o.s += x;
-        }
-    }
-    st.clear();
-}
-
 bool tph_on() {
     static const bool on = [] {
         const char *e = getenv("SVB_JIT_TPH");
@@ -930,7 +891,6 @@ bool tph_on() {
 }
 
 void flush_tile_phases(Out &o) {
-    materialize_tid(o, 0, "ph");
     if (!t_tph || t_tph->empty()) return;
     std::vector<int> conds;
     for (const TilePhase &f : *t_tph)
@@ -984,11 +944,6 @@ void flush_tile_phases(Out &o) {
 
 // multiply slot s's collected tile-uniform factors into hs<s> (before hs<s> is read)
 void materialize_slot_tile(Out &o, int s) {
-    {
-        char acc[8];
-        snprintf(acc, sizeof acc, "hs%d", s);
-        materialize_tid(o, 1 + s, acc);
-    }
     if (!t_shs || t_shs[s].empty()) return;
     std::vector<SlotTilePhase> &fs = t_shs[s];
     std::vector<char> done(fs.size(), 0);
@@ -1058,22 +1013,6 @@ void emit_phase(Out &o, const FGate &g) {
             t_phase_sign = false;
             return;
         }
-    }
-    if (t_tid && hoist_on() && g.tl < FTILEBIT && g.cl < FTILEBIT) {
-        Out q;
-        q("{ const bool b = %s;\n", pbit(g.tl).c_str());
-        if (g.cl >= 0) q("if (%s) {\n", pbit(g.cl).c_str());
-        if (one0)
-            q("pq = cm(b ? %s : 1.0, b ? %s : 0.0, pq);\n", lit(d1.x).c_str(), lit(d1.y).c_str());
-        else
-            q("pq = cm(b ? %s : %s, b ? %s : %s, pq);\n", lit(d1.x).c_str(), lit(d0.x).c_str(), lit(d1.y).c_str(),
-              lit(d0.y).c_str());
-        if (g.cl >= 0) q("}\n");
-        q("}\n");
-        t_tid[0].push_back(q.s);
-        t_phase = true;
-        t_phase_sign = false;
-        return;
     }
     o("{ const bool b = %s;\n", pbit(g.tl).c_str());
     if (g.cl >= 0) o("if (%s) {\n", pbit(g.cl).c_str());
@@ -1173,17 +1112,6 @@ bool slot_phase_take(Out &o, const FGate &g) {
         const int pb = (tpos < FTPOS_THREAD) ? g.cl : g.tl;  // the predicate's bit
         if (t_shs && t_pool && tph_on() && pb >= FTILEBIT && pb - FTILEBIT < 32) {
             t_shs[s].push_back(SlotTilePhase{pb - FTILEBIT, f1, f0});
-            t_hs |= 1u << s;
-            return true;
-        }
-    }
-    {
-        const int pb = (tpos < FTPOS_THREAD) ? g.cl : g.tl;
-        if (t_tid && hoist_on() && pb >= 0 && pb < FTILEBIT) {
-            Out q;
-            q("{ const bool b = %s; pq = cm(b ? %s : %s, b ? %s : %s, pq); }\n", pred.c_str(), lit(f1.x).c_str(),
-              lit(f0.x).c_str(), lit(f1.y).c_str(), lit(f0.y).c_str());
-            t_tid[1 + s].push_back(q.s);
             t_hs |= 1u << s;
             return true;
         }
@@ -1493,8 +1421,6 @@ int store_hazard(const FGroup &G, int threads, int tbits) {
 
 // variant: 0 exact, 1 FMA, 2 FMA + factor extraction (F: the global factor
 // carried in and out; last: the circuit's last fused pass, which applies F)
-static bool fast_variant_hoist(int variant) { return variant == 2 && hoist_on(); }
-
 std::string jit_body(const FPass &P, int variant, double2 &F, bool last);
 
 std::string jit_source(const FPass &P, int variant, double2 &F, bool last) {
@@ -1517,10 +1443,6 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
     const bool fma = variant >= 1, fast = variant == 2;
     const int mode = jit_pass_mode(P);
     Out o;
-    Out pro;  // thread-only phase products, computed once before the tile loop (materialize_tid)
-    size_t pro_at = std::string::npos;
-    t_pro = fast_variant_hoist(variant) ? &pro : nullptr;
-    t_npre = 0;
     const int FTILE = 1 << P.fm, FTHREADS = jit_wg_threads(P), FTBITS = P.fm - P.fs;
     const bool ring = mode == 3;
     const bool split = mode == 4;
@@ -1678,7 +1600,6 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
           "if (t < ntiles) { fill((unsigned)bi << 16, a + tbase(t)); mb_arrive_cp(&mbar[bi]); } };\n");
         o("if (threadIdx.x < 3) mb_init(&mbar[threadIdx.x], %d);\n__syncthreads();\n", FTHREADS);
         o("if (wg == 0) { fill3(0, 0); fill3(2, 2); } else { fill3(1, 1); }\n");
-        pro_at = o.s.size();
         o("for (i64 j = wg;; j += 2) {\n"
           "const i64 tix = blockIdx.x + j * gridDim.x;\n"
           "if (tix >= ntiles) break;\n"
@@ -1691,7 +1612,6 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             o("if (blockIdx.x < ntiles) { fillA(a + tbase(blockIdx.x)); fillB(a + tbase(blockIdx.x)); }\n");
         else if (mode != 0)
             o("if (blockIdx.x < ntiles) fill(reinterpret_cast<unsigned char *>(dsm), a + tbase(blockIdx.x));\n");
-        pro_at = o.s.size();
         o("int it = 0;\nfor (i64 tix = blockIdx.x; tix < ntiles; tix += gridDim.x, ++it) {\n");
         o("d2 *const pa = a + tbase(tix);\n");
     }
@@ -1783,16 +1703,13 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
             for (int k = 0; k < NS(); ++k) o("d2 hs%d = mk(1.0, 0.0);\n", k);
             std::vector<TilePhase> tph;
             std::vector<SlotTilePhase> shs[FSMAX];
-            std::vector<std::string> tidf[1 + FSMAX];
             t_tph = &tph;
             t_shs = shs;
-            t_tid = tidf;
             for (int q = G.first; q < G.first + G.count; ++q) emit_gate_fast(o, P.gates[q], code, F);
             flush_tile_phases(o);  // (ph is only read below, at the group's end)
             for (int k = 0; k < NS(); ++k) materialize_slot_tile(o, k);  // (hs<k> too)
             t_tph = nullptr;
             t_shs = nullptr;
-            t_tid = nullptr;
             const double mag = cabsh(F);
             const bool applyF = gi == P.ngroups - 1 && (last || mag < 0x1p-200 || mag > 0x1p200) &&
                                 !(F.x == 1.0 && F.y == 0.0);
@@ -1932,12 +1849,6 @@ std::string jit_body(const FPass &P, int variant, double2 &F, bool last) {
     o("}\n");
     if (mode != 0 && !ring) o.s += wait_all;
     o("}\n");
-    t_pro = nullptr;
-    if (t_npre > 0 && pro_at != std::string::npos) {
-        char decl[96];
-        snprintf(decl, sizeof decl, "__shared__ d2 spre[%d][%d];\n", t_npre, FTHREADS);
-        o.s.insert(pro_at, std::string(decl) + pro.s);
-    }
     return o.s;
 }
 

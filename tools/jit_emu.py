@@ -117,7 +117,6 @@ def translate(src: str):
     nthreads = int(m.group(1))
     body = body.replace(m.group(0), "static void kpass_body(")
     body = body.replace("__constant__ ", "")
-    body = body.replace("__shared__ d2 spre", "static d2 spre")  # hoisted thread-only phase products (per-thread slots)
     body = re.sub(r"extern __shared__ d2 dsm\[\];", "d2 *dsm = g_smem;", body)
     body = re.sub(r"__shared__ alignas\(16\) d2 dsm\[\d+\];", "d2 *dsm = g_smem;", body)
     body = body.replace("threadIdx.x", "t_tid").replace("blockIdx.x", "g_bid").replace("gridDim.x", "g_grid")
